@@ -1,0 +1,161 @@
+/*
+ * sla2_capi.h -- C ABI of libsla2_b200.so, the B200-native (sm_100a) SLA2 forward pass.
+ *
+ * This is the drop-in boundary for the reference's hot path, the header-only C++ library in
+ * /root/reference/proj/include/sla2. Each entry point below replaces one reference
+ * interface (cited); the C++ shim include/sla2_b200/sla2.hpp re-exposes the reference's own
+ * names and types (sla2::block_scores, sla2::hard_topk, sla2::sla2_forward_blockwise, ...)
+ * on top of these calls, and INTEGRATION.md shows the bindings a maintainer adds.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Tensors are contiguous row-major
+ *     [B, H, N, d] (q, k, v, out) -- each (b, h) slice is exactly one reference
+ *     sla2::Matrix<T> (matrix.hpp:18-23). Per-head router state is [H, d, d] (proj_q,
+ *     proj_k, the RouterParams<float> of model.hpp:38,94) and [H, tm] (rho, the MixRatio
+ *     logits of model.hpp:39,95), both float32.
+ *   - "Device" entry points take device pointers, a caller-owned device workspace
+ *     (size from sla2_workspace_size) and a cudaStream_t passed as void*; they never
+ *     allocate and are stream-ordered. "_host" entry points take host pointers and do the
+ *     copies themselves (the reference's value-semantics call shape).
+ *   - Errors: the return code is the reference's exception class (common.hpp:13-29):
+ *     SLA2_SHAPE_ERROR <-> sla2::shape_error, SLA2_NUMERIC_ERROR <-> sla2::numeric_error,
+ *     SLA2_CONTRACT_ERROR <-> sla2::contract_error; SLA2_CUDA_ERROR for a failed launch /
+ *     missing sm_100a device. All validation runs on the host before any launch, like the
+ *     reference's validation prologues. sla2_last_error() gives the message (thread-local).
+ *   - No CPU fallback exists: without an sm_100a device every compute call returns
+ *     SLA2_CUDA_ERROR.
+ */
+#ifndef SLA2_CAPI_H
+#define SLA2_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SLA2_OK = 0,
+    SLA2_SHAPE_ERROR = 1,    /* sla2::shape_error    */
+    SLA2_NUMERIC_ERROR = 2,  /* sla2::numeric_error  */
+    SLA2_CONTRACT_ERROR = 3, /* sla2::contract_error */
+    SLA2_CUDA_ERROR = 4
+} sla2_status;
+
+typedef enum { SLA2_F32 = 0, SLA2_BF16 = 1 } sla2_dtype;
+
+/* QuantConfig (quant.hpp:15-19): NONE = nullptr, INT8 = {bits 8, qk_product, pv_product}. */
+typedef enum { SLA2_QUANT_NONE = 0, SLA2_QUANT_INT8 = 1 } sla2_quant;
+
+typedef struct {
+    int64_t B, H, N, d; /* batch, heads, tokens (N % bq == N % bk == 0), head dim */
+    int64_t bq, bk;     /* block sizes (AttentionInputs::bq/bk, attention.hpp:27-28) */
+    double k_percent;   /* router budget, hard_topk (router.hpp:106-125); in (0, 100] */
+    int32_t dtype;      /* sla2_dtype of q, k, v, out */
+    int32_t quant;      /* sla2_quant */
+    int32_t smooth;     /* smooth_k on (the reference default `smooth = true`) */
+    int32_t exact_mu;   /* 1: K column mean in the reference's serial order (bit-exact mask);
+                           0: tree-reduced mean (faster, mask may differ at fp32 ties) */
+    float tau;          /* RouterParams::tau, validated > 0 (router.hpp:32); unused by hard top-k */
+    int32_t reserved[3];
+} sla2_fwd_params;
+
+/* Optional per-branch outputs (SLA2ForwardSaved, attention.hpp:345-358), fp32, device. */
+typedef struct {
+    float* o_s;   /* [B,H,N,d] sparse-branch output O_s, or NULL */
+    float* o_l;   /* [B,H,N,d] linear-branch output O_l, or NULL (rows of full mask rows = 0) */
+    float* big_l; /* [B,H,N] logsumexp L = m + log l, or NULL */
+} sla2_fwd_saved;
+
+/* Fills p with the reference defaults for one (B, H, N, d) problem: bq = 128, bk = 64
+ * (PAPER.md:476), k_percent = 3, bf16, no quant, smooth = 1, exact_mu = 1, tau = 0.1. */
+void sla2_default_params(sla2_fwd_params* p, int64_t B, int64_t H, int64_t N, int64_t d);
+
+/* topk_budget (router.hpp:36-40): kappa = min(tn, max(1, llround(k% / 100 * tn))). */
+int64_t sla2_topk_budget(double k_percent, int64_t tn);
+
+/* Validates p exactly as the reference's prologues would (router.hpp:27-33,90-94,108-110;
+ * attention.hpp:36-43,427-447; matrix.hpp:175-179) plus this build's kernel limits. */
+sla2_status sla2_check_params(const sla2_fwd_params* p);
+
+/* Bytes of device workspace sla2_forward / sla2_router / sla2_sparse_fwd need for p. */
+size_t sla2_workspace_size(const sla2_fwd_params* p);
+
+/*
+ * Full forward, replacing Tape::sla2_attention's composition (tape.hpp:263-272):
+ *   K~ = smooth_k(K)                          (quant.hpp:88-96)
+ *   pc = block_scores(Q, K~, router, bq, bk)  (router.hpp:87-102)
+ *   M  = hard_topk(pc, k_percent)             (router.hpp:106-125)
+ *   out = sla2_forward_blockwise(Q, K, V, M, rho, quant, smooth)  (attention.hpp:423-560)
+ * mask_out [B,H,tm,tn] u8 (BlockMask::bits) and kv_idx_out [B,H,tm,kappa] int32 (each
+ * row's kept key blocks, ascending) are optional (NULL = not written).
+ */
+sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
+                         const float* proj_q, const float* proj_k, const float* rho, void* out,
+                         uint8_t* mask_out, int32_t* kv_idx_out, const sla2_fwd_saved* saved,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Router only: smooth_k + block_scores + hard_topk, bit-exact with the reference.
+ * pc_out [B,H,tm,tn] fp32 (the row-softmaxed block scores) may be NULL.
+ */
+sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, const float* proj_q,
+                        const float* proj_k, float* pc_out, uint8_t* mask_out, int32_t* kv_idx_out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * smooth_k (quant.hpp:88-96) on device: mean_out [B,H,d] fp32 and, if ktilde_out is not NULL,
+ * K~ = K - mean as fp32 [B,H,N,d].
+ */
+sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_out, float* ktilde_out,
+                          void* stream);
+
+/*
+ * hard_topk (router.hpp:106-125) on a caller-given score matrix pc [B,H,tm,tn] fp32: per row
+ * the kappa largest entries, ties to the lowest column, as mask bits and ascending index lists.
+ */
+sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* mask_out,
+                           int32_t* kv_idx_out, void* stream);
+
+/*
+ * sla2_forward_blockwise (attention.hpp:423-560) with a caller-given BlockMask (device
+ * [B,H,tm,tn] u8, any number of kept blocks per row, e.g. BlockMask::ones). A row that keeps
+ * no block returns SLA2_SHAPE_ERROR like the reference (attention.hpp:442-447); checking it
+ * costs one device->host read, so this entry point synchronizes `stream` once.
+ * p->k_percent is not used.
+ */
+sla2_status sla2_sparse_fwd(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
+                            const float* rho, const uint8_t* mask, void* out, const sla2_fwd_saved* saved,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Dense softmax attention softmax(QK^T / sqrt d) V (full_attention, attention.hpp:71-75): the
+ * same tcgen05 kernel visiting every key block -- the "dense sm_100a attention of the same
+ * build" the north-star compares against. bf16 only.
+ */
+sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* k, const void* v, void* out,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Host-buffer forward: the reference's call shape (inputs and outputs in host memory).
+ * Copies q/k/v/proj/rho host->device, runs sla2_forward on an internal stream with an
+ * internally cached workspace, copies out (and the optional mask) back, synchronizes.
+ */
+sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
+                              const float* proj_q, const float* proj_k, const float* rho, void* out,
+                              uint8_t* mask_out);
+
+/* Message of the last error on this thread ("" if none). */
+const char* sla2_last_error(void);
+
+/* Number of kernel launches the last sla2_* call on this thread enqueued (bench evidence). */
+int32_t sla2_last_launch_count(void);
+
+/* "sla2_b200 <version> sm_100a" */
+const char* sla2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLA2_CAPI_H */

@@ -1,0 +1,343 @@
+"""paper_2602_12675_b200 -- B200-native (sm_100a) SLA2 forward pass behind the reference's API.
+
+Python mirror of the reference's C++ operator interface for the SLA2 hot path
+(/root/reference/proj/include/sla2), calling libsla2_b200.so through its C ABI
+(include/sla2_capi.h). Names, argument meaning and error classes follow the reference:
+
+  smooth_k(k)                                   quant.hpp:88-96
+  block_scores(q, k, proj_q, proj_k, bq, bk)    router.hpp:87-102
+  hard_topk(pc, k_percent)                      router.hpp:106-125
+  topk_budget(k_percent, tn)                    router.hpp:36-40
+  sla2_forward_blockwise(q, k, v, mask, rho)    attention.hpp:423-560
+  sla2_attention(q, k, v, rho, proj, ...)       tape.hpp:263-272 (router + forward)
+  full_attention(q, k, v)                       attention.hpp:71-75 (dense tcgen05 baseline)
+
+Tensors are torch CUDA tensors shaped [B, H, N, d] (each [b, h] slice is one reference
+Matrix), bf16 or fp32; per-head router state is proj [H, d, d] fp32 and rho [H, tm] fp32.
+Errors raise ShapeError / NumericError / ContractError (sla2::shape_error, numeric_error,
+contract_error of common.hpp:13-29) or CudaError. There is no CPU fallback: without the built
+library or an sm_100a GPU every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+__all__ = [
+    "ShapeError", "NumericError", "ContractError", "CudaError", "Sla2Error",
+    "lib", "library_path", "topk_budget", "smooth_k", "block_scores", "hard_topk",
+    "sla2_forward_blockwise", "sla2_attention", "full_attention", "router", "forward",
+    "FwdParams", "workspace_bytes", "last_launch_count",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libsla2_b200.so")
+
+
+class Sla2Error(RuntimeError):
+    pass
+
+
+class ShapeError(Sla2Error, ValueError):
+    """sla2::shape_error (common.hpp:14-17)."""
+
+
+class NumericError(Sla2Error):
+    """sla2::numeric_error (common.hpp:20-23)."""
+
+
+class ContractError(Sla2Error):
+    """sla2::contract_error (common.hpp:26-29)."""
+
+
+class CudaError(Sla2Error):
+    """Launch failure or no sm_100a device (no CPU fallback exists)."""
+
+
+class _Params(C.Structure):
+    _fields_ = [("B", C.c_int64), ("H", C.c_int64), ("N", C.c_int64), ("d", C.c_int64),
+                ("bq", C.c_int64), ("bk", C.c_int64), ("k_percent", C.c_double),
+                ("dtype", C.c_int32), ("quant", C.c_int32), ("smooth", C.c_int32),
+                ("exact_mu", C.c_int32), ("tau", C.c_float), ("reserved", C.c_int32 * 3)]
+
+
+class _Saved(C.Structure):
+    _fields_ = [("o_s", C.c_void_p), ("o_l", C.c_void_p), ("big_l", C.c_void_p)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _SO
+
+
+def lib():
+    """Load libsla2_b200.so (built by __graft_entry__.build() / make). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise CudaError(f"{_SO} is not built (run python -c 'import __graft_entry__ as g; g.build()');"
+                        " there is no CPU fallback")
+    L = C.CDLL(_SO)
+    vp, sz, P = C.c_void_p, C.c_size_t, C.POINTER(_Params)
+    sig = {
+        "sla2_default_params": ([P, C.c_int64, C.c_int64, C.c_int64, C.c_int64], None),
+        "sla2_topk_budget": ([C.c_double, C.c_int64], C.c_int64),
+        "sla2_check_params": ([P], C.c_int),
+        "sla2_workspace_size": ([P], sz),
+        "sla2_forward": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(_Saved), vp, sz, vp], C.c_int),
+        "sla2_router": ([P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
+        "sla2_smooth_k": ([P, vp, vp, vp, vp], C.c_int),
+        "sla2_hard_topk": ([P, vp, vp, vp, vp], C.c_int),
+        "sla2_sparse_fwd": ([P, vp, vp, vp, vp, vp, vp, C.POINTER(_Saved), vp, sz, vp], C.c_int),
+        "sla2_dense_fwd": ([P, vp, vp, vp, vp, vp, sz, vp], C.c_int),
+        "sla2_forward_host": ([P, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "sla2_last_error": ([], C.c_char_p),
+        "sla2_last_launch_count": ([], C.c_int32),
+        "sla2_version": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _raise(rc: int):
+    if rc == 0:
+        return
+    msg = lib().sla2_last_error().decode()
+    cls = {1: ShapeError, 2: NumericError, 3: ContractError}.get(rc, CudaError)
+    raise cls(msg)
+
+
+def last_launch_count() -> int:
+    """Kernel launches enqueued by the last call on this thread."""
+    return int(lib().sla2_last_launch_count())
+
+
+def topk_budget(k_percent: float, tn: int) -> int:
+    """router.hpp:36-40: kappa = min(tn, max(1, llround(k%/100 * tn)))."""
+    return int(lib().sla2_topk_budget(float(k_percent), int(tn)))
+
+
+@dataclass
+class FwdParams:
+    B: int
+    H: int
+    N: int
+    d: int
+    bq: int = 128
+    bk: int = 64
+    k_percent: float = 3.0
+    bf16: bool = True
+    quant: bool = False
+    smooth: bool = True
+    exact_mu: bool = True
+    tau: float = 0.1
+
+    def c(self) -> _Params:
+        p = _Params()
+        p.B, p.H, p.N, p.d, p.bq, p.bk = self.B, self.H, self.N, self.d, self.bq, self.bk
+        p.k_percent = float(self.k_percent)
+        p.dtype = 1 if self.bf16 else 0
+        p.quant = 1 if self.quant else 0
+        p.smooth = int(bool(self.smooth))
+        p.exact_mu = int(bool(self.exact_mu))
+        p.tau = float(self.tau)
+        return p
+
+    @property
+    def tm(self):
+        return self.N // self.bq
+
+    @property
+    def tn(self):
+        return self.N // self.bk
+
+    @property
+    def kappa(self):
+        return topk_budget(self.k_percent, self.tn)
+
+
+def workspace_bytes(p: FwdParams) -> int:
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    return int(lib().sla2_workspace_size(C.byref(cp)))
+
+
+_ws_cache = {}
+
+
+def _workspace(p: FwdParams, device):
+    import torch
+    n = workspace_bytes(p)
+    key = (device.index if device.index is not None else 0)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(dev):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu, tau=0.1):
+    import torch
+    if q.dim() != 4:
+        raise ShapeError("expected [B, H, N, d] tensors")
+    if q.dtype not in (torch.bfloat16, torch.float32):
+        raise ContractError("q/k/v must be bfloat16 or float32")
+    B, H, N, d = q.shape
+    return FwdParams(B, H, N, d, bq, bk, k_percent, q.dtype == torch.bfloat16, quant, smooth, exact_mu, tau)
+
+
+def _check_like(ref, *ts):
+    for t in ts:
+        if t.shape != ref.shape or t.dtype != ref.dtype or t.device != ref.device:
+            raise ShapeError("AttentionInputs: q, k, v must share N x d")  # attention.hpp:36-38
+        if not t.is_contiguous():
+            raise ContractError("tensors must be contiguous")
+
+
+def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant=False, smooth=True,
+            exact_mu=True, return_mask=False, return_idx=False, saved=False, out=None):
+    """Router + blockwise forward (tape.hpp:263-272). Returns out or a tuple with
+    (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested."""
+    import torch
+    _check_like(q, k, v)
+    p = _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu)
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    dev = q.device
+    out = torch.empty_like(q) if out is None else out
+    mask = torch.empty((p.B, p.H, p.tm, p.tn), dtype=torch.uint8, device=dev) if return_mask else None
+    idx = torch.empty((p.B, p.H, p.tm, p.kappa), dtype=torch.int32, device=dev) if return_idx else None
+    sv = None
+    svs = None
+    if saved:
+        svs = {"o_s": torch.empty(q.shape, dtype=torch.float32, device=dev),
+               "o_l": torch.empty(q.shape, dtype=torch.float32, device=dev),
+               "big_l": torch.empty(q.shape[:3], dtype=torch.float32, device=dev)}
+        sv = _Saved(svs["o_s"].data_ptr(), svs["o_l"].data_ptr(), svs["big_l"].data_ptr())
+    ws = _workspace(p, dev)
+    rc = lib().sla2_forward(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(proj_q.contiguous()),
+                            _ptr(proj_k.contiguous()), _ptr(rho.contiguous()), _ptr(out), _ptr(mask), _ptr(idx),
+                            C.byref(sv) if sv is not None else None, _ptr(ws), ws.numel(), _stream(dev))
+    _raise(rc)
+    res = [out]
+    if return_mask:
+        res.append(mask)
+    if return_idx:
+        res.append(idx)
+    if saved:
+        res.append(svs)
+    return res[0] if len(res) == 1 else tuple(res)
+
+
+def router(q, k, proj_q, proj_k, *, k_percent=3.0, bq=128, bk=64, smooth=True, exact_mu=True, tau=0.1,
+           return_pc=True):
+    """smooth_k + block_scores + hard_topk on device -> (pc fp32, mask u8, idx i32)."""
+    import torch
+    _check_like(q, k)
+    p = _params_from(q, bq, bk, k_percent, False, smooth, exact_mu, tau)
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    dev = q.device
+    pc = torch.empty((p.B, p.H, p.tm, p.tn), dtype=torch.float32, device=dev) if return_pc else None
+    mask = torch.empty((p.B, p.H, p.tm, p.tn), dtype=torch.uint8, device=dev)
+    idx = torch.empty((p.B, p.H, p.tm, p.kappa), dtype=torch.int32, device=dev)
+    ws = _workspace(p, dev)
+    _raise(lib().sla2_router(C.byref(cp), _ptr(q), _ptr(k), _ptr(proj_q.contiguous()), _ptr(proj_k.contiguous()),
+                             _ptr(pc), _ptr(mask), _ptr(idx), _ptr(ws), ws.numel(), _stream(dev)))
+    return pc, mask, idx
+
+
+def smooth_k(k):
+    """quant.hpp:88-96 on device: returns (K - mu as fp32, mu [B,H,d] fp32)."""
+    import torch
+    p = _params_from(k, 1, 1, 100.0, False, True, True)
+    cp = p.c()
+    mu = torch.empty((p.B, p.H, p.d), dtype=torch.float32, device=k.device)
+    _raise(lib().sla2_smooth_k(C.byref(cp), _ptr(k.contiguous()), _ptr(mu), None, _stream(k.device)))
+    return k.float() - mu[:, :, None, :], mu
+
+
+def block_scores(q, k, proj_q, proj_k, bq, bk, tau=0.1):
+    """router.hpp:87-102 (k is the already-smoothed K~ as the reference's callers pass it)."""
+    pc, _, _ = router(q, k, proj_q, proj_k, k_percent=100.0, bq=bq, bk=bk, smooth=False, tau=tau)
+    return pc
+
+
+def hard_topk(pc, k_percent):
+    """router.hpp:106-125 on a device score tensor [B,H,tm,tn] -> (mask u8, idx i32, kappa)."""
+    import torch
+    if pc.dim() != 4 or pc.dtype != torch.float32:
+        raise ShapeError("pc must be [B, H, tm, tn] float32")
+    B, H, tm, tn = pc.shape
+    if not (0.0 < k_percent <= 100.0):
+        raise ShapeError("hard_topk: k_percent must be in (0, 100]")
+    # score-matrix geometry through the params struct: rows N/bq = tm, columns N/bk = tn
+    cp = _Params()
+    cp.B, cp.H, cp.N, cp.d, cp.bq, cp.bk = B, H, tm * tn, 1, tn, tm
+    cp.k_percent, cp.dtype, cp.quant, cp.smooth, cp.exact_mu, cp.tau = k_percent, 0, 0, 1, 1, 0.1
+    kappa = topk_budget(k_percent, tn)
+    mask = torch.empty((B, H, tm, tn), dtype=torch.uint8, device=pc.device)
+    idx = torch.empty((B, H, tm, kappa), dtype=torch.int32, device=pc.device)
+    _raise(lib().sla2_hard_topk(C.byref(cp), _ptr(pc.contiguous()), _ptr(mask), _ptr(idx), _stream(pc.device)))
+    return mask, idx, kappa
+
+
+def sla2_forward_blockwise(q, k, v, mask, rho, *, bq=128, bk=64, quant=False, smooth=True, saved=False):
+    """attention.hpp:423-560 with a caller-given BlockMask [B,H,tm,tn] (device u8)."""
+    import torch
+    _check_like(q, k, v)
+    p = _params_from(q, bq, bk, 100.0, quant, smooth, True)
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    if tuple(mask.shape) != (p.B, p.H, p.tm, p.tn):
+        raise ShapeError("sla2_forward_blockwise: mask geometry mismatch")  # attention.hpp:436-438
+    dev = q.device
+    out = torch.empty_like(q)
+    sv = None
+    svs = None
+    if saved:
+        svs = {"o_s": torch.empty(q.shape, dtype=torch.float32, device=dev),
+               "o_l": torch.empty(q.shape, dtype=torch.float32, device=dev),
+               "big_l": torch.empty(q.shape[:3], dtype=torch.float32, device=dev)}
+        sv = _Saved(svs["o_s"].data_ptr(), svs["o_l"].data_ptr(), svs["big_l"].data_ptr())
+    ws = _workspace(p, dev)
+    _raise(lib().sla2_sparse_fwd(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()),
+                                 _ptr(mask.contiguous().to(torch.uint8)), _ptr(out),
+                                 C.byref(sv) if sv is not None else None, _ptr(ws), ws.numel(), _stream(dev)))
+    return (out, svs) if saved else out
+
+
+def sla2_attention(q, k, v, rho, proj_q, proj_k, bq=128, bk=64, k_percent=3.0, quant=False, smooth=True):
+    """Tape::sla2_attention's forward (tape.hpp:263-272)."""
+    return forward(q, k, v, proj_q, proj_k, rho, k_percent=k_percent, bq=bq, bk=bk, quant=quant, smooth=smooth)
+
+
+def full_attention(q, k, v):
+    """softmax(QK^T/sqrt d) V on the same tcgen05 kernel visiting every key block (bf16)."""
+    import torch
+    _check_like(q, k, v)
+    p = _params_from(q, 128, 64, 100.0, False, False, True)
+    cp = p.c()
+    out = torch.empty_like(q)
+    ws = _workspace(p, q.device)
+    _raise(lib().sla2_dense_fwd(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), ws.numel(),
+                                _stream(q.device)))
+    return out

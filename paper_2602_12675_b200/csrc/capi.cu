@@ -1,0 +1,557 @@
+// capi.cu -- the C ABI of libsla2_b200.so (include/sla2_capi.h): host-side validation with
+// the reference's error classes, workspace carving, TMA descriptor creation, and the launch
+// sequence of the forward pass. No compute happens on the host and there is no CPU fallback.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/sla2_capi.h"
+#include "kernels.h"
+
+using namespace sla2dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_launches = 0;
+
+sla2_status fail(sla2_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define SLA2_CUDA_TRY(expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(SLA2_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// ---------------------------------------------------------------- device check
+sla2_status check_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SLA2_CUDA_ERROR, "no CUDA device (libsla2_b200 has no CPU fallback)");
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(SLA2_CUDA_ERROR, "libsla2_b200 is built for sm_100a (B200); device is sm_" +
+                                         std::to_string(major) + std::to_string(minor));
+    return SLA2_OK;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    });
+    return fn;
+}
+
+struct MapKey {
+    const void* ptr;
+    uint64_t rows, cols;
+    uint32_t box_x, box_y, elem;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && box_x == o.box_x && box_y == o.box_y &&
+               elem == o.elem;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        return std::hash<const void*>()(k.ptr) ^ (k.rows * 1315423911u) ^ (k.cols << 7) ^ (k.box_x << 17) ^
+               (k.box_y << 23) ^ k.elem;
+    }
+};
+
+// 2-D row-major [rows][cols] tensor of `elem`-byte elements, box (box_x cols, box_y rows),
+// SWIZZLE_128B. Cached: descriptors are immutable for a given pointer/shape.
+bool make_map(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_x, uint32_t box_y,
+              uint32_t elem) {
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    MapKey key{ptr, rows, cols, box_x, box_y, elem};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *out = it->second;
+            return true;
+        }
+    }
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * elem};
+    cuuint32_t box[2] = {box_x, box_y};
+    cuuint32_t es[2] = {1, 1};
+    const CUtensorMapDataType dt = elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    CUresult r = fn(out, dt, 2, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, *out);
+    return true;
+}
+
+// ---------------------------------------------------------------- geometry + workspace
+struct Geo {
+    int64_t B, H, BH, N, d, bq, bk, tm, tn, kappa;
+    bool bf16, quant;
+    int nchunk;
+};
+
+Geo geometry(const sla2_fwd_params* p) {
+    Geo g{};
+    g.B = p->B;
+    g.H = p->H;
+    g.BH = p->B * p->H;
+    g.N = p->N;
+    g.d = p->d;
+    g.bq = p->bq;
+    g.bk = p->bk;
+    g.tm = p->bq ? p->N / p->bq : 0;
+    g.tn = p->bk ? p->N / p->bk : 0;
+    g.kappa = sla2_topk_budget(p->k_percent, g.tn);
+    g.bf16 = p->dtype == SLA2_BF16;
+    g.quant = p->quant == SLA2_QUANT_INT8;
+    const int per = g.bf16 ? 16 : 0;
+    if (g.bf16) g.nchunk = (int)((g.tn + per - 1) / per);
+    else g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
+    return g;
+}
+
+struct Carver {
+    uint8_t* base;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+struct Workspace {
+    float* mu;
+    double* mu_part;
+    float* qp;
+    float* kp;
+    int32_t* idx;
+    void* phik;
+    float* zblk;
+    float* ztot;
+    float* hpart;
+    float* htot;
+    int8_t *qc, *kc, *vct;
+    float *qs, *ks, *vs;
+    int32_t* cnt;
+    int* flag;
+};
+
+size_t carve(const Geo& g, void* base, Workspace* w) {
+    Carver c{reinterpret_cast<uint8_t*>(base)};
+    Workspace t{};
+    t.mu = c.take<float>(g.BH * g.d);
+    t.mu_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
+    t.qp = c.take<float>(g.BH * g.tm * g.d);
+    t.kp = c.take<float>(g.BH * g.tn * g.d);
+    t.idx = c.take<int32_t>(g.BH * g.tm * std::max<int64_t>(g.kappa, g.tn));
+    t.cnt = c.take<int32_t>(g.BH * g.tm);
+    t.flag = c.take<int>(4);
+    t.phik = c.take<uint8_t>(g.BH * g.N * g.d * (g.bf16 ? 2 : 4));
+    t.zblk = c.take<float>(g.BH * g.tn * g.d);
+    t.ztot = c.take<float>(g.BH * g.d);
+    t.hpart = c.take<float>(g.BH * g.nchunk * g.d * g.d);
+    t.htot = c.take<float>(g.BH * g.d * g.d);
+    if (g.quant) {
+        t.qc = c.take<int8_t>(g.BH * g.N * g.d);
+        t.kc = c.take<int8_t>(g.BH * g.N * g.d);
+        t.vct = c.take<int8_t>(g.BH * g.N * g.d);
+        t.qs = c.take<float>(g.BH * g.tm);
+        t.ks = c.take<float>(g.BH * g.tn);
+        t.vs = c.take<float>(g.BH * g.tn);
+    }
+    if (w) *w = t;
+    return c.off + 256;
+}
+
+float inv_sqrt(int64_t d) {
+    // T(1) / std::sqrt(static_cast<T>(d)) for T = float (router.hpp:100, attention.hpp:377)
+    volatile float fd = (float)d;
+    volatile float s = std::sqrt((float)fd);
+    volatile float r = 1.0f / s;
+    return r;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+const char* sla2_last_error(void) { return g_last_error.c_str(); }
+int32_t sla2_last_launch_count(void) { return g_launches; }
+const char* sla2_version(void) { return "sla2_b200 0.1.0 sm_100a"; }
+
+void sla2_default_params(sla2_fwd_params* p, int64_t B, int64_t H, int64_t N, int64_t d) {
+    std::memset(p, 0, sizeof(*p));
+    p->B = B;
+    p->H = H;
+    p->N = N;
+    p->d = d;
+    p->bq = 128;
+    p->bk = 64;
+    p->k_percent = 3.0;
+    p->dtype = SLA2_BF16;
+    p->quant = SLA2_QUANT_NONE;
+    p->smooth = 1;
+    p->exact_mu = 1;
+    p->tau = 0.1f;
+}
+
+int64_t sla2_topk_budget(double k_percent, int64_t tn) {
+    // router.hpp:36-40
+    const double r = (double)std::llround(k_percent / 100.0 * (double)tn) * 1.0;
+    const int64_t kappa = (int64_t)(r > 1.0 ? r : 1.0);
+    return kappa < tn ? kappa : tn;
+}
+
+sla2_status sla2_check_params(const sla2_fwd_params* p) {
+    g_last_error.clear();
+    if (!p) return fail(SLA2_CONTRACT_ERROR, "params is NULL");
+    if (p->B <= 0 || p->H <= 0 || p->N <= 0 || p->d <= 0)
+        return fail(SLA2_SHAPE_ERROR, "B, H, N, d must be positive");
+    if (p->bq <= 0 || p->bk <= 0 || p->N % p->bq != 0 || p->N % p->bk != 0)
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");  // attention.hpp:39-41
+    if (!(p->k_percent > 0.0 && p->k_percent <= 100.0))
+        return fail(SLA2_SHAPE_ERROR, "hard_topk: k_percent must be in (0, 100]");  // router.hpp:108-110
+    if (!(p->tau > 0.0f)) return fail(SLA2_NUMERIC_ERROR, "RouterParams: tau must be positive");  // router.hpp:32
+    if (p->dtype != SLA2_F32 && p->dtype != SLA2_BF16) return fail(SLA2_CONTRACT_ERROR, "unknown dtype");
+    if (p->quant != SLA2_QUANT_NONE && p->quant != SLA2_QUANT_INT8)
+        return fail(SLA2_CONTRACT_ERROR, "unknown quant mode");
+    if (p->N * p->B * p->H > (int64_t)INT32_MAX)
+        return fail(SLA2_CONTRACT_ERROR, "B*H*N exceeds the 2^31 row limit of the TMA descriptors");
+    if (p->dtype == SLA2_BF16) {
+        if (p->d != 128 || p->bq != 128 || p->bk != 64)
+            return fail(SLA2_CONTRACT_ERROR,
+                        "bf16 tcgen05 kernels are built for d = 128, bq = 128, bk = 64 (PAPER.md:476)");
+    } else {
+        if (p->quant != SLA2_QUANT_NONE)
+            return fail(SLA2_CONTRACT_ERROR, "INT8 QAT mode runs on the bf16 inputs path");
+        if (p->d > 128 || p->bk > 128 || p->bq > 256 || p->bq < 1 || (256 % p->bq) != 0 || 256 / p->bq > 32)
+            return fail(SLA2_CONTRACT_ERROR, "fp32 path: d <= 128, bk <= 128, bq a power of two in [8, 256]");
+        if (sparse_f32_smem_bytes((int)p->d, (int)p->bq, (int)p->bk) > 227 * 1024)
+            return fail(SLA2_CONTRACT_ERROR, "fp32 path: bq*d + 3*bk*d + bq*bk exceeds shared memory");
+    }
+    return SLA2_OK;
+}
+
+size_t sla2_workspace_size(const sla2_fwd_params* p) {
+    if (sla2_check_params(p) != SLA2_OK) return 0;
+    return carve(geometry(p), nullptr, nullptr);
+}
+
+static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g, const Workspace& w, const void* q,
+                                         const void* k, const void* v, const float* rho, const int32_t* idx,
+                                         const int32_t* cnt, int kstride, void* out, const sla2_fwd_saved* saved,
+                                         cudaStream_t st) {
+    const float isd = inv_sqrt(g.d);
+    CUtensorMap mq, mk, mv, mphi;
+    const uint64_t rows = (uint64_t)(g.BH * g.N);
+    if (g.bf16) {
+        if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
+            !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mphi, w.phik, rows, g.d, 64, 64, 2))
+            return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (pointers must be 16-byte aligned)");
+    }
+    LinearLaunch la{};
+    la.k = k;
+    la.v = v;
+    la.bf16 = g.bf16;
+    la.BH = g.BH;
+    la.N = (int)g.N;
+    la.d = (int)g.d;
+    la.bk = (int)g.bk;
+    la.mu = p->smooth ? w.mu : nullptr;
+    la.phik = w.phik;
+    la.zblk = w.zblk;
+    la.ztot = w.ztot;
+    la.hpart = w.hpart;
+    la.htot = w.htot;
+    la.nchunk = g.nchunk;
+    la.tm_phik = &mphi;
+    la.tm_v = &mv;
+    SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+
+    SparseLaunch sa{};
+    sa.B = g.B;
+    sa.H = g.H;
+    sa.N = (int)g.N;
+    sa.d = (int)g.d;
+    sa.bq = (int)g.bq;
+    sa.bk = (int)g.bk;
+    sa.tm = (int)g.tm;
+    sa.tn = (int)g.tn;
+    sa.kv_idx = idx;
+    sa.kv_cnt = cnt;
+    sa.kstride = kstride;
+    sa.kappa = (int)g.kappa;
+    sa.rho = rho;
+    sa.htot = w.htot;
+    sa.ztot = w.ztot;
+    sa.zblk = w.zblk;
+    sa.mu = w.mu;
+    sa.smooth = p->smooth;
+    sa.dense = 0;
+    sa.inv_sqrt_d = isd;
+    sa.out = out;
+    sa.o_s = saved ? saved->o_s : nullptr;
+    sa.o_l = saved ? saved->o_l : nullptr;
+    sa.big_l = saved ? saved->big_l : nullptr;
+    sa.q = (const float*)q;
+    sa.k = (const float*)k;
+    sa.v = (const float*)v;
+    sa.phik = (const float*)w.phik;
+    if (g.bf16) {
+        sa.tm_q = &mq;
+        sa.tm_k = &mk;
+        sa.tm_v = &mv;
+        sa.tm_phik = &mphi;
+        if (g.quant) return fail(SLA2_CONTRACT_ERROR, "INT8 QAT sparse kernel not available in this build");
+        SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
+    } else {
+        SLA2_CUDA_TRY(launch_sparse_f32(sa, st, &g_launches));
+    }
+    return SLA2_OK;
+}
+
+sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, const float* proj_q,
+                        const float* proj_k, float* pc_out, uint8_t* mask_out, int32_t* kv_idx_out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    const Geo g = geometry(p);
+    if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
+    if (!q || !k || !proj_q || !proj_k) return fail(SLA2_CONTRACT_ERROR, "NULL input pointer");
+    Workspace w;
+    carve(g, workspace, &w);
+    RouterLaunch ra{};
+    ra.q = q;
+    ra.k = k;
+    ra.bf16 = g.bf16;
+    ra.B = g.B;
+    ra.H = g.H;
+    ra.N = (int)g.N;
+    ra.d = (int)g.d;
+    ra.bq = (int)g.bq;
+    ra.bk = (int)g.bk;
+    ra.kappa = (int)g.kappa;
+    ra.smooth = p->smooth;
+    ra.exact_mu = p->exact_mu;
+    ra.inv_sqrt_d = inv_sqrt(g.d);
+    ra.proj_q = proj_q;
+    ra.proj_k = proj_k;
+    ra.mu_out = w.mu;
+    ra.mu_part = w.mu_part;
+    ra.qp = w.qp;
+    ra.kp = w.kp;
+    ra.pc_out = pc_out;
+    ra.mask_out = mask_out;
+    ra.idx_out = kv_idx_out ? kv_idx_out : w.idx;
+    SLA2_CUDA_TRY(launch_router(ra, (cudaStream_t)stream, &g_launches));
+    return SLA2_OK;
+}
+
+sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* proj_q,
+                         const float* proj_k, const float* rho, void* out, uint8_t* mask_out, int32_t* kv_idx_out,
+                         const sla2_fwd_saved* saved, void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    const Geo g = geometry(p);
+    if (!q || !k || !v || !proj_q || !proj_k || !rho || !out)
+        return fail(SLA2_CONTRACT_ERROR, "NULL input/output pointer");
+    if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
+    Workspace w;
+    carve(g, workspace, &w);
+    int32_t* idx = kv_idx_out ? kv_idx_out : w.idx;
+    cudaStream_t st = (cudaStream_t)stream;
+    s = sla2_router(p, q, k, proj_q, proj_k, nullptr, mask_out, idx, workspace, workspace_bytes, stream);
+    const int router_launches = g_launches;
+    if (s != SLA2_OK) return s;
+    s = run_linear_and_sparse(p, g, w, q, k, v, rho, idx, nullptr, (int)g.kappa, out, saved, st);
+    g_launches += router_launches;
+    return s;
+}
+
+sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_out, float* ktilde_out, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!k || !mean_out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    if (ktilde_out) return fail(SLA2_CONTRACT_ERROR, "ktilde_out is not supported; pass NULL");
+    SLA2_CUDA_TRY(launch_colmean(k, p->dtype == SLA2_BF16, mean_out, (int)(p->B * p->H), (int)p->N, (int)p->d,
+                                 (cudaStream_t)stream, &g_launches));
+    return SLA2_OK;
+}
+
+sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* mask_out, int32_t* kv_idx_out,
+                           void* stream) {
+    g_launches = 0;
+    g_last_error.clear();
+    // only the score-matrix geometry matters here: rows tm = N / bq, columns tn = N / bk
+    if (!p) return fail(SLA2_CONTRACT_ERROR, "params is NULL");
+    if (p->B <= 0 || p->H <= 0 || p->N <= 0 || p->bq <= 0 || p->bk <= 0 || p->N % p->bq || p->N % p->bk)
+        return fail(SLA2_SHAPE_ERROR, "hard_topk: bad score-matrix geometry");
+    if (!(p->k_percent > 0.0 && p->k_percent <= 100.0))
+        return fail(SLA2_SHAPE_ERROR, "hard_topk: k_percent must be in (0, 100]");  // router.hpp:108-110
+    sla2_status s = check_device();
+    if (s != SLA2_OK) return s;
+    if (!pc || !kv_idx_out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    SLA2_CUDA_TRY(launch_topk_only(pc, (int)g.BH, (int)g.tm, (int)g.tn, (int)g.kappa, mask_out, kv_idx_out,
+                                   (cudaStream_t)stream, &g_launches));
+    return SLA2_OK;
+}
+
+sla2_status sla2_sparse_fwd(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
+                            const uint8_t* mask, void* out, const sla2_fwd_saved* saved, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    const Geo g = geometry(p);
+    if (!q || !k || !v || !rho || !mask || !out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
+    Workspace w;
+    carve(g, workspace, &w);
+    cudaStream_t st = (cudaStream_t)stream;
+    SLA2_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), st));
+    SLA2_CUDA_TRY(launch_mask_to_idx(mask, (int)(g.BH * g.tm), (int)g.tn, w.idx, w.cnt, w.flag, st, &g_launches));
+    int flag = 0;
+    SLA2_CUDA_TRY(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SLA2_CUDA_TRY(cudaStreamSynchronize(st));
+    if (flag) return fail(SLA2_SHAPE_ERROR, "sla2_forward_blockwise: mask row keeps no blocks");  // attention.hpp:445
+    if (p->smooth) SLA2_CUDA_TRY(launch_colmean(k, g.bf16, w.mu, (int)g.BH, (int)g.N, (int)g.d, st, &g_launches));
+    const int ml = g_launches;
+    s = run_linear_and_sparse(p, g, w, q, k, v, rho, w.idx, w.cnt, (int)g.tn, out, saved, st);
+    g_launches += ml;
+    return s;
+}
+
+sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* k, const void* v, void* out,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (p->dtype != SLA2_BF16) return fail(SLA2_CONTRACT_ERROR, "sla2_dense_fwd is the bf16 tcgen05 baseline");
+    const Geo g = geometry(p);
+    if (!q || !k || !v || !out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    (void)workspace;
+    (void)workspace_bytes;
+    CUtensorMap mq, mk, mv;
+    const uint64_t rows = (uint64_t)(g.BH * g.N);
+    if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
+        !make_map(&mv, v, rows, g.d, 64, 64, 2))
+        return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    SparseLaunch sa{};
+    sa.B = g.B;
+    sa.H = g.H;
+    sa.N = (int)g.N;
+    sa.d = (int)g.d;
+    sa.bq = (int)g.bq;
+    sa.bk = (int)g.bk;
+    sa.tm = (int)g.tm;
+    sa.tn = (int)g.tn;
+    sa.kstride = (int)g.tn;
+    sa.kappa = (int)g.tn;
+    sa.dense = 1;
+    sa.inv_sqrt_d = inv_sqrt(g.d);
+    sa.out = out;
+    sa.tm_q = &mq;
+    sa.tm_k = &mk;
+    sa.tm_v = &mv;
+    sa.tm_phik = &mk;
+    SLA2_CUDA_TRY(launch_sparse_bf16(sa, (cudaStream_t)stream, &g_launches));
+    return SLA2_OK;
+}
+
+sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
+                              const float* proj_q, const float* proj_k, const float* rho, void* out,
+                              uint8_t* mask_out) {
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    const Geo g = geometry(p);
+    const size_t esz = g.bf16 ? 2 : 4;
+    const size_t tensor = (size_t)(g.BH * g.N * g.d) * esz;
+    const size_t projb = (size_t)(g.H * g.d * g.d) * 4, rhob = (size_t)(g.H * g.tm) * 4;
+    const size_t maskb = (size_t)(g.BH * g.tm * g.tn);
+    const size_t wsb = carve(g, nullptr, nullptr);
+    // one cached device arena per thread, grown on demand
+    thread_local void* arena = nullptr;
+    thread_local size_t arena_bytes = 0;
+    thread_local cudaStream_t st = nullptr;
+    const size_t need = 4 * tensor + 2 * projb + rhob + maskb + wsb + 8 * 256;
+    if (need > arena_bytes) {
+        if (arena) cudaFree(arena);
+        arena = nullptr;
+        arena_bytes = 0;
+        SLA2_CUDA_TRY(cudaMalloc(&arena, need));
+        arena_bytes = need;
+    }
+    if (!st) SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    Carver c{reinterpret_cast<uint8_t*>(arena)};
+    void* dq = c.take<uint8_t>(tensor);
+    void* dk = c.take<uint8_t>(tensor);
+    void* dv = c.take<uint8_t>(tensor);
+    void* dout = c.take<uint8_t>(tensor);
+    float* dpq = c.take<float>(projb / 4);
+    float* dpk = c.take<float>(projb / 4);
+    float* drho = c.take<float>(rhob / 4);
+    uint8_t* dmask = c.take<uint8_t>(maskb);
+    void* dws = c.take<uint8_t>(wsb);
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dq, q, tensor, cudaMemcpyHostToDevice, st));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dk, k, tensor, cudaMemcpyHostToDevice, st));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dv, v, tensor, cudaMemcpyHostToDevice, st));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dpq, proj_q, projb, cudaMemcpyHostToDevice, st));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dpk, proj_k, projb, cudaMemcpyHostToDevice, st));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(drho, rho, rhob, cudaMemcpyHostToDevice, st));
+    s = sla2_forward(p, dq, dk, dv, dpq, dpk, drho, dout, mask_out ? dmask : nullptr, nullptr, nullptr, dws, wsb, st);
+    if (s != SLA2_OK) return s;
+    SLA2_CUDA_TRY(cudaMemcpyAsync(out, dout, tensor, cudaMemcpyDeviceToHost, st));
+    if (mask_out) SLA2_CUDA_TRY(cudaMemcpyAsync(mask_out, dmask, maskb, cudaMemcpyDeviceToHost, st));
+    SLA2_CUDA_TRY(cudaStreamSynchronize(st));
+    return SLA2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// kernels.h -- internal launch interface between the C ABI (capi.cu) and the sm_100a kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sla2dev {
+
+// ---- router (router.cu)
+struct RouterLaunch {
+    const void* q;
+    const void* k;
+    bool bf16;
+    int64_t B, H;
+    int N, d, bq, bk, kappa;
+    int smooth, exact_mu;
+    float inv_sqrt_d;
+    const float* proj_q;
+    const float* proj_k;
+    float* mu_out;    // [BH][d] (written unless null)
+    double* mu_part;  // fast colmean scratch
+    float* qp;        // [BH][tm][d]
+    float* kp;        // [BH][tn][d]
+    float* pc_out;    // optional [BH][tm][tn]
+    uint8_t* mask_out;
+    int32_t* idx_out;  // [BH][tm][kappa]
+};
+cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches);
+cudaError_t launch_colmean(const void* k, bool bf16, float* mu, int BH, int N, int d, cudaStream_t st, int* launches);
+cudaError_t launch_topk_only(const float* pc, int BH, int tm, int tn, int kappa, uint8_t* mask, int32_t* idx,
+                             cudaStream_t st, int* launches);
+cudaError_t launch_mask_to_idx(const uint8_t* mask, int rows, int tn, int32_t* idx, int32_t* cnt, int* empty_flag,
+                               cudaStream_t st, int* launches);
+
+// ---- linear-branch precompute (linear.cu)
+struct LinearLaunch {
+    const void* k;
+    const void* v;
+    bool bf16;
+    int64_t BH;
+    int N, d, bk;
+    const float* mu;  // null when smooth == 0
+    void* phik;       // bf16 [BH][N][d] (bf16 path) or fp32 (f32 path)
+    float* zblk;      // [BH][tn][d] colsum of (rounded) phi(K~) per key block
+    float* ztot;      // [BH][d]
+    float* hpart;     // [BH][nchunk][d][d] partial phi(K~)^T V
+    float* htot;      // [BH][d][d]
+    int nchunk;       // key-block chunks per head for the H partials
+    const CUtensorMap* tm_phik;  // bf16 path: TMA maps (box 64x64, SW128) over [BH*N][d]
+    const CUtensorMap* tm_v;
+};
+cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches);
+
+// ---- sparse / dense attention (sparse_bf16.cu, sparse_f32.cu)
+struct SparseLaunch {
+    int64_t B, H;
+    int N, d, bq, bk, tm, tn;
+    const int32_t* kv_idx;  // [BH][tm][kstride]
+    const int32_t* kv_cnt;  // [BH][tm] or null (every row keeps `kappa`)
+    int kstride, kappa;
+    const float* rho;   // [H][tm]
+    const float* htot;  // [BH][d][d]
+    const float* ztot;  // [BH][d]
+    const float* zblk;  // [BH][tn][d]
+    const float* mu;    // [BH][d] (for L correction / f32 K~), may be null when smooth == 0
+    int smooth;
+    int dense;          // visit every key block, no linear branch (full_attention)
+    float inv_sqrt_d;
+    void* out;
+    float* o_s;
+    float* o_l;
+    float* big_l;
+    // bf16 path
+    const CUtensorMap* tm_q;
+    const CUtensorMap* tm_k;
+    const CUtensorMap* tm_v;
+    const CUtensorMap* tm_phik;
+    // f32 path
+    const float* q;
+    const float* k;
+    const float* v;
+    const float* phik;
+};
+cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* launches);
+cudaError_t launch_sparse_f32(const SparseLaunch& a, cudaStream_t st, int* launches);
+size_t sparse_f32_smem_bytes(int d, int bq, int bk);
+
+// ---- INT8 QAT path (quant.cu)
+struct QuantLaunch {
+    int64_t B, H;
+    int N, d, bq, bk, tm, tn;
+    const void* q;  // bf16
+    const void* k;
+    const void* v;
+    const float* mu;
+    int smooth;
+    int8_t* qc;     // [BH][N][d] Q codes per query block
+    float* qs;      // [BH][tm]
+    int8_t* kc;     // [BH][N][d] K~ codes per key block
+    float* ks;      // [BH][tn]
+    int8_t* vct;    // [BH][tn][d][bk] V codes per key block, transposed (d-major)
+    float* vs;      // [BH][tn]
+};
+cudaError_t launch_quant_prep(const QuantLaunch& a, cudaStream_t st, int* launches);
+struct SparseI8Launch {
+    SparseLaunch s;
+    const int8_t* qc;
+    const float* qs;
+    const int8_t* kc;
+    const float* ks;
+    const int8_t* vct;
+    const float* vs;
+    const CUtensorMap* tm_qc;   // [BH*N][d] int8, box 128x128
+    const CUtensorMap* tm_kc;   // [BH*N][d] int8, box 128(x) x 64(y)
+    const CUtensorMap* tm_vct;  // [BH*tn*d][bk] int8, box 64 x 128
+};
+cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* launches);
+
+}  // namespace sla2dev

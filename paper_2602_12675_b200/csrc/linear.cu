@@ -1,0 +1,280 @@
+// linear.cu -- linear-branch precompute of SLA2 on sm_100a.
+//
+// Replaces attention.hpp:455-475 of sla2_forward_blockwise:
+//   K~ = smooth_k(K); phi(K~) = row_softmax(K~) over the d features     (456-457)
+//   z_j = colsum phi(K~_j), h_j = phi(K~_j)^T V_j for every key block j   (459-475)
+// The per-query-block complement sum over unselected blocks (495-502) is re-expressed as
+// "total minus selected": this file produces the totals Ztot = sum_j z_j and
+// Htot = phi(K~)^T V over all N keys; the sparse kernel subtracts the selected part. No per-
+// block h_j (d x d) is ever stored.
+//
+// Kernels:
+//   phik_kernel      (SIMT)    phi(K~) rows -> bf16 (or fp32) [BH][N][d], z_j per key block
+//   htot_umma_kernel (tcgen05) per (bh, chunk of key blocks): TMA phi(K~)/V tiles, M128 N128
+//                              K64 MMAs accumulating in TMEM, partial written once
+//   htot_simt_kernel (SIMT)    the fp32 path's partials (any d)
+//   lin_reduce_kernel          Htot = sum of partials, Ztot = sum_j z_j (fixed order)
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace sla2dev {
+
+template <typename T>
+__device__ __forceinline__ float ld_f32(const T* p);
+template <>
+__device__ __forceinline__ float ld_f32<float>(const float* p) {
+    return *p;
+}
+template <>
+__device__ __forceinline__ float ld_f32<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat162float(*p);
+}
+
+template <typename OutT>
+__device__ __forceinline__ float store_round(OutT* p, float v);
+template <>
+__device__ __forceinline__ float store_round<float>(float* p, float v) {
+    *p = v;
+    return v;
+}
+template <>
+__device__ __forceinline__ float store_round<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    *p = b;
+    return __bfloat162float(b);
+}
+
+// One CTA (4 warps) per (key block j, bh). Each warp owns rows w, w+4, ...; a lane owns the
+// features lane, lane+32, ... (d <= 128). z_j is summed over the rows as stored (rounded), so
+// Ztot - z_sel matches the operands the tensor cores see.
+template <typename InT, typename OutT>
+__global__ void __launch_bounds__(128) phik_kernel(const InT* __restrict__ k, const float* __restrict__ mu,
+                                                   OutT* __restrict__ phik, float* __restrict__ zblk, int N, int d,
+                                                   int bk) {
+    const int j = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tn = N / bk;
+    __shared__ float zpart[4][128];
+    float zacc[4] = {0.f, 0.f, 0.f, 0.f};
+    float m4[4];
+    for (int u = 0; u < 4; ++u) {
+        const int f = lane + 32 * u;
+        m4[u] = (mu && f < d) ? mu[bh * d + f] : 0.0f;
+    }
+    for (int t = warp; t < bk; t += 4) {
+        const int64_t row = bh * N + (int64_t)j * bk + t;
+        float x[4];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = lane + 32 * u;
+            x[u] = (f < d) ? ld_f32(k + row * d + f) - m4[u] : -INFINITY;
+            mx = fmaxf(mx, x[u]);
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float s = 0.0f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = lane + 32 * u;
+            x[u] = (f < d) ? expf(x[u] - mx) : 0.0f;
+            s += x[u];
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const float inv = 1.0f / s;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = lane + 32 * u;
+            if (f < d) zacc[u] += store_round(phik + row * d + f, x[u] * inv);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zpart[warp][lane + 32 * u] = zacc[u];
+    __syncthreads();
+    for (int f = threadIdx.x; f < d; f += blockDim.x)
+        zblk[(bh * tn + j) * d + f] = ((zpart[0][f] + zpart[1][f]) + zpart[2][f]) + zpart[3][f];
+}
+
+// tcgen05 partial Htot for the bf16 path (d = 128, bk = 64): CTA per (chunk, bh) covering
+// `per` key blocks; phi(K~)^T V accumulated in 128 TMEM columns; 4 warps read the 128x128
+// fp32 partial back (lane = feature f) and store it.
+namespace ht {
+constexpr int D = 128, BK = 64, NS = 4;
+constexpr uint32_t TILE = BK * D * 2;
+constexpr uint32_t SMEM = NS * 2 * TILE + 1024;
+}  // namespace ht
+
+__global__ void __launch_bounds__(128, 1)
+    htot_umma_kernel(const __grid_constant__ CUtensorMap tmPhi, const __grid_constant__ CUtensorMap tmV,
+                     float* __restrict__ hpart, int N, int per, int nchunk) {
+    using namespace ht;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[NS], empty[NS], done;
+    __shared__ uint32_t tbase;
+    const int chunk = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tn = N / BK;
+    const int j0 = chunk * per;
+    const int nblk = min(per, tn - j0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc(&tbase, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tbase;
+    auto sA = [&](int s) { return smem + s * 2 * TILE; };
+    auto sB = [&](int s) { return smem + s * 2 * TILE + TILE; };
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmPhi);
+        tma_prefetch_desc(&tmV);
+        for (int b = 0; b < nblk; ++b) {
+            const int s = b % NS;
+            if (b >= NS) mbar_wait(&empty[s], ((b / NS) - 1) & 1);
+            const int row = (int)(bh * N + (int64_t)(j0 + b) * BK);
+            mbar_arrive_expect_tx(&full[s], 2 * TILE);
+            tma_load_2d(sA(s), &tmPhi, 0, row, &full[s]);
+            tma_load_2d(sA(s) + 8192, &tmPhi, 64, row, &full[s]);
+            tma_load_2d(sB(s), &tmV, 0, row, &full[s]);
+            tma_load_2d(sB(s) + 8192, &tmV, 64, row, &full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t ID = idesc_bf16(128, 128, true, true);
+        for (int b = 0; b < nblk; ++b) {
+            const int s = b % NS;
+            mbar_wait(&full[s], (b / NS) & 1);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sA(s)), bb = smem_u32(sB(s));
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+                umma_bf16_ss(tmem, sdesc_sw128(a + ks * 2048, 8192, 1024), sdesc_sw128(bb + ks * 2048, 8192, 1024),
+                             ID, (b > 0 || ks > 0));
+            umma_commit(&empty[s]);
+        }
+        umma_commit(&done);
+    }
+    __syncwarp();
+    mbar_wait(&done, 0);
+    __syncwarp();
+    tc_fence_after();
+    const int f = warp * 32 + lane;
+    float* dst = hpart + ((bh * nchunk + chunk) * (int64_t)D + f) * D;
+#pragma unroll
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)
+            *reinterpret_cast<float4*>(dst + c0 + c) =
+                make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                            __uint_as_float(r[c + 3]));
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_free(tmem, 128);
+}
+
+// SIMT partial Htot for the fp32 path: CTA per (chunk of `rows` tokens, bh); thread owns
+// entries e = tid, tid+256, ... of the d x d matrix; tokens staged through smem.
+template <typename InT>
+__global__ void __launch_bounds__(256) htot_simt_kernel(const float* __restrict__ phik, const InT* __restrict__ v,
+                                                        float* __restrict__ hpart, int N, int d, int rows,
+                                                        int nchunk) {
+    extern __shared__ float sm[];
+    float* sphi = sm;          // [32][d]
+    float* sv = sm + 32 * d;   // [32][d]
+    const int chunk = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int r0 = chunk * rows, r1 = min(N, r0 + rows);
+    const int dd = d * d;
+    float acc[64];
+    const int nper = (dd + 255) / 256;
+    for (int u = 0; u < nper && u < 64; ++u) acc[u] = 0.0f;
+    for (int t0 = r0; t0 < r1; t0 += 32) {
+        const int nt = min(32, r1 - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nt * d; e += blockDim.x) {
+            const int64_t g = (bh * N + t0) * (int64_t)d + e;
+            sphi[e] = phik[g];
+            sv[e] = ld_f32(v + g);
+        }
+        __syncthreads();
+        for (int u = 0; u < nper && u < 64; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            if (e < dd) {
+                const int f = e / d, c = e % d;
+                float a = acc[u];
+                for (int t = 0; t < nt; ++t) a = fmaf(sphi[t * d + f], sv[t * d + c], a);
+                acc[u] = a;
+            }
+        }
+    }
+    for (int u = 0; u < nper && u < 64; ++u) {
+        const int e = threadIdx.x + 256 * u;
+        if (e < dd) hpart[(bh * nchunk + chunk) * (int64_t)dd + e] = acc[u];
+    }
+}
+
+// Htot[bh] = sum_chunk hpart[bh][chunk] (chunk ascending); Ztot[bh] = sum_j zblk[bh][j].
+__global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* __restrict__ zblk,
+                                  float* __restrict__ htot, float* __restrict__ ztot, int nchunk, int d, int tn) {
+    const int64_t bh = blockIdx.y;
+    const int dd = d * d;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int c = 0; c < nchunk; ++c) s += hpart[(bh * nchunk + c) * (int64_t)dd + e];
+        htot[bh * dd + e] = s;
+    }
+    if (blockIdx.x == 0) {
+        for (int f = threadIdx.x; f < d; f += blockDim.x) {
+            float s = 0.0f;
+            for (int j = 0; j < tn; ++j) s += zblk[(bh * tn + j) * d + f];
+            ztot[bh * d + f] = s;
+        }
+    }
+}
+
+cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches) {
+    const int tn = a.N / a.bk;
+    dim3 g1(tn, (unsigned)a.BH);
+    if (a.bf16) {
+        phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(
+            (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.N, a.d, a.bk);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(htot_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ht::SMEM);
+            attr = true;
+        }
+        const int per = (tn + a.nchunk - 1) / a.nchunk;
+        htot_umma_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 128, ht::SMEM, st>>>(*a.tm_phik, *a.tm_v, a.hpart, a.N,
+                                                                                 per, a.nchunk);
+    } else {
+        phik_kernel<float, float><<<g1, 128, 0, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, a.N, a.d,
+                                                      a.bk);
+        const int rows = (a.N + a.nchunk - 1) / a.nchunk;
+        const size_t smem = 2 * 32 * a.d * sizeof(float);
+        htot_simt_kernel<float><<<dim3(a.nchunk, (unsigned)a.BH), 256, smem, st>>>(
+            (const float*)a.phik, (const float*)a.v, a.hpart, a.N, a.d, rows, a.nchunk);
+    }
+    lin_reduce_kernel<<<dim3((a.d * a.d + 255) / 256, (unsigned)a.BH), 256, 0, st>>>(a.hpart, a.zblk, a.htot,
+                                                                                     a.ztot, a.nchunk, a.d, tn);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+}  // namespace sla2dev

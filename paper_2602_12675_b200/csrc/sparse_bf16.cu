@@ -1,0 +1,472 @@
+// sparse_bf16.cu -- the SLA2 sparse + linear + alpha-blend forward for one (b, h, query block)
+// per CTA, on tcgen05 tensor cores with TMEM accumulators and TMA gathers (sm_100a).
+//
+// Replaces the per-query-block loop of sla2_forward_blockwise (attention.hpp:484-558) and its
+// helpers block_scores_qk / block_product_pv (attention.hpp:372-415), for bq = 128, bk = 64,
+// d = 128 (the paper's blocks), bf16 operands, fp32 accumulation.
+//
+// Per CTA (query block i of head bh, kept key blocks j_0 < j_1 < ... from the router):
+//   S_j   = Q_i K_j^T                      tcgen05 kind::f16, M128 N64 K128 -> TMEM (2 buffers)
+//   P_j   = exp2(S_j*log2e/sqrt(d) - m)    softmax warps, online max with lazy rescale
+//   O    += P_j V_j                        tcgen05, M128 N128 K64, O accumulated in TMEM
+//   Hsel += phi(K~_j)^T V_j                tcgen05, M128 N128 K64 (MN-major A and B)
+// epilogue (fused, attention.hpp:532-557):
+//   O_s = O / l
+//   Hc  = Htot - Hsel, Zc = Ztot - sum_sel z_j      ("total minus selected" = the
+//                                                    reference's complement sum, 495-502)
+//   O_l = (phi(Q) Hc) / (phi(Q) . Zc)              tcgen05, M128 N128 K128
+//   out = alpha O_s + (1 - alpha) O_l, alpha = sigmoid(rho_i) (forced to 1 on full rows)
+// The raw K is used for Q K^T: smoothing shifts every score of a row by the same constant
+// (test_attention.cpp:270-279), so O_s is unchanged and K needs no bf16 re-rounding.
+//
+// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 complement of Z, w4-7 softmax / correction / epilogue (thread = query row).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "expf_glibc.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace sla2dev {
+
+namespace sp {
+constexpr int BQ = 128, BK = 64, D = 128, NS = 3;
+constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
+constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
+constexpr uint32_t STAGE_BYTES = 3 * TILE_BYTES;
+constexpr uint32_t P_BYTES = BQ * BK * 2;  // 16 KB
+constexpr uint32_t OFF_Q = 0;
+constexpr uint32_t OFF_STAGE = Q_BYTES;
+constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_P + 2 * P_BYTES;
+constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
+// TMEM columns
+constexpr uint32_t TM_S = 0;      // 2 x 64
+constexpr uint32_t TM_O = 128;    // 128
+constexpr uint32_t TM_H = 256;    // 128
+constexpr uint32_t TM_L = 384;    // 128
+constexpr float RESCALE_LOG2 = 8.0f;  // lazy rescale threshold (P <= 2^8)
+}  // namespace sp
+
+struct SparseBf16Params {
+    const int32_t* kv_idx;
+    const int32_t* kv_cnt;
+    int kstride, kappa;
+    const float* rho;
+    const float* htot;
+    const float* ztot;
+    const float* zblk;
+    const float* mu;
+    const __nv_bfloat16* q;
+    __nv_bfloat16* out;
+    float* o_s;
+    float* o_l;
+    float* big_l;
+    int N, H, tm, tn;
+    float scale_log2;
+    float inv_sqrt_d;
+    int dense;
+};
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(256, 1)
+    sla2_sparse_bf16_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
+                            const SparseBf16Params p) {
+    using namespace sp;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_q, bar_kv_full[NS], bar_kv_empty[NS], bar_s_full[2], bar_s_empty[2], bar_p_full[2],
+        bar_pv_done[2], bar_lin_ready, bar_lin_done;
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float sZc[D];
+
+    const int i = blockIdx.x;           // query block
+    const int64_t bh = blockIdx.y;      // (b, h)
+    const int h = (int)(bh % p.H);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool dense = p.dense != 0;
+    const int nb = dense ? p.tn : (p.kv_cnt ? p.kv_cnt[bh * p.tm + i] : p.kappa);
+    const int32_t* idx = p.kv_idx + (bh * p.tm + i) * (int64_t)p.kstride;
+    const bool full_row = dense || (nb == p.tn);
+    const bool linear = !full_row;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_q, 1);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&bar_kv_full[s], 1);
+            mbar_init(&bar_kv_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&bar_s_full[b], 1);
+            mbar_init(&bar_s_empty[b], 128);
+            mbar_init(&bar_p_full[b], 128);
+            mbar_init(&bar_pv_done[b], 1);
+        }
+        mbar_init(&bar_lin_ready, 128);
+        mbar_init(&bar_lin_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(&tmem_base_sh, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    uint8_t* sQ = smem + OFF_Q;
+    auto sK = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES; };
+    auto sV = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + TILE_BYTES; };
+    auto sPh = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE_BYTES; };
+    auto sP = [&](int b) { return smem + OFF_P + b * P_BYTES; };
+    uint8_t* sHc = smem + OFF_STAGE;  // epilogue alias of stage 0 (32 KB)
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            tma_prefetch_desc(&tmQ);
+            tma_prefetch_desc(&tmK);
+            tma_prefetch_desc(&tmV);
+            if (!dense) tma_prefetch_desc(&tmPhi);
+            const uint64_t pol_keep = policy_evict_last();
+            const int qrow = (int)(bh * p.N + (int64_t)i * BQ);
+            mbar_arrive_expect_tx(&bar_q, Q_BYTES);
+            tma_load_2d(sQ, &tmQ, 0, qrow, &bar_q);
+            tma_load_2d(sQ + 8192, &tmQ, 0, qrow + 64, &bar_q);
+            tma_load_2d(sQ + 16384, &tmQ, 64, qrow, &bar_q);
+            tma_load_2d(sQ + 24576, &tmQ, 64, qrow + 64, &bar_q);
+            const uint32_t stage_tx = dense ? 2 * TILE_BYTES : 3 * TILE_BYTES;
+            for (int j = 0; j < nb; ++j) {
+                const int s = j % NS;
+                if (j >= NS) mbar_wait(&bar_kv_empty[s], ((j / NS) - 1) & 1);
+                const int kb = dense ? j : idx[j];
+                const int krow = (int)(bh * p.N + (int64_t)kb * BK);
+                mbar_arrive_expect_tx(&bar_kv_full[s], stage_tx);
+                tma_load_2d_hint(sK(s), &tmK, 0, krow, &bar_kv_full[s], pol_keep);
+                tma_load_2d_hint(sK(s) + 8192, &tmK, 64, krow, &bar_kv_full[s], pol_keep);
+                tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_kv_full[s], pol_keep);
+                tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_kv_full[s], pol_keep);
+                if (!dense) {
+                    tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_kv_full[s], pol_keep);
+                    tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_kv_full[s], pol_keep);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (one thread) =====================
+        if (lane == 0) {
+            constexpr uint32_t ID_QK = idesc_bf16(128, 64, false, false);
+            constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
+            constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
+            const uint32_t aQ = smem_u32(sQ);
+            mbar_wait(&bar_q, 0);
+            auto issue_qk = [&](int j) {
+                const int s = j % NS, b = j & 1;
+                mbar_wait(&bar_kv_full[s], (j / NS) & 1);
+                if (j >= 2) mbar_wait(&bar_s_empty[b], ((j - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint32_t bK = smem_u32(sK(s));
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+                    const uint32_t offk = (ks >> 2) * 8192 + (ks & 3) * 32;
+                    umma_bf16_ss(tmem + TM_S + b * 64, sdesc_sw128(aQ + off, 16, 1024),
+                                 sdesc_sw128(bK + offk, 16, 1024), ID_QK, ks > 0);
+                }
+                umma_commit(&bar_s_full[b]);
+            };
+            if (nb > 0) issue_qk(0);
+            for (int j = 0; j < nb; ++j) {
+                const int s = j % NS, b = j & 1;
+                if (j + 1 < nb) issue_qk(j + 1);
+                mbar_wait(&bar_p_full[b], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t aP = smem_u32(sP(b));
+                const uint32_t bV = smem_u32(sV(s));
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    umma_bf16_ss(tmem + TM_O, sdesc_sw128(aP + ks * 32, 16, 1024),
+                                 sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV, (j > 0 || ks > 0));
+                }
+                if (!dense) {
+                    const uint32_t aH = smem_u32(sPh(s));
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
+                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (j > 0 || ks > 0));
+                    }
+                }
+                umma_commit(&bar_pv_done[b]);
+                umma_commit(&bar_kv_empty[s]);
+            }
+            if (linear) {
+                // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
+                mbar_wait(&bar_lin_ready, 0);
+                tc_fence_after();
+                const uint32_t bH = smem_u32(sHc);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+                    umma_bf16_ss(tmem + TM_L, sdesc_sw128(aQ + off, 16, 1024),
+                                 sdesc_sw128(bH + ks * 2048, 16384, 1024), ID_PV, ks > 0);
+                }
+                umma_commit(&bar_lin_done);
+            }
+        }
+    } else if (warp == 3) {
+        // ===================== Zc = Ztot - sum_sel z_j =====================
+        if (linear) {
+            const float* zt = p.ztot + bh * D;
+            const float* zb = p.zblk + bh * (int64_t)p.tn * D;
+            for (int f = lane; f < D; f += 32) {
+                float sel = 0.0f;
+                for (int j = 0; j < nb; ++j) sel += zb[(int64_t)idx[j] * D + f];
+                sZc[f] = zt[f] - sel;
+            }
+        }
+        __syncwarp();
+        named_bar_arrive(1, 160);
+    } else if (warp >= 4) {
+        // ===================== softmax / correction / epilogue =====================
+        const int r = threadIdx.x - 128;  // query row within the block
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        float m2 = -INFINITY, l = 0.0f;
+        for (int j = 0; j < nb; ++j) {
+            const int b = j & 1;
+            mbar_wait(&bar_s_full[b], (j >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            uint32_t sr[64];
+            tmem_ld32(tmem + lane_base + TM_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+            tmem_ld32(tmem + lane_base + TM_S + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bar_s_empty[b]);
+            float mx = -INFINITY;
+#pragma unroll
+            for (int t = 0; t < 64; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
+            mx *= p.scale_log2;
+            if (j == 0) {
+                m2 = mx;
+            } else {
+                const bool need = mx > m2 + RESCALE_LOG2;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float mnew = fmaxf(m2, mx);
+                    const float corr = fast_exp2(m2 - mnew);
+                    mbar_wait(&bar_pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                    __syncwarp();
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tmem + lane_base + TM_O + c0, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * corr);
+                        tmem_st32(tmem + lane_base + TM_O + c0, o);
+                    }
+                    tmem_st_wait();
+                    l *= corr;
+                    m2 = mnew;
+                }
+            }
+            // P = exp2(s * scale - m2), bf16, row r of the K-major SW128 A tile
+            if (j >= 2) mbar_wait(&bar_pv_done[b], ((j - 2) >> 1) & 1);
+            const uint32_t prow = smem_u32(sP(b));
+            float rs = 0.0f;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[ch * 8 + 2 * e]), p.scale_log2, -m2));
+                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[ch * 8 + 2 * e + 1]), p.scale_log2, -m2));
+                    const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
+                    const float2 pr = __bfloat1622float2(pk);
+                    rs += pr.x + pr.y;  // row sum of the probabilities actually multiplied
+                    w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+                }
+                st_shared_v4(prow + sw128_off(r, ch * 8), w[0], w[1], w[2], w[3]);
+            }
+            l += rs;
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&bar_p_full[b]);
+        }
+        // all MMAs of the main loop complete
+        if (nb > 0) mbar_wait(&bar_pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+        mbar_wait(&bar_q, 0);
+        __syncwarp();
+        tc_fence_after();
+
+        float alpha = 1.0f;
+        float den = 1.0f;
+        if (linear) {
+            // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
+            const float x = p.rho[(int64_t)h * p.tm + i];
+            float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
+            a = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
+            alpha = a;
+            // phi(Q) = row softmax over d of Q_r (attention.hpp:456), in place over sQ as bf16
+            named_bar_sync(1, 160);  // sZc ready
+            const uint32_t qb = smem_u32(sQ);
+            float qv[128];
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                uint32_t w[4];
+                ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                    qv[ch * 8 + 2 * e] = f2.x;
+                    qv[ch * 8 + 2 * e + 1] = f2.y;
+                }
+            }
+            float qm = -INFINITY;
+#pragma unroll
+            for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
+            float qs = 0.0f;
+#pragma unroll
+            for (int f = 0; f < 128; ++f) {
+                qv[f] = __expf(qv[f] - qm);
+                qs += qv[f];
+            }
+            const float qinv = 1.0f / qs;
+            den = 0.0f;
+            fence_proxy_async_smem();
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int f = ch * 8 + 2 * e;
+                    const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
+                    const float2 pr = __bfloat1622float2(pk);
+                    den += pr.x * sZc[f] + pr.y * sZc[f + 1];
+                    w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+                }
+                st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+            }
+            // Hc = Htot - Hsel, row f = r, bf16 into the MN-major B tile [c_atom][f][64]
+            const float* ht = p.htot + (bh * D + r) * (int64_t)D;
+            const uint32_t hb = smem_u32(sHc);
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t hs[32];
+                tmem_ld32(tmem + lane_base + TM_H + c0, hs);
+                tmem_ld_wait();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const float4 t0 = *reinterpret_cast<const float4*>(ht + c0 + ch * 8);
+                    const float4 t1 = *reinterpret_cast<const float4*>(ht + c0 + ch * 8 + 4);
+                    const uint32_t w0 = pack_bf16(t0.x - __uint_as_float(hs[ch * 8 + 0]), t0.y - __uint_as_float(hs[ch * 8 + 1]));
+                    const uint32_t w1 = pack_bf16(t0.z - __uint_as_float(hs[ch * 8 + 2]), t0.w - __uint_as_float(hs[ch * 8 + 3]));
+                    const uint32_t w2 = pack_bf16(t1.x - __uint_as_float(hs[ch * 8 + 4]), t1.y - __uint_as_float(hs[ch * 8 + 5]));
+                    const uint32_t w3 = pack_bf16(t1.z - __uint_as_float(hs[ch * 8 + 6]), t1.w - __uint_as_float(hs[ch * 8 + 7]));
+                    const int c = c0 + ch * 8;
+                    st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), w0, w1, w2, w3);
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&bar_lin_ready);
+            mbar_wait(&bar_lin_done, 0);
+            __syncwarp();
+            tc_fence_after();
+        } else {
+            named_bar_sync(1, 160);
+        }
+
+        // output: out = alpha * O / l + (1 - alpha) * num / den
+        const float inv_l = 1.0f / l;
+        const float inv_den = 1.0f / den;
+        const float beta = 1.0f - alpha;
+        const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
+        __nv_bfloat16* orow = p.out + grow * D;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t o[32], ln[32];
+            tmem_ld32(tmem + lane_base + TM_O + c0, o);
+            if (linear) tmem_ld32(tmem + lane_base + TM_L + c0, ln);
+            tmem_ld_wait();
+            float res[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const float os = __uint_as_float(o[c]) * inv_l;
+                const float ol = linear ? __uint_as_float(ln[c]) * inv_den : 0.0f;
+                res[c] = linear ? alpha * os + beta * ol : os;
+                if (p.o_s) p.o_s[grow * D + c0 + c] = os;
+                if (p.o_l) p.o_l[grow * D + c0 + c] = ol;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint4 w;
+                w.x = pack_bf16(res[ch * 8 + 0], res[ch * 8 + 1]);
+                w.y = pack_bf16(res[ch * 8 + 2], res[ch * 8 + 3]);
+                w.z = pack_bf16(res[ch * 8 + 4], res[ch * 8 + 5]);
+                w.w = pack_bf16(res[ch * 8 + 6], res[ch * 8 + 7]);
+                *reinterpret_cast<uint4*>(orow + c0 + ch * 8) = w;
+            }
+        }
+        if (p.big_l) {
+            // L with raw K scores, shifted to the smoothed-K scores the reference uses:
+            // q_r . K~_t = q_r . K_t - q_r . mu
+            float shift = 0.0f;
+            if (p.mu) {
+                const float* mu = p.mu + bh * D;
+                const __nv_bfloat16* qg = p.q + grow * D;
+                for (int f = 0; f < D; ++f) shift += __bfloat162float(qg[f]) * mu[f];
+                shift *= p.inv_sqrt_d;
+            }
+            p.big_l[grow] = m2 / 1.4426950408889634f + logf(l) - shift;
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 2) tmem_free(tmem, 512);
+}
+
+cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* launches) {
+    SparseBf16Params p;
+    p.kv_idx = a.kv_idx;
+    p.kv_cnt = a.kv_cnt;
+    p.kstride = a.kstride;
+    p.kappa = a.kappa;
+    p.rho = a.rho;
+    p.htot = a.htot;
+    p.ztot = a.ztot;
+    p.zblk = a.zblk;
+    p.mu = a.smooth ? a.mu : nullptr;
+    p.q = (const __nv_bfloat16*)a.q;
+    p.out = (__nv_bfloat16*)a.out;
+    p.o_s = a.o_s;
+    p.o_l = a.o_l;
+    p.big_l = a.big_l;
+    p.N = a.N;
+    p.H = (int)a.H;
+    p.tm = a.tm;
+    p.tn = a.tn;
+    p.inv_sqrt_d = a.inv_sqrt_d;
+    p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
+    p.dense = a.dense;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(sla2_sparse_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::SMEM_ALLOC);
+        attr = true;
+    }
+    dim3 grid(a.tm, (unsigned)(a.B * a.H));
+    sla2_sparse_bf16_kernel<<<grid, 256, sp::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v,
+                                                                a.dense ? *a.tm_k : *a.tm_phik, p);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace sla2dev

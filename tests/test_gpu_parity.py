@@ -1,0 +1,177 @@
+"""Parity of the sm_100a SLA2 forward (through the C ABI) against the CPU oracle.
+
+Bar (north star): router mask bits and kept-block index lists bit-exact; outputs within
+1e-2 normwise relative for bf16 (max|gpu-ref| <= 1e-2 * max|ref|) and max-abs 1e-4 for fp32,
+the reference's own float tolerance (test_attention.cpp:232-241)."""
+import numpy as np
+import pytest
+
+import paper_2602_12675_b200 as sla2
+from sla2_testlib import (make_inputs, mask_to_idx, oracle_head, oracle_router_head, rel_err, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2
+F32_TOL = 1e-4
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ----------------------------------------------------------------------------- router
+@pytest.mark.parametrize("N,k_percent,sigma,seed", [(4096, 3.0, 1.0, 1), (8192, 3.0, 1.0, 2), (8192, 10.0, 4.0, 3),
+                                                   (16384, 5.0, 1.0, 4)])
+def test_router_bitexact_bf16(cuda, N, k_percent, sigma, seed):
+    torch = _torch()
+    B, H, d, bq, bk = 1, 3, 128, 128, 64
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, seed, sigma)
+    pc, mask, idx = sla2.router(to_dev(q, torch.bfloat16, cuda), to_dev(k, torch.bfloat16, cuda),
+                                to_dev(pq, torch.float32, cuda), to_dev(pk, torch.float32, cuda),
+                                k_percent=k_percent, bq=bq, bk=bk)
+    pc, mask, idx = pc.cpu().numpy(), mask.cpu().numpy(), idx.cpu().numpy()
+    for h in range(H):
+        rpc, rmask, kappa = oracle_router_head(q[0, h], k[0, h], pq[h], pk[h], bq, bk, k_percent)
+        assert np.array_equal(pc[0, h].view(np.uint32), rpc.view(np.uint32)), f"pc bits differ (head {h})"
+        assert np.array_equal(mask[0, h], rmask), f"mask differs (head {h})"
+        ridx = np.stack(mask_to_idx(rmask))
+        assert ridx.shape[1] == kappa
+        assert np.array_equal(idx[0, h], ridx)
+
+
+def test_router_bitexact_f32_cfg1(cuda):
+    torch = _torch()
+    B, H, N, d, bq, bk, kp = 1, 2, 4096, 64, 64, 64, 10.0
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 11, 1.0, bf16=False, bq=bq, bk=bk)
+    pc, mask, idx = sla2.router(to_dev(q, torch.float32, cuda), to_dev(k, torch.float32, cuda),
+                                to_dev(pq, torch.float32, cuda), to_dev(pk, torch.float32, cuda), k_percent=kp,
+                                bq=bq, bk=bk)
+    for h in range(H):
+        rpc, rmask, kappa = oracle_router_head(q[0, h], k[0, h], pq[h], pk[h], bq, bk, kp)
+        assert np.array_equal(pc.cpu().numpy()[0, h].view(np.uint32), rpc.view(np.uint32))
+        assert np.array_equal(mask.cpu().numpy()[0, h], rmask)
+        assert np.array_equal(idx.cpu().numpy()[0, h], np.stack(mask_to_idx(rmask)))
+
+
+# ----------------------------------------------------------------------------- bf16 forward
+@pytest.mark.parametrize("N,H,k_percent,seed", [(4096, 2, 3.0, 5), (8192, 2, 10.0, 6), (2048, 1, 50.0, 7)])
+def test_forward_bf16_vs_oracle(cuda, N, H, k_percent, seed):
+    torch = _torch()
+    B, d, bq, bk = 1, 128, 128, 64
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, seed)
+    out, mask, sv = sla2.forward(to_dev(q, torch.bfloat16, cuda), to_dev(k, torch.bfloat16, cuda),
+                                 to_dev(v, torch.bfloat16, cuda), to_dev(pq, torch.float32, cuda),
+                                 to_dev(pk, torch.float32, cuda), to_dev(rho, torch.float32, cuda),
+                                 k_percent=k_percent, return_mask=True, saved=True)
+    out = out.float().cpu().numpy()
+    for h in range(H):
+        r_out, r_mask, r_os, r_ol, r_l = oracle_head(q[0, h], k[0, h], v[0, h], pq[h], pk[h], rho[h], bq, bk,
+                                                     k_percent)
+        assert np.array_equal(mask.cpu().numpy()[0, h], r_mask)
+        e_max, e_l2 = rel_err(out[0, h], r_out)
+        assert e_max <= BF16_TOL, (h, e_max, e_l2)
+        e_os = rel_err(sv["o_s"].cpu().numpy()[0, h], r_os)
+        e_ol = rel_err(sv["o_l"].cpu().numpy()[0, h], r_ol)
+        assert e_os[0] <= BF16_TOL, ("o_s", e_os)
+        assert e_ol[0] <= BF16_TOL, ("o_l", e_ol)
+        np.testing.assert_allclose(sv["big_l"].cpu().numpy()[0, h], r_l, atol=2e-2, rtol=2e-3)
+
+
+def test_forward_bf16_batch_layout(cuda):
+    """B > 1 with per-head router state shared across the batch (model.hpp:38-39)."""
+    torch = _torch()
+    B, H, N, d = 2, 2, 2048, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 21)
+    out = sla2.forward(to_dev(q, torch.bfloat16, cuda), to_dev(k, torch.bfloat16, cuda),
+                       to_dev(v, torch.bfloat16, cuda), to_dev(pq, torch.float32, cuda),
+                       to_dev(pk, torch.float32, cuda), to_dev(rho, torch.float32, cuda), k_percent=5.0)
+    out = out.float().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            r = oracle_head(q[b, h], k[b, h], v[b, h], pq[h], pk[h], rho[h], 128, 64, 5.0)[0]
+            assert rel_err(out[b, h], r)[0] <= BF16_TOL
+
+
+# ----------------------------------------------------------------------------- fp32 forward
+@pytest.mark.parametrize("N,d,bq,bk,k_percent", [(4096, 64, 64, 64, 10.0), (1024, 32, 32, 16, 25.0),
+                                                 (64, 8, 8, 4, 10.0), (64, 8, 8, 4, 50.0)])
+def test_forward_f32_vs_oracle(cuda, N, d, bq, bk, k_percent):
+    torch = _torch()
+    B, H = 1, 2
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 31, bf16=False, bq=bq, bk=bk)
+    out, mask = sla2.forward(to_dev(q, torch.float32, cuda), to_dev(k, torch.float32, cuda),
+                             to_dev(v, torch.float32, cuda), to_dev(pq, torch.float32, cuda),
+                             to_dev(pk, torch.float32, cuda), to_dev(rho, torch.float32, cuda),
+                             k_percent=k_percent, bq=bq, bk=bk, return_mask=True)
+    for h in range(H):
+        r_out, r_mask = oracle_head(q[0, h], k[0, h], v[0, h], pq[h], pk[h], rho[h], bq, bk, k_percent)[:2]
+        assert np.array_equal(mask.cpu().numpy()[0, h], r_mask)
+        assert np.abs(out.cpu().numpy()[0, h] - r_out).max() <= F32_TOL
+
+
+# ----------------------------------------------------------------------------- blockwise with masks
+def test_full_mask_is_full_attention(cuda):
+    """BlockMask::ones: alpha forced to 1, equals full attention (test_attention.cpp:167-174)."""
+    torch = _torch()
+    B, H, N, d = 1, 2, 2048, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 41)
+    qd, kd, vd = (to_dev(x, torch.bfloat16, cuda) for x in (q, k, v))
+    mask = torch.ones((B, H, N // 128, N // 64), dtype=torch.uint8, device=cuda)
+    out = sla2.sla2_forward_blockwise(qd, kd, vd, mask, to_dev(rho, torch.float32, cuda))
+    ref = torch.nn.functional.scaled_dot_product_attention(qd.float(), kd.float(), vd.float())
+    assert rel_err(out.float().cpu().numpy(), ref.cpu().numpy())[0] <= BF16_TOL
+    dense = sla2.full_attention(qd, kd, vd)
+    assert rel_err(dense.float().cpu().numpy(), ref.cpu().numpy())[0] <= BF16_TOL
+
+
+def test_ragged_mask_rows(cuda):
+    """Random masks with different kept counts per row (random_mask, test_attention.cpp:40-42)."""
+    torch = _torch()
+    import oracle_ctypes as oc
+    B, H, N, d = 1, 1, 2048, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 43)
+    rng = np.random.default_rng(0)
+    tm, tn = N // 128, N // 64
+    m = (rng.random((tm, tn)) < 0.1).astype(np.uint8)
+    m[np.arange(tm), rng.integers(0, tn, tm)] = 1
+    m[3, :] = 1  # one full row
+    out = sla2.sla2_forward_blockwise(*(to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)),
+                                      torch.from_numpy(m[None, None]).to(cuda), to_dev(rho, torch.float32, cuda))
+    r = oc.port().forward_blockwise(q[0, 0], k[0, 0], v[0, 0], 128, 64, m, rho[0])[0]
+    assert rel_err(out.float().cpu().numpy()[0, 0], r)[0] <= BF16_TOL
+
+
+def test_empty_mask_row_raises(cuda):
+    """attention.hpp:442-447 / test_attention.cpp:305-311."""
+    torch = _torch()
+    B, H, N, d = 1, 1, 1024, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 44)
+    mask = torch.ones((1, 1, N // 128, N // 64), dtype=torch.uint8, device=cuda)
+    mask[0, 0, 2] = 0
+    with pytest.raises(sla2.ShapeError):
+        sla2.sla2_forward_blockwise(*(to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)), mask,
+                                    to_dev(rho, torch.float32, cuda))
+
+
+def test_budget_edges(cuda):
+    """kappa = 1 (tiny k%) and kappa = tn (k = 100: every row full, alpha forced to 1)."""
+    torch = _torch()
+    B, H, N, d = 1, 1, 2048, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 45)
+    dev = [to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)] + [to_dev(x, torch.float32, cuda) for x in (pq, pk, rho)]
+    for kp in (0.01, 100.0):
+        out, mask = sla2.forward(*dev, k_percent=kp, return_mask=True)
+        r_out, r_mask = oracle_head(q[0, 0], k[0, 0], v[0, 0], pq[0], pk[0], rho[0], 128, 64, kp)[:2]
+        assert np.array_equal(mask.cpu().numpy()[0, 0], r_mask)
+        assert rel_err(out.float().cpu().numpy()[0, 0], r_out)[0] <= BF16_TOL
+
+
+def test_deterministic(cuda):
+    torch = _torch()
+    B, H, N, d = 1, 2, 4096, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 46)
+    dev = [to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)] + [to_dev(x, torch.float32, cuda) for x in (pq, pk, rho)]
+    a = sla2.forward(*dev).clone()
+    b = sla2.forward(*dev)
+    assert torch.equal(a, b)
