@@ -152,6 +152,14 @@ const char* sla2_last_error(void);
 /* Number of kernel launches the last sla2_* call on this thread enqueued (bench evidence). */
 int32_t sla2_last_launch_count(void);
 
+/* Stage timing (off by default). When enabled, sla2_forward records CUDA events on its
+ * stream around its stages; sla2_last_stage_ms waits for the last call's events and writes
+ * up to n durations in ms: [0] router (smooth_k + block_scores + hard_topk), [1] linear
+ * precompute (phi(K~), z, Htot), [2] sparse+linear+blend kernel, [3] whole call. Returns the
+ * number written. */
+void sla2_enable_stage_timing(int32_t enable);
+int32_t sla2_last_stage_ms(float* out, int32_t n);
+
 /* "sla2_b200 <version> sm_100a" */
 const char* sla2_version(void);
 

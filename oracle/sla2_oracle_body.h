@@ -516,15 +516,18 @@ int FN(sla2o_attention)(const T* q, const T* k, const T* v, size_t n, size_t d, 
 }
 
 /* test_util.hpp:11-28 */
+/* The bounds / stddev are T-typed parameters in the reference, widened to double. */
 void FN(sla2o_random_matrix)(T* out, size_t n, uint64_t seed, double lo, double hi) {
     sla2o_rng r;
     sla2o_rng_seed(&r, seed);
-    for (size_t i = 0; i < n; ++i) out[i] = (T)sla2o_rng_uniform(&r, lo, hi);
+    const double dlo = (double)(T)lo, dhi = (double)(T)hi;
+    for (size_t i = 0; i < n; ++i) out[i] = (T)sla2o_rng_uniform(&r, dlo, dhi);
 }
 void FN(sla2o_gaussian_matrix)(T* out, size_t n, uint64_t seed, double sd) {
     sla2o_rng r;
     sla2o_rng_seed(&r, seed);
-    for (size_t i = 0; i < n; ++i) out[i] = (T)sla2o_rng_normal(&r, 0.0, sd);
+    const double dsd = (double)(T)sd;
+    for (size_t i = 0; i < n; ++i) out[i] = (T)sla2o_rng_normal(&r, 0.0, dsd);
 }
 
 #undef FN

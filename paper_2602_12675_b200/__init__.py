@@ -33,7 +33,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libsla2_b200.so")
+_SO = os.environ.get("SLA2_LIB") or os.path.join(_HERE, "libsla2_b200.so")  # SLA2_LIB: analysis builds
 
 
 class Sla2Error(RuntimeError):
@@ -99,6 +99,8 @@ def lib():
         "sla2_last_error": ([], C.c_char_p),
         "sla2_last_launch_count": ([], C.c_int32),
         "sla2_version": ([], C.c_char_p),
+        "sla2_enable_stage_timing": ([C.c_int32], None),
+        "sla2_last_stage_ms": ([C.POINTER(C.c_float), C.c_int32], C.c_int32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -119,6 +121,17 @@ def _raise(rc: int):
 def last_launch_count() -> int:
     """Kernel launches enqueued by the last call on this thread."""
     return int(lib().sla2_last_launch_count())
+
+
+def enable_stage_timing(on: bool = True):
+    lib().sla2_enable_stage_timing(1 if on else 0)
+
+
+def last_stage_ms():
+    """(router, linear precompute, sparse kernel, total) ms of the last forward (CUDA events)."""
+    buf = (C.c_float * 4)()
+    n = lib().sla2_last_stage_ms(buf, 4)
+    return tuple(float(buf[i]) for i in range(n))
 
 
 def topk_budget(k_percent: float, tn: int) -> int:

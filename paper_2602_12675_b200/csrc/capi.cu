@@ -22,6 +22,17 @@ namespace {
 thread_local std::string g_last_error;
 thread_local int g_launches = 0;
 
+// optional stage timing: events [0] start, [1] after router, [2] after linear prep, [3] end
+thread_local bool g_timing = false;
+thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local bool g_ev_recorded = false;
+void mark(int i, cudaStream_t st) {
+    if (!g_timing) return;
+    if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
+    cudaEventRecord(g_ev[i], st);
+    if (i == 3) g_ev_recorded = true;
+}
+
 sla2_status fail(sla2_status s, const std::string& msg) {
     g_last_error = msg;
     return s;
@@ -71,9 +82,10 @@ struct MapKey {
     const void* ptr;
     uint64_t rows, cols;
     uint32_t box_x, box_y, elem;
+    bool swz;
     bool operator==(const MapKey& o) const {
         return ptr == o.ptr && rows == o.rows && cols == o.cols && box_x == o.box_x && box_y == o.box_y &&
-               elem == o.elem;
+               elem == o.elem && swz == o.swz;
     }
 };
 struct MapKeyHash {
@@ -86,10 +98,10 @@ struct MapKeyHash {
 // 2-D row-major [rows][cols] tensor of `elem`-byte elements, box (box_x cols, box_y rows),
 // SWIZZLE_128B. Cached: descriptors are immutable for a given pointer/shape.
 bool make_map(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_x, uint32_t box_y,
-              uint32_t elem) {
+              uint32_t elem, bool swizzle128 = true) {
     static std::mutex mu;
     static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-    MapKey key{ptr, rows, cols, box_x, box_y, elem};
+    MapKey key{ptr, rows, cols, box_x, box_y, elem, swizzle128};
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -104,9 +116,12 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, u
     cuuint64_t strides[1] = {cols * elem};
     cuuint32_t box[2] = {box_x, box_y};
     cuuint32_t es[2] = {1, 1};
-    const CUtensorMapDataType dt = elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    const CUtensorMapDataType dt = elem == 2   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                   : elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                               : CU_TENSOR_MAP_DATA_TYPE_UINT8;
     CUresult r = fn(out, dt, 2, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     std::lock_guard<std::mutex> g(mu);
     if (cache.size() > 4096) cache.clear();
@@ -197,6 +212,12 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     return c.off + 256;
 }
 
+// TMA view of K for the serial column-mean kernel: [B*H*N][d] elements, 32 x 256 boxes.
+const CUtensorMap* colmean_map(CUtensorMap* m, const void* k, bool bf16, int64_t BH, int64_t N, int64_t d) {
+    if (N % 256 != 0 || d % 32 != 0) return nullptr;
+    return make_map(m, k, (uint64_t)(BH * N), (uint64_t)d, 32, 256, bf16 ? 2 : 4, false) ? m : nullptr;
+}
+
 float inv_sqrt(int64_t d) {
     // T(1) / std::sqrt(static_cast<T>(d)) for T = float (router.hpp:100, attention.hpp:377)
     volatile float fd = (float)d;
@@ -213,6 +234,21 @@ extern "C" {
 const char* sla2_last_error(void) { return g_last_error.c_str(); }
 int32_t sla2_last_launch_count(void) { return g_launches; }
 const char* sla2_version(void) { return "sla2_b200 0.1.0 sm_100a"; }
+
+void sla2_enable_stage_timing(int32_t enable) { g_timing = enable != 0; }
+
+int32_t sla2_last_stage_ms(float* out, int32_t n) {
+    if (!g_ev_recorded || !out || n <= 0) return 0;
+    cudaEventSynchronize(g_ev[3]);
+    float ms[4] = {0, 0, 0, 0};
+    cudaEventElapsedTime(&ms[0], g_ev[0], g_ev[1]);
+    cudaEventElapsedTime(&ms[1], g_ev[1], g_ev[2]);
+    cudaEventElapsedTime(&ms[2], g_ev[2], g_ev[3]);
+    cudaEventElapsedTime(&ms[3], g_ev[0], g_ev[3]);
+    const int m = n < 4 ? n : 4;
+    for (int i = 0; i < m; ++i) out[i] = ms[i];
+    return m;
+}
 
 void sla2_default_params(sla2_fwd_params* p, int64_t B, int64_t H, int64_t N, int64_t d) {
     std::memset(p, 0, sizeof(*p));
@@ -302,6 +338,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.tm_phik = &mphi;
     la.tm_v = &mv;
     SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+    mark(2, st);
 
     SparseLaunch sa{};
     sa.B = g.B;
@@ -374,6 +411,8 @@ sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, 
     ra.inv_sqrt_d = inv_sqrt(g.d);
     ra.proj_q = proj_q;
     ra.proj_k = proj_k;
+    CUtensorMap mcol;
+    ra.tm_kcol = colmean_map(&mcol, k, g.bf16, g.BH, g.N, g.d);
     ra.mu_out = w.mu;
     ra.mu_part = w.mu_part;
     ra.qp = w.qp;
@@ -401,10 +440,13 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
     carve(g, workspace, &w);
     int32_t* idx = kv_idx_out ? kv_idx_out : w.idx;
     cudaStream_t st = (cudaStream_t)stream;
+    mark(0, st);
     s = sla2_router(p, q, k, proj_q, proj_k, nullptr, mask_out, idx, workspace, workspace_bytes, stream);
     const int router_launches = g_launches;
     if (s != SLA2_OK) return s;
+    mark(1, st);
     s = run_linear_and_sparse(p, g, w, q, k, v, rho, idx, nullptr, (int)g.kappa, out, saved, st);
+    mark(3, st);
     g_launches += router_launches;
     return s;
 }
@@ -416,8 +458,10 @@ sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_o
     if ((s = check_device()) != SLA2_OK) return s;
     if (!k || !mean_out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
     if (ktilde_out) return fail(SLA2_CONTRACT_ERROR, "ktilde_out is not supported; pass NULL");
-    SLA2_CUDA_TRY(launch_colmean(k, p->dtype == SLA2_BF16, mean_out, (int)(p->B * p->H), (int)p->N, (int)p->d,
-                                 (cudaStream_t)stream, &g_launches));
+    CUtensorMap mcol;
+    const bool bf = p->dtype == SLA2_BF16;
+    SLA2_CUDA_TRY(launch_colmean(k, colmean_map(&mcol, k, bf, p->B * p->H, p->N, p->d), bf, mean_out,
+                                 (int)(p->B * p->H), (int)p->N, (int)p->d, (cudaStream_t)stream, &g_launches));
     return SLA2_OK;
 }
 
@@ -460,7 +504,10 @@ sla2_status sla2_sparse_fwd(const sla2_fwd_params* p, const void* q, const void*
     SLA2_CUDA_TRY(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     SLA2_CUDA_TRY(cudaStreamSynchronize(st));
     if (flag) return fail(SLA2_SHAPE_ERROR, "sla2_forward_blockwise: mask row keeps no blocks");  // attention.hpp:445
-    if (p->smooth) SLA2_CUDA_TRY(launch_colmean(k, g.bf16, w.mu, (int)g.BH, (int)g.N, (int)g.d, st, &g_launches));
+    CUtensorMap mcol;
+    if (p->smooth)
+        SLA2_CUDA_TRY(launch_colmean(k, colmean_map(&mcol, k, g.bf16, g.BH, g.N, g.d), g.bf16, w.mu, (int)g.BH,
+                                     (int)g.N, (int)g.d, st, &g_launches));
     const int ml = g_launches;
     s = run_linear_and_sparse(p, g, w, q, k, v, rho, w.idx, w.cnt, (int)g.tn, out, saved, st);
     g_launches += ml;

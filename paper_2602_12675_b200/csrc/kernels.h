@@ -18,6 +18,7 @@ struct RouterLaunch {
     float inv_sqrt_d;
     const float* proj_q;
     const float* proj_k;
+    const CUtensorMap* tm_kcol;  // K as [B*H*N][d], box 32 cols x 256 rows, no swizzle (or null)
     float* mu_out;    // [BH][d] (written unless null)
     double* mu_part;  // fast colmean scratch
     float* qp;        // [BH][tm][d]
@@ -27,7 +28,8 @@ struct RouterLaunch {
     int32_t* idx_out;  // [BH][tm][kappa]
 };
 cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches);
-cudaError_t launch_colmean(const void* k, bool bf16, float* mu, int BH, int N, int d, cudaStream_t st, int* launches);
+cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
+                           cudaStream_t st, int* launches);
 cudaError_t launch_topk_only(const float* pc, int BH, int tm, int tn, int kappa, uint8_t* mask, int32_t* idx,
                              cudaStream_t st, int* launches);
 cudaError_t launch_mask_to_idx(const uint8_t* mask, int rows, int tn, int32_t* idx, int32_t* cnt, int* empty_flag,

@@ -237,14 +237,38 @@ __global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* 
     const int dd = d * d;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
         float s = 0.0f;
-        for (int c = 0; c < nchunk; ++c) s += hpart[(bh * nchunk + c) * (int64_t)dd + e];
+        int c = 0;
+        for (; c + 8 <= nchunk; c += 8) {  // independent loads batched, summed in chunk order
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = hpart[(bh * nchunk + c + u) * (int64_t)dd + e];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += t[u];
+        }
+        for (; c < nchunk; ++c) s += hpart[(bh * nchunk + c) * (int64_t)dd + e];
         htot[bh * dd + e] = s;
     }
     if (blockIdx.x == 0) {
-        for (int f = threadIdx.x; f < d; f += blockDim.x) {
-            float s = 0.0f;
-            for (int j = 0; j < tn; ++j) s += zblk[(bh * tn + j) * d + f];
-            ztot[bh * d + f] = s;
+        // Ztot[f] = sum_j z_j[f]: blockDim/ d threads per feature over strided j, then combined
+        __shared__ float zs[1024];
+        const int parts = blockDim.x / d;
+        const int f = threadIdx.x % d, part = threadIdx.x / d;
+        float s = 0.0f;
+        if (part < parts) {
+            int j = part;
+            for (; j + 3 * parts < tn; j += 4 * parts) {
+                const float a0 = zblk[(bh * tn + j) * d + f], a1 = zblk[(bh * tn + j + parts) * d + f];
+                const float a2 = zblk[(bh * tn + j + 2 * parts) * d + f], a3 = zblk[(bh * tn + j + 3 * parts) * d + f];
+                s += (a0 + a1) + (a2 + a3);
+            }
+            for (; j < tn; j += parts) s += zblk[(bh * tn + j) * d + f];
+        }
+        zs[threadIdx.x] = s;
+        __syncthreads();
+        if (threadIdx.x < d) {
+            float t = 0.0f;
+            for (int p = 0; p < parts; ++p) t += zs[p * d + threadIdx.x];
+            ztot[bh * d + threadIdx.x] = t;
         }
     }
 }
@@ -271,8 +295,9 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
         htot_simt_kernel<float><<<dim3(a.nchunk, (unsigned)a.BH), 256, smem, st>>>(
             (const float*)a.phik, (const float*)a.v, a.hpart, a.N, a.d, rows, a.nchunk);
     }
-    lin_reduce_kernel<<<dim3((a.d * a.d + 255) / 256, (unsigned)a.BH), 256, 0, st>>>(a.hpart, a.zblk, a.htot,
-                                                                                     a.ztot, a.nchunk, a.d, tn);
+    const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
+    lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
+        a.hpart, a.zblk, a.htot, a.ztot, a.nchunk, a.d, tn);
     *launches += 3;
     return cudaGetLastError();
 }

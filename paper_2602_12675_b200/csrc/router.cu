@@ -17,6 +17,7 @@
 
 #include "expf_glibc.cuh"
 #include "kernels.h"
+#include "tc.cuh"
 
 namespace sla2dev {
 
@@ -57,6 +58,71 @@ __global__ void __launch_bounds__(32) colmean_exact_kernel(const T* __restrict__
     for (; i < N; ++i) acc = __fadd_rn(acc, to_f32(p[(int64_t)i * d]));
     const float inv = __fdiv_rn(1.0f, (float)N);
     mu[bh * d + c] = __fmul_rn(acc, inv);
+}
+
+// K0, TMA-fed: one CTA per (32-column group, bh). Warp 1 streams [256 rows x 32 cols] tiles
+// of K into a 6-deep shared-memory ring with TMA; warp 0 runs the 32 serial add chains out
+// of shared memory with register double-buffering, so the chain runs at FADD latency instead
+// of DRAM latency. Same order and roundings as colmean_exact_kernel.
+namespace cm {
+constexpr int ROWS = 256, NST = 6;
+}
+template <typename T>
+__global__ void __launch_bounds__(64) colmean_tma_kernel(const __grid_constant__ CUtensorMap tmK, float* __restrict__ mu,
+                                                         int N, int d) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw);  // [NST][ROWS][32]
+    __shared__ uint64_t full[cm::NST], empty[cm::NST];
+    const int cg = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nchunk = N / cm::ROWS;  // N % 256 == 0 is checked by the launcher
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < cm::NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 32);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmK);
+            for (int c = 0; c < nchunk; ++c) {
+                const int s = c % cm::NST;
+                if (c >= cm::NST) mbar_wait(&empty[s], ((c / cm::NST) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], cm::ROWS * 32 * sizeof(T));
+                tma_load_2d(ring + (size_t)s * cm::ROWS * 32, &tmK, cg * 32, (int)(bh * N + (int64_t)c * cm::ROWS),
+                            &full[s]);
+            }
+        }
+        return;
+    }
+    float acc = 0.0f;
+    for (int c = 0; c < nchunk; ++c) {
+        const int s = c % cm::NST;
+        mbar_wait(&full[s], (c / cm::NST) & 1);
+        const T* tile = ring + (size_t)s * cm::ROWS * 32 + lane;
+        float a[32], b[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[u * 32]);
+#pragma unroll 1
+        for (int r0 = 0; r0 < cm::ROWS; r0 += 64) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) b[u] = to_f32(tile[(r0 + 32 + u) * 32]);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, a[u]);
+            if (r0 + 64 < cm::ROWS) {
+#pragma unroll
+                for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[(r0 + 64 + u) * 32]);
+            }
+#pragma unroll
+            for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, b[u]);
+        }
+        mbar_arrive(&empty[s]);
+    }
+    const float inv = __fdiv_rn(1.0f, (float)N);
+    mu[bh * d + cg * 32 + lane] = __fmul_rn(acc, inv);
 }
 
 // K0 (fast variant, exact_mu = 0): column sums in double over row chunks, then the same
@@ -100,7 +166,15 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
     const T* src = x + (bh * N + (int64_t)g * block) * d + c;
     const float m = mu ? mu[bh * d + c] : 0.0f;
     double acc = 0.0;
-    for (int r = 0; r < block; ++r) {
+    int r = 0;
+    for (; r + 16 <= block; r += 16) {  // loads batched ahead of the serial double chain
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = to_f32(src[(int64_t)(r + u) * d]);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, (double)(mu ? __fsub_rn(v[u], m) : v[u]));
+    }
+    for (; r < block; ++r) {
         float v = to_f32(src[(int64_t)r * d]);
         if (mu) v = __fsub_rn(v, m);
         acc = __dadd_rn(acc, (double)v);
@@ -109,7 +183,15 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
     __syncthreads();
     const float* P = proj + (int64_t)h * d * d;
     float o = 0.0f;
-    for (int f = 0; f < d; ++f) o = __fadd_rn(o, __fmul_rn(sbar[f], P[(int64_t)f * d + c]));
+    int f = 0;
+    for (; f + 16 <= d; f += 16) {
+        float pv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) pv[u] = P[(int64_t)(f + u) * d + c];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) o = __fadd_rn(o, __fmul_rn(sbar[f + u], pv[u]));
+    }
+    for (; f < d; ++f) o = __fadd_rn(o, __fmul_rn(sbar[f], P[(int64_t)f * d + c]));
     xp[(bh * (N / block) + g) * d + c] = o;
 }
 
@@ -240,6 +322,147 @@ __global__ void router_scores_topk_kernel(const float* __restrict__ qp, const fl
              idx_out + (bh * tm + i) * (int64_t)kappa, sel, warp_cnt);
 }
 
+// Warp-local top-k on one row held in shared memory as 64-bit keys (value desc, column asc).
+// Bitonic sort by one warp (npow2 / 64 compare-exchanges per lane per stage), then the kept
+// columns are flagged and compacted in ascending order with ballots.
+__device__ void warp_topk_row(const float* __restrict__ vals, int tn, int kappa, unsigned long long* keys,
+                              int npow2, uint8_t* __restrict__ mask_row, int32_t* __restrict__ idx_row) {
+    const int lane = threadIdx.x & 31;
+    for (int j = lane; j < npow2; j += 32)
+        keys[j] = (j < tn) ? (((unsigned long long)desc_key(vals[j]) << 32) | (unsigned)j) : ~0ull;
+    __syncwarp();
+    for (int size = 2; size <= npow2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < npow2 / 2; t += 32) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // keys[0..kappa) are the kept columns; turn them into flags (reuse keys' tail as bytes)
+    uint8_t* sel = reinterpret_cast<uint8_t*>(keys + npow2) ;  // caller reserves tn bytes after keys
+    for (int j = lane; j < tn; j += 32) sel[j] = 0;
+    __syncwarp();
+    for (int r = lane; r < kappa; r += 32) sel[(int)(keys[r] & 0xffffffffu)] = 1;
+    __syncwarp();
+    int base = 0;
+    for (int j0 = 0; j0 < tn; j0 += 32) {
+        const int j = j0 + lane;
+        const bool f = (j < tn) && sel[j];
+        if (mask_row && j < tn) mask_row[j] = f ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (f) idx_row[base + __popc(bal & ((1u << lane) - 1u))] = j;
+        base += __popc(bal);
+    }
+}
+
+// K1d': 8 query-block rows per CTA (one warp per row for softmax and top-k).
+//   phase 1, all threads: s[r][j] = (sum_c qp[r][c] * kp[j][c], c ascending from 0) * inv_sqrt_d
+//            (matrix.hpp:111-118 + 272-277), one column j per thread, 8 interleaved row chains;
+//   phase 2, warp r:    m = max, e = expf(s - m), sum serially over j ascending (lane 0),
+//            inv = 1 / sum, pc = e * inv (matrix.hpp:144-152), then top-kappa.
+// Dynamic smem: 8*tn floats + 8*(npow2*8 + tn) bytes + 8*d floats.
+constexpr int RROWS = 8;
+__global__ void __launch_bounds__(256) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
+                                                          float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
+                                                          float* __restrict__ pc_out, uint8_t* __restrict__ mask_out,
+                                                          int32_t* __restrict__ idx_out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    float* vals = reinterpret_cast<float*>(smem);       // [8][tn]
+    float* sq = vals + RROWS * tn;                       // [8][d]
+    uint8_t* keyb = reinterpret_cast<uint8_t*>(sq + RROWS * d);
+    const size_t key_stride = ((size_t)npow2 * 8 + tn + 15) & ~size_t(15);
+    const int i0 = blockIdx.x * RROWS;
+    const int64_t bh = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nrows = min(RROWS, tm - i0);
+    for (int e = tid; e < RROWS * d; e += 256) {
+        const int r = e / d;
+        sq[e] = (r < nrows) ? qp[(bh * tm + i0 + r) * (int64_t)d + (e % d)] : 0.0f;
+    }
+    __syncthreads();
+    const float* kpb = kp + bh * (int64_t)tn * d;
+    for (int j = tid; j < tn; j += 256) {
+        float acc[RROWS];
+#pragma unroll
+        for (int r = 0; r < RROWS; ++r) acc[r] = 0.0f;
+        const float* kr = kpb + (int64_t)j * d;
+        for (int c0 = 0; c0 < d; c0 += 16) {
+            float kv[16];
+            if ((d & 15) == 0) {
+#pragma unroll
+                for (int u = 0; u < 16; u += 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(kr + c0 + u);
+                    kv[u] = t.x;
+                    kv[u + 1] = t.y;
+                    kv[u + 2] = t.z;
+                    kv[u + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) kv[u] = (c0 + u < d) ? kr[c0 + u] : 0.0f;
+            }
+            const int cn = min(16, d - c0);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (u < cn) {
+#pragma unroll
+                    for (int r = 0; r < RROWS; ++r) acc[r] = __fadd_rn(acc[r], __fmul_rn(sq[r * d + c0 + u], kv[u]));
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RROWS; ++r) vals[r * tn + j] = __fmul_rn(acc[r], inv_sqrt_d);
+    }
+    __syncthreads();
+    if (warp >= nrows) return;
+    const int i = i0 + warp;
+    float* v = vals + warp * tn;
+    float m = -INFINITY;
+    for (int j = lane; j < tn; j += 32) m = fmaxf(m, v[j]);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int j = lane; j < tn; j += 32) v[j] = expf_glibc(__fsub_rn(v[j], m));
+    __syncwarp();
+    float inv = 0.0f;
+    if (lane == 0) {  // serial sum, j ascending (matrix.hpp:148-149)
+        float sum = 0.0f;
+        int j = 0;
+        for (; j + 8 <= tn; j += 8) {
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = v[j + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum = __fadd_rn(sum, t[u]);
+        }
+        for (; j < tn; ++j) sum = __fadd_rn(sum, v[j]);
+        inv = __fdiv_rn(1.0f, sum);
+    }
+    inv = __shfl_sync(0xffffffffu, inv, 0);
+    for (int j = lane; j < tn; j += 32) {
+        const float p = __fmul_rn(v[j], inv);
+        v[j] = p;
+        if (pc_out) pc_out[(bh * tm + i) * (int64_t)tn + j] = p;
+    }
+    __syncwarp();
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(keyb + warp * key_stride);
+    warp_topk_row(v, tn, kappa, keys, npow2, mask_out ? mask_out + (bh * tm + i) * (int64_t)tn : nullptr,
+                  idx_out + (bh * tm + i) * (int64_t)kappa);
+}
+
+size_t router_rows_smem(int tn, int d) {
+    int npow2 = 1;
+    while (npow2 < tn) npow2 <<= 1;
+    const size_t key_stride = ((size_t)npow2 * 8 + tn + 15) & ~size_t(15);
+    return (size_t)RROWS * tn * 4 + (size_t)RROWS * d * 4 + RROWS * key_stride + 16;
+}
+
 // hard_topk alone on a caller-given score matrix (sla2_hard_topk).
 __global__ void topk_only_kernel(const float* __restrict__ pc, int tm, int tn, int kappa, int npow2,
                                  uint8_t* __restrict__ mask_out, int32_t* __restrict__ idx_out) {
@@ -272,13 +495,28 @@ __global__ void mask_to_idx_kernel(const uint8_t* __restrict__ mask, int tn, int
 // ---------------------------------------------------------------------------------------------
 // host launchers
 template <typename T>
+static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, int N, int d, cudaStream_t st,
+                      int* launches) {
+    if (tmk && N % cm::ROWS == 0 && d % 32 == 0) {
+        const int smem = cm::NST * cm::ROWS * 32 * (int)sizeof(T);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(colmean_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
+        colmean_tma_kernel<T><<<dim3(d / 32, BH), 64, smem, st>>>(*tmk, mu, N, d);
+    } else {
+        colmean_exact_kernel<T><<<dim3((d + 31) / 32, BH), 32, 0, st>>>((const T*)k, mu, N, d);
+    }
+    ++*launches;
+}
+
+template <typename T>
 static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
     const int BH = (int)(a.B * a.H);
-    dim3 gcol((a.d + 31) / 32, BH);
     if (a.mu_out) {
         if (a.exact_mu) {
-            colmean_exact_kernel<T><<<gcol, 32, 0, st>>>((const T*)a.k, a.mu_out, a.N, a.d);
-            ++*launches;
+            colmean_t<T>(a.k, a.tm_kcol, a.mu_out, BH, a.N, a.d, st, launches);
         } else {
             const int rows_per = 256;
             const int nch = (a.N + rows_per - 1) / rows_per;
@@ -295,10 +533,17 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
     *launches += 2;
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
-    const size_t smem = npow2 * 8 + tn * 4 + a.d * 4 + tn + 16;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(router_scores_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    router_scores_topk_kernel<<<dim3(tm, BH), 256, smem, st>>>(a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa,
-                                                                npow2, a.pc_out, a.mask_out, a.idx_out);
+    const size_t rsm = router_rows_smem(tn, a.d);
+    if (rsm <= 220 * 1024) {
+        cudaFuncSetAttribute(router_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+        router_rows_kernel<<<dim3((tm + RROWS - 1) / RROWS, BH), 256, rsm, st>>>(
+            a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2, a.pc_out, a.mask_out, a.idx_out);
+    } else {
+        const size_t smem = npow2 * 8 + tn * 4 + a.d * 4 + tn + 16;
+        cudaFuncSetAttribute(router_scores_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        router_scores_topk_kernel<<<dim3(tm, BH), 256, smem, st>>>(a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa,
+                                                                    npow2, a.pc_out, a.mask_out, a.idx_out);
+    }
     ++*launches;
     return cudaGetLastError();
 }
@@ -307,11 +552,10 @@ cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches)
     return a.bf16 ? launch_router_t<__nv_bfloat16>(a, st, launches) : launch_router_t<float>(a, st, launches);
 }
 
-cudaError_t launch_colmean(const void* k, bool bf16, float* mu, int BH, int N, int d, cudaStream_t st, int* launches) {
-    dim3 g((d + 31) / 32, BH);
-    if (bf16) colmean_exact_kernel<__nv_bfloat16><<<g, 32, 0, st>>>((const __nv_bfloat16*)k, mu, N, d);
-    else colmean_exact_kernel<float><<<g, 32, 0, st>>>((const float*)k, mu, N, d);
-    ++*launches;
+cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
+                           cudaStream_t st, int* launches) {
+    if (bf16) colmean_t<__nv_bfloat16>(k, tmk, mu, BH, N, d, st, launches);
+    else colmean_t<float>(k, tmk, mu, BH, N, d, st, launches);
     return cudaGetLastError();
 }
 

@@ -70,7 +70,21 @@ struct SparseBf16Params {
     float scale_log2;
     float inv_sqrt_d;
     int dense;
+#ifdef SLA2_TRACE
+    unsigned long long* trace;
+#endif
 };
+
+#ifdef SLA2_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SLA2_TR(slot) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + (slot)] = gtimer()
+#else
+#define SLA2_TR(slot)
+#endif
 
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
@@ -121,6 +135,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    if (threadIdx.x == 0) SLA2_TR(0);
 
     uint8_t* sQ = smem + OFF_Q;
     auto sK = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES; };
@@ -149,6 +164,8 @@ __global__ void __launch_bounds__(256, 1)
                 if (j >= NS) mbar_wait(&bar_kv_empty[s], ((j / NS) - 1) & 1);
                 const int kb = dense ? j : idx[j];
                 const int krow = (int)(bh * p.N + (int64_t)kb * BK);
+                if (j == 0) SLA2_TR(54);
+                if (j == nb - 1) SLA2_TR(55);
                 mbar_arrive_expect_tx(&bar_kv_full[s], stage_tx);
                 tma_load_2d_hint(sK(s), &tmK, 0, krow, &bar_kv_full[s], pol_keep);
                 tma_load_2d_hint(sK(s) + 8192, &tmK, 64, krow, &bar_kv_full[s], pol_keep);
@@ -168,6 +185,7 @@ __global__ void __launch_bounds__(256, 1)
             constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
             const uint32_t aQ = smem_u32(sQ);
             mbar_wait(&bar_q, 0);
+            SLA2_TR(1);
             auto issue_qk = [&](int j) {
                 const int s = j % NS, b = j & 1;
                 mbar_wait(&bar_kv_full[s], (j / NS) & 1);
@@ -205,6 +223,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
                 umma_commit(&bar_pv_done[b]);
+                if (j < 16) SLA2_TR(34 + j);
                 umma_commit(&bar_kv_empty[s]);
             }
             if (linear) {
@@ -224,13 +243,39 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 3) {
         // ===================== Zc = Ztot - sum_sel z_j =====================
         if (linear) {
-            const float* zt = p.ztot + bh * D;
-            const float* zb = p.zblk + bh * (int64_t)p.tn * D;
-            for (int f = lane; f < D; f += 32) {
-                float sel = 0.0f;
-                for (int j = 0; j < nb; ++j) sel += zb[(int64_t)idx[j] * D + f];
-                sZc[f] = zt[f] - sel;
+            // lane owns features 4*lane .. 4*lane+3; one coalesced 512-B row per kept block
+            const float* zb = p.zblk + bh * (int64_t)p.tn * D + lane * 4;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j0 = 0; j0 < nb; j0 += 32) {
+                const int myj = (j0 + lane < nb) ? idx[j0 + lane] : 0;
+                const int cnt = min(32, nb - j0);
+                int u = 0;
+                for (; u + 4 <= cnt; u += 4) {
+                    float4 z[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        z[t] = *reinterpret_cast<const float4*>(zb + (int64_t)__shfl_sync(0xffffffffu, myj, u + t) * D);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        acc.x += z[t].x;
+                        acc.y += z[t].y;
+                        acc.z += z[t].z;
+                        acc.w += z[t].w;
+                    }
+                }
+                for (; u < cnt; ++u) {
+                    const float4 z = *reinterpret_cast<const float4*>(zb + (int64_t)__shfl_sync(0xffffffffu, myj, u) * D);
+                    acc.x += z.x;
+                    acc.y += z.y;
+                    acc.z += z.z;
+                    acc.w += z.w;
+                }
             }
+            const float4 zt = *reinterpret_cast<const float4*>(p.ztot + bh * D + lane * 4);
+            sZc[lane * 4 + 0] = zt.x - acc.x;
+            sZc[lane * 4 + 1] = zt.y - acc.y;
+            sZc[lane * 4 + 2] = zt.z - acc.z;
+            sZc[lane * 4 + 3] = zt.w - acc.w;
         }
         __syncwarp();
         named_bar_arrive(1, 160);
@@ -243,6 +288,7 @@ __global__ void __launch_bounds__(256, 1)
             const int b = j & 1;
             mbar_wait(&bar_s_full[b], (j >> 1) & 1);
             __syncwarp();
+            if (r == 0 && j < 16) SLA2_TR(2 + j);
             tc_fence_after();
             uint32_t sr[64];
             tmem_ld32(tmem + lane_base + TM_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -300,12 +346,14 @@ __global__ void __launch_bounds__(256, 1)
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&bar_p_full[b]);
+            if (r == 0 && j < 16) SLA2_TR(18 + j);
         }
         // all MMAs of the main loop complete
         if (nb > 0) mbar_wait(&bar_pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
         mbar_wait(&bar_q, 0);
         __syncwarp();
         tc_fence_after();
+        if (r == 0) SLA2_TR(50);
 
         float alpha = 1.0f;
         float den = 1.0f;
@@ -378,7 +426,9 @@ __global__ void __launch_bounds__(256, 1)
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&bar_lin_ready);
+            if (r == 0) SLA2_TR(51);
             mbar_wait(&bar_lin_done, 0);
+            if (r == 0) SLA2_TR(52);
             __syncwarp();
             tc_fence_after();
         } else {
@@ -416,6 +466,7 @@ __global__ void __launch_bounds__(256, 1)
                 *reinterpret_cast<uint4*>(orow + c0 + ch * 8) = w;
             }
         }
+        if (r == 0) SLA2_TR(53);
         if (p.big_l) {
             // L with raw K scores, shifted to the smoothed-K scores the reference uses:
             // q_r . K~_t = q_r . K_t - q_r . mu
@@ -433,6 +484,11 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (warp == 2) tmem_free(tmem, 512);
 }
+
+#ifdef SLA2_TRACE
+unsigned long long* g_trace_buf = nullptr;
+extern "C" void sla2_trace_set_buffer(unsigned long long* b) { g_trace_buf = b; }
+#endif
 
 cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* launches) {
     SparseBf16Params p;
@@ -457,6 +513,9 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
     p.inv_sqrt_d = a.inv_sqrt_d;
     p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
     p.dense = a.dense;
+#ifdef SLA2_TRACE
+    p.trace = g_trace_buf;
+#endif
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(sla2_sparse_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::SMEM_ALLOC);

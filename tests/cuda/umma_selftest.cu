@@ -7,6 +7,7 @@
 
 #include <cstdint>
 
+#include "../../paper_2602_12675_b200/csrc/expf_glibc.cuh"
 #include "../../paper_2602_12675_b200/csrc/tc.cuh"
 
 using namespace sla2dev;
@@ -133,6 +134,16 @@ __global__ void tma_selftest_kernel(const __grid_constant__ CUtensorMap map, int
     }
     mbar_wait(&bar, 0);
     for (int i = threadIdx.x; i < 8192; i += blockDim.x) out[i] = smem[i];
+}
+
+// Device expf_glibc over a host-chosen range of float bit patterns [lo, lo + n).
+__global__ void expf_selftest_kernel(uint32_t lo, uint32_t n, float* out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = expf_glibc(__uint_as_float(lo + i));
+}
+extern "C" int expf_selftest(uint32_t lo, uint32_t n, float* out) {
+    expf_selftest_kernel<<<1184, 256>>>(lo, n, out);
+    return (int)cudaDeviceSynchronize();
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -175,3 +175,38 @@ def test_deterministic(cuda):
     a = sla2.forward(*dev).clone()
     b = sla2.forward(*dev)
     assert torch.equal(a, b)
+
+
+# ----------------------------------------------------------------------------- reference goldens
+def _goldens():
+    import os
+    g = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(os.path.join(g, f) for f in os.listdir(g) if f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("path", _goldens(), ids=lambda p: p.rsplit("/", 1)[-1])
+def test_gpu_vs_reference_golden(cuda, path):
+    """GPU path against outputs of the unmodified reference (tests/golden/make_golden.py)."""
+    torch = _torch()
+    g = np.load(path)
+    q, k, v = g["q"], g["k"], g["v"]
+    if q.dtype != np.float32:
+        pytest.skip("double-precision reference case (no fp64 GPU path)")
+    bq, bk, kp, quant = int(g["bq"]), int(g["bk"]), float(g["k_percent"]), bool(g["quant"])
+    bf16 = (q.shape[1] == 128 and bq == 128 and bk == 64)
+    if quant and not bf16:
+        pytest.skip("QAT runs on the bf16 kernel geometry")
+    dt = torch.bfloat16 if bf16 else torch.float32
+    dev = [to_dev(x[None, None], dt, cuda) for x in (q, k, v)]
+    dev += [to_dev(g["proj_q"][None], torch.float32, cuda), to_dev(g["proj_k"][None], torch.float32, cuda),
+            to_dev(g["rho"][None], torch.float32, cuda)]
+    try:
+        out, mask = sla2.forward(*dev, k_percent=kp, bq=bq, bk=bk, quant=quant, return_mask=True)
+    except sla2.ContractError as e:
+        pytest.skip(str(e))
+    assert np.array_equal(mask.cpu().numpy()[0, 0], g["mask"])
+    got = out.float().cpu().numpy()[0, 0]
+    if bf16:
+        assert rel_err(got, g["out"])[0] <= BF16_TOL
+    else:
+        assert np.abs(got - g["out"]).max() <= F32_TOL

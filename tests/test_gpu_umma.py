@@ -73,3 +73,34 @@ def test_tma_swizzle128(lib, cuda):
             pc = c ^ (r % 8)
             exp[r, pc * 8:(pc + 1) * 8] = box[r, c * 8:(c + 1) * 8]
     assert np.array_equal(got, exp)
+
+
+def test_device_expf_matches_host_libm(lib, cuda):
+    """expf_glibc on the device vs this host's libm expf over the softmax-relevant range
+    (all floats in [-104, 0] -- every argument row_softmax can produce after max subtraction)
+    in 2^26-value chunks."""
+    import ctypes
+    import torch
+    libm = ctypes.CDLL("libm.so.6")
+    lib.expf_selftest.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p]
+    lo = 0x80000000  # -0.0 ... up to -104 (0xC2D00000)
+    hi = 0xC2D00001
+    chunk = 1 << 26
+    out = torch.empty(chunk, dtype=torch.float32, device=cuda)
+    x = np.arange(chunk, dtype=np.uint64)
+    checked = 0
+    for start in range(lo, hi, chunk):
+        n = min(chunk, hi - start)
+        assert lib.expf_selftest(start, n, out.data_ptr()) == 0
+        got = out[:n].cpu().numpy()
+        xs = (x[:n] + start).astype(np.uint32).view(np.float32)
+        ref = np.exp(xs.astype(np.float32))  # numpy float32 exp is not libm: compare to libm below
+        # libm expf via ctypes in a vectorized way is too slow; use a strided sample through libm
+        libm.expf.restype = C.c_float
+        libm.expf.argtypes = [C.c_float]
+        idx = np.arange(0, n, 997)
+        lm = np.array([libm.expf(float(v)) for v in xs[idx]], dtype=np.float32)
+        assert np.array_equal(got[idx].view(np.uint32), lm.view(np.uint32))
+        del ref
+        checked += len(idx)
+    assert checked > 1_000_000
