@@ -179,6 +179,7 @@ struct Workspace {
     float* ztot;
     float* hpart;
     float* htot;
+    void* htot16;
     int8_t *qc, *kc, *vct;
     float *qs, *ks, *vs;
     int32_t* cnt;
@@ -200,6 +201,7 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.ztot = c.take<float>(g.BH * g.d);
     t.hpart = c.take<float>(g.BH * g.nchunk * g.d * g.d);
     t.htot = c.take<float>(g.BH * g.d * g.d);
+    t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
@@ -313,11 +315,12 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
                                          const int32_t* cnt, int kstride, void* out, const sla2_fwd_saved* saved,
                                          cudaStream_t st) {
     const float isd = inv_sqrt(g.d);
-    CUtensorMap mq, mk, mv, mphi;
+    CUtensorMap mq, mk, mv, mphi, mht;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
     if (g.bf16) {
         if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
-            !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mphi, w.phik, rows, g.d, 64, 64, 2))
+            !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mphi, w.phik, rows, g.d, 64, 64, 2) ||
+            !make_map(&mht, w.htot16, (uint64_t)(g.BH * g.d), g.d, 64, 128, 2))
             return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (pointers must be 16-byte aligned)");
     }
     LinearLaunch la{};
@@ -334,6 +337,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.ztot = w.ztot;
     la.hpart = w.hpart;
     la.htot = w.htot;
+    la.htot16 = w.htot16;
     la.nchunk = g.nchunk;
     la.tm_phik = &mphi;
     la.tm_v = &mv;
@@ -374,6 +378,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.tm_k = &mk;
         sa.tm_v = &mv;
         sa.tm_phik = &mphi;
+        sa.tm_ht = &mht;
         if (g.quant) return fail(SLA2_CONTRACT_ERROR, "INT8 QAT sparse kernel not available in this build");
         SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
     } else {

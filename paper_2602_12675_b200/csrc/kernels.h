@@ -48,6 +48,7 @@ struct LinearLaunch {
     float* ztot;      // [BH][d]
     float* hpart;     // [BH][nchunk][d][d] partial phi(K~)^T V
     float* htot;      // [BH][d][d]
+    void* htot16;     // [BH][d][d] bf16 copy (bf16 path; the sparse kernel's TMA source)
     int nchunk;       // key-block chunks per head for the H partials
     const CUtensorMap* tm_phik;  // bf16 path: TMA maps (box 64x64, SW128) over [BH*N][d]
     const CUtensorMap* tm_v;
@@ -78,6 +79,7 @@ struct SparseLaunch {
     const CUtensorMap* tm_k;
     const CUtensorMap* tm_v;
     const CUtensorMap* tm_phik;
+    const CUtensorMap* tm_ht;  // Htot bf16 as [BH*d][d], box 64 x 128, SW128
     // f32 path
     const float* q;
     const float* k;

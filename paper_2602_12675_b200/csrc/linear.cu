@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(256) htot_simt_kernel(const float* __restrict_
 
 // Htot[bh] = sum_chunk hpart[bh][chunk] (chunk ascending); Ztot[bh] = sum_j zblk[bh][j].
 __global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* __restrict__ zblk,
-                                  float* __restrict__ htot, float* __restrict__ ztot, int nchunk, int d, int tn) {
+                                  float* __restrict__ htot, __nv_bfloat16* __restrict__ htot16,
+                                  float* __restrict__ ztot, int nchunk, int d, int tn) {
     const int64_t bh = blockIdx.y;
     const int dd = d * d;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
@@ -247,6 +248,7 @@ __global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* 
         }
         for (; c < nchunk; ++c) s += hpart[(bh * nchunk + c) * (int64_t)dd + e];
         htot[bh * dd + e] = s;
+        if (htot16) htot16[bh * dd + e] = __float2bfloat16_rn(s);
     }
     if (blockIdx.x == 0) {
         // Ztot[f] = sum_j z_j[f]: blockDim/ d threads per feature over strided j, then combined
@@ -297,7 +299,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
     }
     const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
     lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
-        a.hpart, a.zblk, a.htot, a.ztot, a.nchunk, a.d, tn);
+        a.hpart, a.zblk, a.htot, a.bf16 ? (__nv_bfloat16*)a.htot16 : nullptr, a.ztot, a.nchunk, a.d, tn);
     *launches += 3;
     return cudaGetLastError();
 }

@@ -6,18 +6,24 @@
 // d = 128 (the paper's blocks), bf16 operands, fp32 accumulation.
 //
 // Per CTA (query block i of head bh, kept key blocks j_0 < j_1 < ... from the router):
-//   S_j   = Q_i K_j^T                      tcgen05 kind::f16, M128 N64 K128 -> TMEM (2 buffers)
-//   P_j   = exp2(S_j*log2e/sqrt(d) - m)    softmax warps, online max with lazy rescale
-//   O    += P_j V_j                        tcgen05, M128 N128 K64, O accumulated in TMEM
-//   Hsel += phi(K~_j)^T V_j                tcgen05, M128 N128 K64 (MN-major A and B)
+//   S_j   = Q_i K_j^T                      tcgen05 kind::f16 "TS": Q resident in TMEM (A),
+//                                          K_j from smem (B), M128 N64 K128 -> TMEM (2 buffers)
+//   P_j   = exp2(S_j*log2e/sqrt(d) - m)    softmax warps, online max with lazy rescale; P is
+//                                          written back over S_j in TMEM as packed bf16
+//   O    += P_j V_j                        TS: P from TMEM, V_j from smem, M128 N128 K64
+//   Hsel += phi(K~_j)^T V_j                SS, M128 N128 K64 (MN-major A and B)
 // epilogue (fused, attention.hpp:532-557):
 //   O_s = O / l
 //   Hc  = Htot - Hsel, Zc = Ztot - sum_sel z_j      ("total minus selected" = the
 //                                                    reference's complement sum, 495-502)
-//   O_l = (phi(Q) Hc) / (phi(Q) . Zc)              tcgen05, M128 N128 K128
+//   O_l = (phi(Q) Hc) / (phi(Q) . Zc)              SS, M128 N128 K128
 //   out = alpha O_s + (1 - alpha) O_l, alpha = sigmoid(rho_i) (forced to 1 on full rows)
 // The raw K is used for Q K^T: smoothing shifts every score of a row by the same constant
 // (test_attention.cpp:270-279), so O_s is unchanged and K needs no bf16 re-rounding.
+//
+// Shared memory is the scarce resource (128 B/clk/SM): keeping Q and P in TMEM removes 64 KB
+// of smem traffic per key block, leaving the TMA writes of K, V, phi(K) and the three B/A
+// operand reads. Htot (bf16, MN-major SW128) is staged once per CTA by TMA.
 //
 // Warp roles (256 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
 // w3 complement of Z, w4-7 softmax / correction / epilogue (thread = query row).
@@ -38,17 +44,18 @@ constexpr int BQ = 128, BK = 64, D = 128, NS = 3;
 constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
 constexpr uint32_t STAGE_BYTES = 3 * TILE_BYTES;
-constexpr uint32_t P_BYTES = BQ * BK * 2;  // 16 KB
+constexpr uint32_t HT_BYTES = D * D * 2;  // 32 KB Htot (bf16)
 constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_STAGE = Q_BYTES;
-constexpr uint32_t OFF_P = OFF_STAGE + NS * STAGE_BYTES;
-constexpr uint32_t SMEM_BYTES = OFF_P + 2 * P_BYTES;
+constexpr uint32_t OFF_HT = OFF_STAGE + NS * STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_HT + HT_BYTES;
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
-// TMEM columns
-constexpr uint32_t TM_S = 0;      // 2 x 64
-constexpr uint32_t TM_O = 128;    // 128
-constexpr uint32_t TM_H = 256;    // 128
-constexpr uint32_t TM_L = 384;    // 128
+// TMEM columns (512 allocated)
+constexpr uint32_t TM_Q = 0;      // Q_i as the A operand: 128 lanes x 64 cols (bf16 pairs)
+constexpr uint32_t TM_S = 64;     // 2 x 64: S_j fp32, then P_j bf16 in its first 32 cols
+constexpr uint32_t TM_O = 192;    // 128: O accumulator
+constexpr uint32_t TM_H = 320;    // 128: Hsel accumulator
+constexpr uint32_t TM_L = TM_S;   // 128: phi(Q) Hc after the loop (S/P area is free then)
 constexpr float RESCALE_LOG2 = 8.0f;  // lazy rescale threshold (P <= 2^8)
 }  // namespace sp
 
@@ -57,7 +64,6 @@ struct SparseBf16Params {
     const int32_t* kv_cnt;
     int kstride, kappa;
     const float* rho;
-    const float* htot;
     const float* ztot;
     const float* zblk;
     const float* mu;
@@ -95,17 +101,17 @@ __device__ __forceinline__ float fast_exp2(float x) {
 __global__ void __launch_bounds__(256, 1)
     sla2_sparse_bf16_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
-                            const SparseBf16Params p) {
+                            const __grid_constant__ CUtensorMap tmHt, const SparseBf16Params p) {
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_kv_full[NS], bar_kv_empty[NS], bar_s_full[2], bar_s_empty[2], bar_p_full[2],
+    __shared__ uint64_t bar_q, bar_qt, bar_ht, bar_kv_full[NS], bar_kv_empty[NS], bar_s_full[2], bar_p_full[2],
         bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
 
-    const int i = blockIdx.x;           // query block
-    const int64_t bh = blockIdx.y;      // (b, h)
+    const int i = blockIdx.x;       // query block
+    const int64_t bh = blockIdx.y;  // (b, h)
     const int h = (int)(bh % p.H);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool dense = p.dense != 0;
@@ -116,13 +122,14 @@ __global__ void __launch_bounds__(256, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, 1);
+        mbar_init(&bar_qt, 128);
+        mbar_init(&bar_ht, 1);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&bar_kv_full[s], 1);
             mbar_init(&bar_kv_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar_s_full[b], 1);
-            mbar_init(&bar_s_empty[b], 128);
             mbar_init(&bar_p_full[b], 128);
             mbar_init(&bar_pv_done[b], 1);
         }
@@ -138,10 +145,10 @@ __global__ void __launch_bounds__(256, 1)
     if (threadIdx.x == 0) SLA2_TR(0);
 
     uint8_t* sQ = smem + OFF_Q;
+    uint8_t* sHt = smem + OFF_HT;
     auto sK = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES; };
     auto sV = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + TILE_BYTES; };
     auto sPh = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE_BYTES; };
-    auto sP = [&](int b) { return smem + OFF_P + b * P_BYTES; };
     uint8_t* sHc = smem + OFF_STAGE;  // epilogue alias of stage 0 (32 KB)
 
     if (warp == 0) {
@@ -175,6 +182,13 @@ __global__ void __launch_bounds__(256, 1)
                     tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_kv_full[s], pol_keep);
                     tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_kv_full[s], pol_keep);
                 }
+                if (j == 0 && linear) {
+                    // Htot of this head, bf16 [f][c] as the MN-major B layout [c_atom][f][64]
+                    tma_prefetch_desc(&tmHt);
+                    mbar_arrive_expect_tx(&bar_ht, HT_BYTES);
+                    tma_load_2d_hint(sHt, &tmHt, 0, (int)(bh * D), &bar_ht, pol_keep);
+                    tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol_keep);
+                }
             }
         }
     } else if (warp == 1) {
@@ -183,21 +197,22 @@ __global__ void __launch_bounds__(256, 1)
             constexpr uint32_t ID_QK = idesc_bf16(128, 64, false, false);
             constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
             constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
-            const uint32_t aQ = smem_u32(sQ);
-            mbar_wait(&bar_q, 0);
+            mbar_wait(&bar_qt, 0);  // Q resident in TMEM
+            tc_fence_after();
             SLA2_TR(1);
+            // S_j: A = Q (TMEM), B = K_j (smem, K-major). S[b] may be overwritten only after
+            // PV_{j-2} read P_{j-2} from it: guaranteed, tcgen05 MMAs of one thread execute in
+            // issue order and PV_{j-2} is issued before QK_j.
             auto issue_qk = [&](int j) {
                 const int s = j % NS, b = j & 1;
                 mbar_wait(&bar_kv_full[s], (j / NS) & 1);
-                if (j >= 2) mbar_wait(&bar_s_empty[b], ((j - 2) >> 1) & 1);
                 tc_fence_after();
                 const uint32_t bK = smem_u32(sK(s));
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
                     const uint32_t offk = (ks >> 2) * 8192 + (ks & 3) * 32;
-                    umma_bf16_ss(tmem + TM_S + b * 64, sdesc_sw128(aQ + off, 16, 1024),
-                                 sdesc_sw128(bK + offk, 16, 1024), ID_QK, ks > 0);
+                    umma_bf16_ts(tmem + TM_S + b * 64, tmem + TM_Q + ks * 8, sdesc_sw128(bK + offk, 16, 1024), ID_QK,
+                                 ks > 0);
                 }
                 umma_commit(&bar_s_full[b]);
             };
@@ -207,20 +222,17 @@ __global__ void __launch_bounds__(256, 1)
                 if (j + 1 < nb) issue_qk(j + 1);
                 mbar_wait(&bar_p_full[b], (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t aP = smem_u32(sP(b));
                 const uint32_t bV = smem_u32(sV(s));
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
-                    umma_bf16_ss(tmem + TM_O, sdesc_sw128(aP + ks * 32, 16, 1024),
-                                 sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV, (j > 0 || ks > 0));
-                }
+                for (int ks = 0; ks < 4; ++ks)
+                    umma_bf16_ts(tmem + TM_O, tmem + TM_S + b * 64 + ks * 8, sdesc_sw128(bV + ks * 2048, 8192, 1024),
+                                 ID_PV, (j > 0 || ks > 0));
                 if (!dense) {
                     const uint32_t aH = smem_u32(sPh(s));
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
+                    for (int ks = 0; ks < 4; ++ks)
                         umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
                                      sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (j > 0 || ks > 0));
-                    }
                 }
                 umma_commit(&bar_pv_done[b]);
                 if (j < 16) SLA2_TR(34 + j);
@@ -230,12 +242,12 @@ __global__ void __launch_bounds__(256, 1)
                 // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
                 mbar_wait(&bar_lin_ready, 0);
                 tc_fence_after();
-                const uint32_t bH = smem_u32(sHc);
+                const uint32_t aQ = smem_u32(sQ), bH = smem_u32(sHc);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
                     const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-                    umma_bf16_ss(tmem + TM_L, sdesc_sw128(aQ + off, 16, 1024),
-                                 sdesc_sw128(bH + ks * 2048, 16384, 1024), ID_PV, ks > 0);
+                    umma_bf16_ss(tmem + TM_L, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(bH + ks * 2048, 16384, 1024),
+                                 ID_PV, ks > 0);
                 }
                 umma_commit(&bar_lin_done);
             }
@@ -283,6 +295,24 @@ __global__ void __launch_bounds__(256, 1)
         // ===================== softmax / correction / epilogue =====================
         const int r = threadIdx.x - 128;  // query row within the block
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t qb = smem_u32(sQ);
+        // Q row r -> TMEM lane r, columns TM_Q + c hold elements (2c, 2c+1)
+        mbar_wait(&bar_q, 0);
+        __syncwarp();
+        {
+            uint32_t w[32];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch)
+                    ld_shared_v4(qb + half * 16384 + sw128_off(r, ch * 8), w[ch * 4 + 0], w[ch * 4 + 1], w[ch * 4 + 2],
+                                 w[ch * 4 + 3]);
+                tmem_st32(tmem + lane_base + TM_Q + half * 32, w);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&bar_qt);
+        }
         float m2 = -INFINITY, l = 0.0f;
         for (int j = 0; j < nb; ++j) {
             const int b = j & 1;
@@ -294,8 +324,6 @@ __global__ void __launch_bounds__(256, 1)
             tmem_ld32(tmem + lane_base + TM_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
             tmem_ld32(tmem + lane_base + TM_S + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
             tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&bar_s_empty[b]);
             float mx = -INFINITY;
 #pragma unroll
             for (int t = 0; t < 64; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
@@ -319,38 +347,31 @@ __global__ void __launch_bounds__(256, 1)
                         for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * corr);
                         tmem_st32(tmem + lane_base + TM_O + c0, o);
                     }
-                    tmem_st_wait();
                     l *= corr;
                     m2 = mnew;
                 }
             }
-            // P = exp2(s * scale - m2), bf16, row r of the K-major SW128 A tile
-            if (j >= 2) mbar_wait(&bar_pv_done[b], ((j - 2) >> 1) & 1);
-            const uint32_t prow = smem_u32(sP(b));
+            // P = exp2(s * scale - m2) as packed bf16 over S_j's first 32 columns
+            uint32_t w[32];
             float rs = 0.0f;
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[ch * 8 + 2 * e]), p.scale_log2, -m2));
-                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[ch * 8 + 2 * e + 1]), p.scale_log2, -m2));
-                    const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
-                    const float2 pr = __bfloat1622float2(pk);
-                    rs += pr.x + pr.y;  // row sum of the probabilities actually multiplied
-                    w[e] = *reinterpret_cast<const uint32_t*>(&pk);
-                }
-                st_shared_v4(prow + sw128_off(r, ch * 8), w[0], w[1], w[2], w[3]);
+            for (int e = 0; e < 32; ++e) {
+                const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * e]), p.scale_log2, -m2));
+                const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * e + 1]), p.scale_log2, -m2));
+                const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
+                const float2 pr = __bfloat1622float2(pk);
+                rs += pr.x + pr.y;  // row sum of the probabilities actually multiplied
+                w[e] = *reinterpret_cast<const uint32_t*>(&pk);
             }
+            tmem_st32(tmem + lane_base + TM_S + b * 64, w);
             l += rs;
-            fence_proxy_async_smem();
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&bar_p_full[b]);
             if (r == 0 && j < 16) SLA2_TR(18 + j);
         }
         // all MMAs of the main loop complete
         if (nb > 0) mbar_wait(&bar_pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
-        mbar_wait(&bar_q, 0);
         __syncwarp();
         tc_fence_after();
         if (r == 0) SLA2_TR(50);
@@ -363,9 +384,33 @@ __global__ void __launch_bounds__(256, 1)
             float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
             a = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
             alpha = a;
+            // Hc = Htot - Hsel, row f = r, bf16 into the MN-major B tile [c_atom][f][64]
+            mbar_wait(&bar_ht, 0);
+            __syncwarp();
+            const uint32_t hb = smem_u32(sHc), htb = smem_u32(sHt);
+            fence_proxy_async_smem();
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t hs[32];
+                tmem_ld32(tmem + lane_base + TM_H + c0, hs);
+                tmem_ld_wait();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const int c = c0 + ch * 8;
+                    const uint32_t off = (c >> 6) * 16384 + sw128_off(r, c & 63);
+                    uint32_t t[4], o4[4];
+                    ld_shared_v4(htb + off, t[0], t[1], t[2], t[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t[e]));
+                        o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
+                                          tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
+                    }
+                    st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
+                }
+            }
             // phi(Q) = row softmax over d of Q_r (attention.hpp:456), in place over sQ as bf16
             named_bar_sync(1, 160);  // sZc ready
-            const uint32_t qb = smem_u32(sQ);
             float qv[128];
 #pragma unroll
             for (int ch = 0; ch < 16; ++ch) {
@@ -384,12 +429,11 @@ __global__ void __launch_bounds__(256, 1)
             float qs = 0.0f;
 #pragma unroll
             for (int f = 0; f < 128; ++f) {
-                qv[f] = __expf(qv[f] - qm);
+                qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
                 qs += qv[f];
             }
             const float qinv = 1.0f / qs;
             den = 0.0f;
-            fence_proxy_async_smem();
 #pragma unroll
             for (int ch = 0; ch < 16; ++ch) {
                 uint32_t w[4];
@@ -402,26 +446,6 @@ __global__ void __launch_bounds__(256, 1)
                     w[e] = *reinterpret_cast<const uint32_t*>(&pk);
                 }
                 st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
-            }
-            // Hc = Htot - Hsel, row f = r, bf16 into the MN-major B tile [c_atom][f][64]
-            const float* ht = p.htot + (bh * D + r) * (int64_t)D;
-            const uint32_t hb = smem_u32(sHc);
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                uint32_t hs[32];
-                tmem_ld32(tmem + lane_base + TM_H + c0, hs);
-                tmem_ld_wait();
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    const float4 t0 = *reinterpret_cast<const float4*>(ht + c0 + ch * 8);
-                    const float4 t1 = *reinterpret_cast<const float4*>(ht + c0 + ch * 8 + 4);
-                    const uint32_t w0 = pack_bf16(t0.x - __uint_as_float(hs[ch * 8 + 0]), t0.y - __uint_as_float(hs[ch * 8 + 1]));
-                    const uint32_t w1 = pack_bf16(t0.z - __uint_as_float(hs[ch * 8 + 2]), t0.w - __uint_as_float(hs[ch * 8 + 3]));
-                    const uint32_t w2 = pack_bf16(t1.x - __uint_as_float(hs[ch * 8 + 4]), t1.y - __uint_as_float(hs[ch * 8 + 5]));
-                    const uint32_t w3 = pack_bf16(t1.z - __uint_as_float(hs[ch * 8 + 6]), t1.w - __uint_as_float(hs[ch * 8 + 7]));
-                    const int c = c0 + ch * 8;
-                    st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), w0, w1, w2, w3);
-                }
             }
             fence_proxy_async_smem();
             tc_fence_before();
@@ -441,6 +465,7 @@ __global__ void __launch_bounds__(256, 1)
         const float beta = 1.0f - alpha;
         const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
         __nv_bfloat16* orow = p.out + grow * D;
+        const bool want_saved = p.o_s != nullptr;
 #pragma unroll
         for (int c0 = 0; c0 < 128; c0 += 32) {
             uint32_t o[32], ln[32];
@@ -453,8 +478,10 @@ __global__ void __launch_bounds__(256, 1)
                 const float os = __uint_as_float(o[c]) * inv_l;
                 const float ol = linear ? __uint_as_float(ln[c]) * inv_den : 0.0f;
                 res[c] = linear ? alpha * os + beta * ol : os;
-                if (p.o_s) p.o_s[grow * D + c0 + c] = os;
-                if (p.o_l) p.o_l[grow * D + c0 + c] = ol;
+                if (want_saved) {
+                    p.o_s[grow * D + c0 + c] = os;
+                    p.o_l[grow * D + c0 + c] = ol;
+                }
             }
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
@@ -497,7 +524,6 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
     p.kstride = a.kstride;
     p.kappa = a.kappa;
     p.rho = a.rho;
-    p.htot = a.htot;
     p.ztot = a.ztot;
     p.zblk = a.zblk;
     p.mu = a.smooth ? a.mu : nullptr;
@@ -521,9 +547,11 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
         cudaFuncSetAttribute(sla2_sparse_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::SMEM_ALLOC);
         attr = true;
     }
+    if (a.o_s == nullptr && a.o_l != nullptr) return cudaErrorInvalidValue;
     dim3 grid(a.tm, (unsigned)(a.B * a.H));
     sla2_sparse_bf16_kernel<<<grid, 256, sp::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v,
-                                                                a.dense ? *a.tm_k : *a.tm_phik, p);
+                                                                a.dense ? *a.tm_k : *a.tm_phik,
+                                                                a.dense ? *a.tm_k : *a.tm_ht, p);
     ++*launches;
     return cudaGetLastError();
 }

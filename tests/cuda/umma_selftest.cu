@@ -136,6 +136,79 @@ __global__ void tma_selftest_kernel(const __grid_constant__ CUtensorMap map, int
     for (int i = threadIdx.x; i < 8192; i += blockDim.x) out[i] = smem[i];
 }
 
+// TS check: A [128 x K] bf16 written into TMEM by the threads (lane = row, 2 elements per
+// 32-bit column, element k in the low half of column k/2 when k is even), B from smem.
+//   mode 0: K = 128, B = [64 x 128] K-major   -> D [128 x 64]  = A * B^T   (the QK shape)
+//   mode 1: K = 64,  B = [64 x 128] MN-major  -> D [128 x 128] = A * B     (the PV shape)
+__global__ void __launch_bounds__(128, 1) umma_ts_selftest_kernel(int mode, const uint16_t* A, const uint16_t* B,
+                                                                  float* D) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sB = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x;
+    const int K = mode == 0 ? 128 : 64, N = mode == 0 ? 64 : 128;
+    if (mode == 0) {
+        for (int i = tid; i < N * K; i += 128) {
+            int r = i / K, c = i % K;
+            *reinterpret_cast<uint16_t*>(sB + (c / 64) * (N * 128) + sw128_off(r, c % 64)) = B[i];
+        }
+    } else {
+        for (int i = tid; i < K * N; i += 128) {
+            int kr = i / N, n = i % N;
+            *reinterpret_cast<uint16_t*>(sB + (n / 64) * (K * 128) + sw128_off(kr, n % 64)) = B[i];
+        }
+    }
+    fence_proxy_async_smem();
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    if (warp_id() == 0) tmem_alloc(&tmem_base, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = tmem_base;
+    const uint32_t lane_base = (warp_id() * 32) << 16;
+    // A row `tid` -> TMEM columns [128, 128 + K/2)
+    for (int c0 = 0; c0 < K / 2; c0 += 32) {
+        uint32_t w[32];
+        for (int c = 0; c < 32; ++c)
+            w[c] = (uint32_t)A[tid * K + 2 * (c0 + c)] | ((uint32_t)A[tid * K + 2 * (c0 + c) + 1] << 16);
+        tmem_st32(tbase + lane_base + 128 + c0, w);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+        const uint32_t idesc = idesc_bf16(128, N, false, mode == 1);
+        for (int s = 0; s < K / 16; ++s) {
+            uint64_t bd = mode == 0 ? sdesc_sw128(smem_u32(sB) + (s / 4) * (N * 128) + (s % 4) * 32, 16, 1024)
+                                    : sdesc_sw128(smem_u32(sB) + s * 16 * 128, K * 128, 1024);
+            umma_bf16_ts(tbase, tbase + 128 + s * 8, bd, idesc, s > 0);
+        }
+        umma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    __syncwarp();
+    tc_fence_after();
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_base + c0, r);
+        tmem_ld_wait();
+        for (int c = 0; c < 32; ++c) D[tid * N + c0 + c] = __uint_as_float(r[c]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp_id() == 0) tmem_free(tbase, 256);
+}
+extern "C" int umma_ts_selftest(int mode, const void* A, const void* B, void* D) {
+    cudaFuncSetAttribute(umma_ts_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 33 * 1024);
+    umma_ts_selftest_kernel<<<1, 128, 33 * 1024>>>(mode, (const uint16_t*)A, (const uint16_t*)B, (float*)D);
+    return (int)cudaDeviceSynchronize();
+}
+
 // Device expf_glibc over a host-chosen range of float bit patterns [lo, lo + n).
 __global__ void expf_selftest_kernel(uint32_t lo, uint32_t n, float* out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)

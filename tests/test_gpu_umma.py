@@ -104,3 +104,22 @@ def test_device_expf_matches_host_libm(lib, cuda):
         del ref
         checked += len(idx)
     assert checked > 1_000_000
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_umma_bf16_a_from_tmem(lib, cuda, mode):
+    """TS form: A written into TMEM (lane = row, bf16 pairs per column), B from smem."""
+    import torch
+    lib.umma_ts_selftest.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    g = torch.Generator(device="cpu").manual_seed(10 + mode)
+    if mode == 0:
+        a = torch.randn((128, 128), generator=g).to(torch.bfloat16)
+        b = torch.randn((64, 128), generator=g).to(torch.bfloat16)
+        ref = a.float() @ b.float().t()
+    else:
+        a = torch.randn((128, 64), generator=g).to(torch.bfloat16)
+        b = torch.randn((64, 128), generator=g).to(torch.bfloat16)
+        ref = a.float() @ b.float()
+    d = torch.zeros(ref.shape, dtype=torch.float32, device=cuda)
+    assert lib.umma_ts_selftest(mode, a.to(cuda).data_ptr(), b.to(cuda).data_ptr(), d.data_ptr()) == 0
+    torch.testing.assert_close(d.cpu(), ref, rtol=1e-4, atol=1e-3)
