@@ -173,6 +173,8 @@ struct Workspace {
     double* mu_part;
     float* qp;
     float* kp;
+    float* qbar;
+    float* kbar;
     int32_t* idx;
     void* phik;
     float* zblk;
@@ -193,6 +195,8 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.mu_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
     t.qp = c.take<float>(g.BH * g.tm * g.d);
     t.kp = c.take<float>(g.BH * g.tn * g.d);
+    t.qbar = c.take<float>(g.BH * g.tm * g.d);
+    t.kbar = c.take<float>(g.BH * g.tn * g.d);
     t.idx = c.take<int32_t>(g.BH * g.tm * std::max<int64_t>(g.kappa, g.tn));
     t.cnt = c.take<int32_t>(g.BH * g.tm);
     t.flag = c.take<int>(4);
@@ -216,8 +220,9 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
 
 // TMA view of K for the serial column-mean kernel: [B*H*N][d] elements, 32 x 256 boxes.
 const CUtensorMap* colmean_map(CUtensorMap* m, const void* k, bool bf16, int64_t BH, int64_t N, int64_t d) {
-    if (N % 256 != 0 || d % 32 != 0) return nullptr;
-    return make_map(m, k, (uint64_t)(BH * N), (uint64_t)d, 32, 256, bf16 ? 2 : 4, false) ? m : nullptr;
+    const uint32_t cols = bf16 ? 64 : 32;  // one 128-byte segment per row
+    if (N % 128 != 0 || d % cols != 0) return nullptr;
+    return make_map(m, k, (uint64_t)(BH * N), (uint64_t)d, cols, 128, bf16 ? 2 : 4, false) ? m : nullptr;
 }
 
 float inv_sqrt(int64_t d) {
@@ -422,6 +427,8 @@ sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, 
     ra.mu_part = w.mu_part;
     ra.qp = w.qp;
     ra.kp = w.kp;
+    ra.qbar = w.qbar;
+    ra.kbar = w.kbar;
     ra.pc_out = pc_out;
     ra.mask_out = mask_out;
     ra.idx_out = kv_idx_out ? kv_idx_out : w.idx;

@@ -23,6 +23,8 @@ struct RouterLaunch {
     double* mu_part;  // fast colmean scratch
     float* qp;        // [BH][tm][d]
     float* kp;        // [BH][tn][d]
+    float* qbar;      // [BH][tm][d] pooled scratch
+    float* kbar;      // [BH][tn][d] pooled scratch
     float* pc_out;    // optional [BH][tm][tn]
     uint8_t* mask_out;
     int32_t* idx_out;  // [BH][tm][kappa]

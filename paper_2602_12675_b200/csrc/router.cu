@@ -60,61 +60,66 @@ __global__ void __launch_bounds__(32) colmean_exact_kernel(const T* __restrict__
     mu[bh * d + c] = __fmul_rn(acc, inv);
 }
 
-// K0, TMA-fed: one CTA per (32-column group, bh). Warp 1 streams [256 rows x 32 cols] tiles
-// of K into a 6-deep shared-memory ring with TMA; warp 0 runs the 32 serial add chains out
-// of shared memory with register double-buffering, so the chain runs at FADD latency instead
-// of DRAM latency. Same order and roundings as colmean_exact_kernel.
+// K0, TMA-fed: one CTA per (group of 128-byte column strips, bh): 64 bf16 / 32 fp32 columns,
+// so every TMA box row is a full 128-byte segment. The last warp streams [128 rows x COLS]
+// tiles into an 8-deep shared-memory ring; each compute warp runs 32 serial add chains out of
+// shared memory with register double-buffering, so each chain runs at FADD latency instead of
+// DRAM latency. Same order and roundings as colmean_exact_kernel.
 namespace cm {
-constexpr int ROWS = 256, NST = 6;
+constexpr int ROWS = 128, NST = 8;
 }
 template <typename T>
-__global__ void __launch_bounds__(64) colmean_tma_kernel(const __grid_constant__ CUtensorMap tmK, float* __restrict__ mu,
+__global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__ CUtensorMap tmK, float* __restrict__ mu,
                                                          int N, int d) {
+    constexpr int COLS = 128 / sizeof(T);
+    constexpr int NCW = COLS / 32;  // compute warps
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    T* ring = reinterpret_cast<T*>(smem_raw);  // [NST][ROWS][32]
+    T* ring = reinterpret_cast<T*>(smem_raw);  // [NST][ROWS][COLS]
     __shared__ uint64_t full[cm::NST], empty[cm::NST];
     const int cg = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nchunk = N / cm::ROWS;  // N % 256 == 0 is checked by the launcher
+    const int nchunk = N / cm::ROWS;  // N % 128 == 0 is checked by the launcher
     if (threadIdx.x == 0) {
         for (int s = 0; s < cm::NST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 32);
+            mbar_init(&empty[s], COLS);
         }
         fence_barrier_init();
     }
     __syncthreads();
-    if (warp == 1) {
+    if (warp == NCW) {
         if (lane == 0) {
             tma_prefetch_desc(&tmK);
             for (int c = 0; c < nchunk; ++c) {
                 const int s = c % cm::NST;
                 if (c >= cm::NST) mbar_wait(&empty[s], ((c / cm::NST) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], cm::ROWS * 32 * sizeof(T));
-                tma_load_2d(ring + (size_t)s * cm::ROWS * 32, &tmK, cg * 32, (int)(bh * N + (int64_t)c * cm::ROWS),
-                            &full[s]);
+                mbar_arrive_expect_tx(&full[s], cm::ROWS * COLS * sizeof(T));
+                tma_load_2d(ring + (size_t)s * cm::ROWS * COLS, &tmK, cg * COLS,
+                            (int)(bh * N + (int64_t)c * cm::ROWS), &full[s]);
             }
         }
         return;
     }
+    if (warp > NCW) return;
+    const int col = warp * 32 + lane;
     float acc = 0.0f;
     for (int c = 0; c < nchunk; ++c) {
         const int s = c % cm::NST;
         mbar_wait(&full[s], (c / cm::NST) & 1);
-        const T* tile = ring + (size_t)s * cm::ROWS * 32 + lane;
+        const T* tile = ring + (size_t)s * cm::ROWS * COLS + col;
         float a[32], b[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[u * 32]);
+        for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[u * COLS]);
 #pragma unroll 1
         for (int r0 = 0; r0 < cm::ROWS; r0 += 64) {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) b[u] = to_f32(tile[(r0 + 32 + u) * 32]);
+            for (int u = 0; u < 32; ++u) b[u] = to_f32(tile[(r0 + 32 + u) * COLS]);
 #pragma unroll
             for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, a[u]);
             if (r0 + 64 < cm::ROWS) {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[(r0 + 64 + u) * 32]);
+                for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[(r0 + 64 + u) * COLS]);
             }
 #pragma unroll
             for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, b[u]);
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(64) colmean_tma_kernel(const __grid_constant__
         mbar_arrive(&empty[s]);
     }
     const float inv = __fdiv_rn(1.0f, (float)N);
-    mu[bh * d + cg * 32 + lane] = __fmul_rn(acc, inv);
+    mu[bh * d + cg * COLS + col] = __fmul_rn(acc, inv);
 }
 
 // K0 (fast variant, exact_mu = 0): column sums in double over row chunks, then the same
@@ -157,29 +162,40 @@ __global__ void colmean_finish_kernel(const double* __restrict__ part, float* __
 // grid (nblocks, B*H), block d. Dynamic smem: d floats.
 template <typename T>
 __global__ void pool_project_kernel(const T* __restrict__ x, const float* __restrict__ mu, const float* __restrict__ proj,
-                                    float* __restrict__ xp, int N, int d, int H, int block) {
-    extern __shared__ float sbar[];
+                                    float* __restrict__ xp, int N, int d, int H, int block,
+                                    float* __restrict__ xbar_out) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    float* sbar = reinterpret_cast<float*>(psm);
+    T* tile = reinterpret_cast<T*>(psm + ((d * sizeof(float) + 15) & ~size_t(15)));  // [block][d]
     const int c = threadIdx.x;
     const int g = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int h = (int)(bh % H);
-    const T* src = x + (bh * N + (int64_t)g * block) * d + c;
+    // stage the whole [block x d] slab with independent 16-byte loads (one DRAM round trip)
+    {
+        const T* src = x + (bh * N + (int64_t)g * block) * d;
+        if (((d * sizeof(T)) & 15) == 0) {
+            const uint4* src4 = reinterpret_cast<const uint4*>(src);
+            uint4* dst4 = reinterpret_cast<uint4*>(tile);
+            const int n16 = (int)((size_t)block * d * sizeof(T) / 16);
+            for (int e = c; e < n16; e += blockDim.x) dst4[e] = src4[e];
+        } else {
+            for (int e = c; e < block * d; e += blockDim.x) tile[e] = src[e];
+        }
+    }
+    __syncthreads();
     const float m = mu ? mu[bh * d + c] : 0.0f;
     double acc = 0.0;
-    int r = 0;
-    for (; r + 16 <= block; r += 16) {  // loads batched ahead of the serial double chain
-        float v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = to_f32(src[(int64_t)(r + u) * d]);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, (double)(mu ? __fsub_rn(v[u], m) : v[u]));
-    }
-    for (; r < block; ++r) {
-        float v = to_f32(src[(int64_t)r * d]);
+    for (int r = 0; r < block; ++r) {
+        float v = to_f32(tile[r * d + c]);
         if (mu) v = __fsub_rn(v, m);
         acc = __dadd_rn(acc, (double)v);
     }
     sbar[c] = __double2float_rn(__ddiv_rn(acc, (double)block));
+    if (xbar_out) {  // pooled rows only; the projection runs in project_kernel
+        xbar_out[(bh * (N / block) + g) * d + c] = sbar[c];
+        return;
+    }
     __syncthreads();
     const float* P = proj + (int64_t)h * d * d;
     float o = 0.0f;
@@ -193,6 +209,59 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
     }
     for (; f < d; ++f) o = __fadd_rn(o, __fmul_rn(sbar[f], P[(int64_t)f * d + c]));
     xp[(bh * (N / block) + g) * d + c] = o;
+}
+
+// xp[g][c] = sum_f xbar[g][f] * P[f][c] (matrix.hpp:121-132: i-k-j order, one serial chain
+// per output, f ascending from 0, separate mul and add), for a tile of 32 pooled rows per CTA.
+// P (d x d) and the xbar tile live in shared memory; each thread owns a 4 x 4 register tile
+// of outputs (16 independent chains). grid (ceil(nrows/32), BH), block 256. Requires d % 16 == 0.
+__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ xbar, const float* __restrict__ proj,
+                                                      float* __restrict__ xp, int nrows, int d, int H) {
+    extern __shared__ __align__(16) float psh[];
+    float* sP = psh;           // [d][d]
+    float* sX = psh + d * d;   // [32][d]
+    const int64_t bh = blockIdx.y;
+    const int h = (int)(bh % H);
+    const int r0 = blockIdx.x * 32;
+    const int tid = threadIdx.x;
+    const int nr = min(32, nrows - r0);
+    {
+        const float4* P4 = reinterpret_cast<const float4*>(proj + (int64_t)h * d * d);
+        float4* s4 = reinterpret_cast<float4*>(sP);
+        for (int e = tid; e < d * d / 4; e += 256) s4[e] = P4[e];
+        const float4* X4 = reinterpret_cast<const float4*>(xbar + (bh * nrows + r0) * (int64_t)d);
+        float4* x4 = reinterpret_cast<float4*>(sX);
+        for (int e = tid; e < 32 * d / 4; e += 256) x4[e] = (e < nr * d / 4) ? X4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    // d / 4 column groups x 8 row groups of 4 rows; 256 threads cover them in d/128 passes
+    const int ncg = d / 4;
+    for (int t = tid; t < ncg * 8; t += 256) {
+        const int cg = t % ncg, rg = t / ncg;
+        float acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+        for (int f = 0; f < d; ++f) {
+            const float4 pv = *reinterpret_cast<const float4*>(sP + f * d + cg * 4);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const float xv = sX[(rg * 4 + a) * d + f];
+                acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(xv, pv.x));
+                acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(xv, pv.y));
+                acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(xv, pv.z));
+                acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(xv, pv.w));
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = rg * 4 + a;
+            if (r < nr)
+                *reinterpret_cast<float4*>(xp + (bh * nrows + r0 + r) * (int64_t)d + cg * 4) =
+                    make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -322,6 +391,55 @@ __global__ void router_scores_topk_kernel(const float* __restrict__ qp, const fl
              idx_out + (bh * tm + i) * (int64_t)kappa, sel, warp_cnt);
 }
 
+// Warp-local top-k for small kappa (<= 64) and tn <= 32 * TKMAX: each lane holds the keys of
+// columns lane, lane+32, ... in registers; kappa rounds of a warp-wide minimum over
+// (desc_key, column) pick exactly the stable-sort prefix (value desc, ties to the lower column).
+template <int TKMAX>  // keys per lane: tn <= 32 * TKMAX
+__device__ void warp_topk_small(const float* __restrict__ vals, int tn, int kappa, uint8_t* __restrict__ mask_row,
+                                int32_t* __restrict__ idx_row, uint8_t* sel) {
+    const int lane = threadIdx.x & 31;
+    const int per = (tn + 31) >> 5;
+    unsigned long long key[TKMAX];
+#pragma unroll
+    for (int u = 0; u < TKMAX; ++u) {
+        const int j = lane + 32 * u;
+        key[u] = (u < per && j < tn) ? (((unsigned long long)desc_key(vals[j]) << 32) | (unsigned)j) : ~0ull;
+    }
+    for (int j = lane; j < tn; j += 32) sel[j] = 0;
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int u = 0; u < TKMAX; ++u) best = key[u] < best ? key[u] : best;
+    __syncwarp();
+    for (int r = 0; r < kappa; ++r) {
+        unsigned long long w = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
+            w = t < w ? t : w;
+        }
+        const int jw = (int)(w & 0xffffffffu);
+        if ((jw & 31) == lane) {  // owner removes it and rescans its registers
+            sel[jw] = 1;
+            best = ~0ull;
+#pragma unroll
+            for (int u = 0; u < TKMAX; ++u) {
+                if (key[u] == w) key[u] = ~0ull;
+                best = key[u] < best ? key[u] : best;
+            }
+        }
+    }
+    __syncwarp();
+    int base = 0;
+    for (int j0 = 0; j0 < tn; j0 += 32) {
+        const int j = j0 + lane;
+        const bool f = (j < tn) && sel[j];
+        if (mask_row && j < tn) mask_row[j] = f ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (f) idx_row[base + __popc(bal & ((1u << lane) - 1u))] = j;
+        base += __popc(bal);
+    }
+}
+
 // Warp-local top-k on one row held in shared memory as 64-bit keys (value desc, column asc).
 // Bitonic sort by one warp (npow2 / 64 compare-exchanges per lane per stage), then the kept
 // columns are flagged and compacted in ascending order with ballots.
@@ -370,6 +488,7 @@ __device__ void warp_topk_row(const float* __restrict__ vals, int tn, int kappa,
 //            inv = 1 / sum, pc = e * inv (matrix.hpp:144-152), then top-kappa.
 // Dynamic smem: 8*tn floats + 8*(npow2*8 + tn) bytes + 8*d floats.
 constexpr int RROWS = 8;
+template <int TK>  // 0: bitonic top-k; otherwise register top-k with TK keys per lane
 __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
                                                           float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
                                                           float* __restrict__ pc_out, uint8_t* __restrict__ mask_out,
@@ -389,6 +508,39 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
     }
     __syncthreads();
     const float* kpb = kp + bh * (int64_t)tn * d;
+    if ((tn & 3) == 0 && (d & 3) == 0) {
+        // register tile: 4 rows x 4 columns per thread, 16 independent serial chains; each
+        // loaded qp / kp value feeds 4 products (shared-memory traffic 1/4 of the naive loop)
+        const int rg = tid >> 7;  // rows rg*4 .. rg*4+3
+        for (int jg = tid & 127; jg * 4 < tn; jg += 128) {
+            float acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+            const float* k0 = kpb + (int64_t)(jg * 4) * d;
+            for (int c = 0; c < d; c += 4) {
+                float4 kv[4], qv[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) kv[b] = *reinterpret_cast<const float4*>(k0 + (int64_t)b * d + c);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) qv[a] = *reinterpret_cast<const float4*>(sq + (rg * 4 + a) * d + c);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        acc[a][b] = __fadd_rn(acc[a][b], __fmul_rn(qv[a].x, kv[b].x));
+                        acc[a][b] = __fadd_rn(acc[a][b], __fmul_rn(qv[a].y, kv[b].y));
+                        acc[a][b] = __fadd_rn(acc[a][b], __fmul_rn(qv[a].z, kv[b].z));
+                        acc[a][b] = __fadd_rn(acc[a][b], __fmul_rn(qv[a].w, kv[b].w));
+                    }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
+        }
+    } else
     for (int j = tid; j < tn; j += 256) {
         float acc[RROWS];
 #pragma unroll
@@ -452,8 +604,10 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
     }
     __syncwarp();
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(keyb + warp * key_stride);
-    warp_topk_row(v, tn, kappa, keys, npow2, mask_out ? mask_out + (bh * tm + i) * (int64_t)tn : nullptr,
-                  idx_out + (bh * tm + i) * (int64_t)kappa);
+    uint8_t* mrow = mask_out ? mask_out + (bh * tm + i) * (int64_t)tn : nullptr;
+    int32_t* irow = idx_out + (bh * tm + i) * (int64_t)kappa;
+    if constexpr (TK > 0) warp_topk_small<TK>(v, tn, kappa, mrow, irow, reinterpret_cast<uint8_t*>(keys));
+    else warp_topk_row(v, tn, kappa, keys, npow2, mrow, irow);
 }
 
 size_t router_rows_smem(int tn, int d) {
@@ -497,26 +651,62 @@ __global__ void mask_to_idx_kernel(const uint8_t* __restrict__ mask, int tn, int
 template <typename T>
 static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, int N, int d, cudaStream_t st,
                       int* launches) {
-    if (tmk && N % cm::ROWS == 0 && d % 32 == 0) {
-        const int smem = cm::NST * cm::ROWS * 32 * (int)sizeof(T);
+    constexpr int COLS = 128 / sizeof(T);
+    if (tmk && N % cm::ROWS == 0 && d % COLS == 0) {
+        const int smem = cm::NST * cm::ROWS * 128;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(colmean_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             attr = true;
         }
-        colmean_tma_kernel<T><<<dim3(d / 32, BH), 64, smem, st>>>(*tmk, mu, N, d);
+        colmean_tma_kernel<T><<<dim3(d / COLS, BH), (COLS / 32 + 1) * 32, smem, st>>>(*tmk, mu, N, d);
     } else {
         colmean_exact_kernel<T><<<dim3((d + 31) / 32, BH), 32, 0, st>>>((const T*)k, mu, N, d);
     }
     ++*launches;
 }
 
+// Pool then project. With d % 16 == 0 (every shipped config) pooling writes xbar to `scratch`
+// and project_kernel reuses P from shared memory across 32 rows; otherwise the per-block
+// kernel projects in place.
+template <typename T>
+static void launch_pool_project(const T* x, const float* mu, const float* proj, float* xp, int N, int d, int H,
+                                int block, int BH, float* scratch, cudaStream_t st, int* launches) {
+    const size_t smem = ((d * sizeof(float) + 15) & ~size_t(15)) + (size_t)block * d * sizeof(T);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(pool_project_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool split = scratch && (d % 16 == 0) && ((size_t)d * d + 32 * d) * 4 <= 200 * 1024;
+    pool_project_kernel<T><<<dim3(N / block, BH), d, smem, st>>>(x, mu, proj, xp, N, d, H, block,
+                                                                  split ? scratch : nullptr);
+    ++*launches;
+    if (split) {
+        const int nrows = N / block;
+        const size_t ps = ((size_t)d * d + 32 * d) * 4;
+        cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+        project_kernel<<<dim3((nrows + 31) / 32, BH), 256, ps, st>>>(scratch, proj, xp, nrows, d, H);
+        ++*launches;
+    }
+}
+
 template <typename T>
 static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
     const int BH = (int)(a.B * a.H);
+    // The exact column mean is a serial chain on a few SMs: run it on a side stream,
+    // concurrently with the query-side pooling/projection, and join before the key side.
+    thread_local cudaStream_t side = nullptr;
+    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (!side) {
+        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+    }
+    bool forked = false;
     if (a.mu_out) {
         if (a.exact_mu) {
-            colmean_t<T>(a.k, a.tm_kcol, a.mu_out, BH, a.N, a.d, st, launches);
+            cudaEventRecord(ev_fork, st);
+            cudaStreamWaitEvent(side, ev_fork, 0);
+            colmean_t<T>(a.k, a.tm_kcol, a.mu_out, BH, a.N, a.d, side, launches);
+            cudaEventRecord(ev_join, side);
+            forked = true;
         } else {
             const int rows_per = 256;
             const int nch = (a.N + rows_per - 1) / rows_per;
@@ -526,18 +716,23 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
         }
     }
     const int tm = a.N / a.bq, tn = a.N / a.bk;
-    pool_project_kernel<T><<<dim3(tm, BH), a.d, a.d * sizeof(float), st>>>((const T*)a.q, nullptr, a.proj_q, a.qp,
-                                                                            a.N, a.d, a.H, a.bq);
-    pool_project_kernel<T><<<dim3(tn, BH), a.d, a.d * sizeof(float), st>>>(
-        (const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d, a.H, a.bk);
-    *launches += 2;
+    launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
+    if (forked) cudaStreamWaitEvent(st, ev_join, 0);
+    launch_pool_project<T>((const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d, a.H, a.bk, BH,
+                           a.kbar, st, launches);
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
     const size_t rsm = router_rows_smem(tn, a.d);
     if (rsm <= 220 * 1024) {
-        cudaFuncSetAttribute(router_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-        router_rows_kernel<<<dim3((tm + RROWS - 1) / RROWS, BH), 256, rsm, st>>>(
-            a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2, a.pc_out, a.mask_out, a.idx_out);
+        const dim3 grid((tm + RROWS - 1) / RROWS, BH);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+            kern<<<grid, 256, rsm, st>>>(a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2, a.pc_out, a.mask_out,
+                                         a.idx_out);
+        };
+        if (a.kappa <= 64 && tn <= 32 * 16) go(router_rows_kernel<16>);
+        else if (a.kappa <= 64 && tn <= 32 * 64) go(router_rows_kernel<64>);
+        else go(router_rows_kernel<0>);
     } else {
         const size_t smem = npow2 * 8 + tn * 4 + a.d * 4 + tn + 16;
         cudaFuncSetAttribute(router_scores_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

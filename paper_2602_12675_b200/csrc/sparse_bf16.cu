@@ -21,12 +21,14 @@
 // The raw K is used for Q K^T: smoothing shifts every score of a row by the same constant
 // (test_attention.cpp:270-279), so O_s is unchanged and K needs no bf16 re-rounding.
 //
-// Shared memory is the scarce resource (128 B/clk/SM): keeping Q and P in TMEM removes 64 KB
-// of smem traffic per key block, leaving the TMA writes of K, V, phi(K) and the three B/A
-// operand reads. Htot (bf16, MN-major SW128) is staged once per CTA by TMA.
+// Shared memory bandwidth (128 B/clk/SM) is the scarce resource: Q and P live in TMEM, so per
+// key block smem sees only the TMA writes of K, V, phi(K) and the B/A operand reads. K has its
+// own 4-deep ring released as soon as its QK MMA completes; V/phi(K) a 3-deep ring released
+// after PV/HS. The MMA thread polls (try_wait) so a late tile never blocks a ready MMA.
 //
-// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 complement of Z, w4-7 softmax / correction / epilogue (thread = query row).
+// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K ring), w1 MMA issuer, w2 TMEM
+// allocator + TMA producer (V/phi(K) ring, Htot), w3 Zc then phi(Q) and its denominators
+// (overlapped with the main loop), w4-7 softmax / correction / epilogue (thread = query row).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -40,15 +42,16 @@
 namespace sla2dev {
 
 namespace sp {
-constexpr int BQ = 128, BK = 64, D = 128, NS = 3;
+constexpr int BQ = 128, BK = 64, D = 128;
+constexpr int NSK = 4, NSV = 3;
 constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
-constexpr uint32_t STAGE_BYTES = 3 * TILE_BYTES;
-constexpr uint32_t HT_BYTES = D * D * 2;  // 32 KB Htot (bf16)
+constexpr uint32_t HT_BYTES = D * D * 2;     // 32 KB Htot (bf16)
 constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_STAGE = Q_BYTES;
-constexpr uint32_t OFF_HT = OFF_STAGE + NS * STAGE_BYTES;
-constexpr uint32_t SMEM_BYTES = OFF_HT + HT_BYTES;
+constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
+constexpr uint32_t OFF_V = OFF_K + NSK * TILE_BYTES;
+constexpr uint32_t OFF_HT = OFF_V + NSV * 2 * TILE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_HT + HT_BYTES;  // 224 KB
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
 // TMEM columns (512 allocated)
 constexpr uint32_t TM_Q = 0;      // Q_i as the A operand: 128 lanes x 64 cols (bf16 pairs)
@@ -105,10 +108,11 @@ __global__ void __launch_bounds__(256, 1)
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_qt, bar_ht, bar_kv_full[NS], bar_kv_empty[NS], bar_s_full[2], bar_p_full[2],
-        bar_pv_done[2], bar_lin_ready, bar_lin_done;
+    __shared__ uint64_t bar_q, bar_qt, bar_phiq, bar_ht, bar_k_full[NSK], bar_k_empty[NSK], bar_v_full[NSV],
+        bar_v_empty[NSV], bar_s_full[2], bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
+    __shared__ float sDen[BQ];
 
     const int i = blockIdx.x;       // query block
     const int64_t bh = blockIdx.y;  // (b, h)
@@ -123,10 +127,15 @@ __global__ void __launch_bounds__(256, 1)
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, 1);
         mbar_init(&bar_qt, 128);
+        mbar_init(&bar_phiq, 32);
         mbar_init(&bar_ht, 1);
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&bar_kv_full[s], 1);
-            mbar_init(&bar_kv_empty[s], 1);
+        for (int s = 0; s < NSK; ++s) {
+            mbar_init(&bar_k_full[s], 1);
+            mbar_init(&bar_k_empty[s], 1);
+        }
+        for (int s = 0; s < NSV; ++s) {
+            mbar_init(&bar_v_full[s], 1);
+            mbar_init(&bar_v_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar_s_full[b], 1);
@@ -146,18 +155,16 @@ __global__ void __launch_bounds__(256, 1)
 
     uint8_t* sQ = smem + OFF_Q;
     uint8_t* sHt = smem + OFF_HT;
-    auto sK = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES; };
-    auto sV = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + TILE_BYTES; };
-    auto sPh = [&](int s) { return smem + OFF_STAGE + s * STAGE_BYTES + 2 * TILE_BYTES; };
-    uint8_t* sHc = smem + OFF_STAGE;  // epilogue alias of stage 0 (32 KB)
+    auto sK = [&](int s) { return smem + OFF_K + s * TILE_BYTES; };
+    auto sV = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES; };
+    auto sPh = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES + TILE_BYTES; };
+    uint8_t* sHc = smem + OFF_V;  // epilogue alias of V/phi stage 0 (32 KB, free after the loop)
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer: Q, K ring =====================
         if (lane == 0) {
             tma_prefetch_desc(&tmQ);
             tma_prefetch_desc(&tmK);
-            tma_prefetch_desc(&tmV);
-            if (!dense) tma_prefetch_desc(&tmPhi);
             const uint64_t pol_keep = policy_evict_last();
             const int qrow = (int)(bh * p.N + (int64_t)i * BQ);
             mbar_arrive_expect_tx(&bar_q, Q_BYTES);
@@ -165,22 +172,36 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sQ + 8192, &tmQ, 0, qrow + 64, &bar_q);
             tma_load_2d(sQ + 16384, &tmQ, 64, qrow, &bar_q);
             tma_load_2d(sQ + 24576, &tmQ, 64, qrow + 64, &bar_q);
-            const uint32_t stage_tx = dense ? 2 * TILE_BYTES : 3 * TILE_BYTES;
             for (int j = 0; j < nb; ++j) {
-                const int s = j % NS;
-                if (j >= NS) mbar_wait(&bar_kv_empty[s], ((j / NS) - 1) & 1);
+                const int s = j % NSK;
+                if (j >= NSK) mbar_wait(&bar_k_empty[s], ((j / NSK) - 1) & 1);
                 const int kb = dense ? j : idx[j];
                 const int krow = (int)(bh * p.N + (int64_t)kb * BK);
                 if (j == 0) SLA2_TR(54);
                 if (j == nb - 1) SLA2_TR(55);
-                mbar_arrive_expect_tx(&bar_kv_full[s], stage_tx);
-                tma_load_2d_hint(sK(s), &tmK, 0, krow, &bar_kv_full[s], pol_keep);
-                tma_load_2d_hint(sK(s) + 8192, &tmK, 64, krow, &bar_kv_full[s], pol_keep);
-                tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_kv_full[s], pol_keep);
-                tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_kv_full[s], pol_keep);
+                mbar_arrive_expect_tx(&bar_k_full[s], TILE_BYTES);
+                tma_load_2d_hint(sK(s), &tmK, 0, krow, &bar_k_full[s], pol_keep);
+                tma_load_2d_hint(sK(s) + 8192, &tmK, 64, krow, &bar_k_full[s], pol_keep);
+            }
+        }
+    } else if (warp == 2) {
+        // ===================== TMA producer: V / phi(K) ring, Htot =====================
+        if (lane == 0) {
+            tma_prefetch_desc(&tmV);
+            if (!dense) tma_prefetch_desc(&tmPhi);
+            const uint64_t pol_keep = policy_evict_last();
+            const uint32_t tx = dense ? TILE_BYTES : 2 * TILE_BYTES;
+            for (int j = 0; j < nb; ++j) {
+                const int s = j % NSV;
+                if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
+                const int kb = dense ? j : idx[j];
+                const int krow = (int)(bh * p.N + (int64_t)kb * BK);
+                mbar_arrive_expect_tx(&bar_v_full[s], tx);
+                tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol_keep);
+                tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol_keep);
                 if (!dense) {
-                    tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_kv_full[s], pol_keep);
-                    tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_kv_full[s], pol_keep);
+                    tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol_keep);
+                    tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol_keep);
                 }
                 if (j == 0 && linear) {
                     // Htot of this head, bf16 [f][c] as the MN-major B layout [c_atom][f][64]
@@ -200,47 +221,58 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&bar_qt, 0);  // Q resident in TMEM
             tc_fence_after();
             SLA2_TR(1);
-            // S_j: A = Q (TMEM), B = K_j (smem, K-major). S[b] may be overwritten only after
-            // PV_{j-2} read P_{j-2} from it: guaranteed, tcgen05 MMAs of one thread execute in
-            // issue order and PV_{j-2} is issued before QK_j.
-            auto issue_qk = [&](int j) {
-                const int s = j % NS, b = j & 1;
-                mbar_wait(&bar_kv_full[s], (j / NS) & 1);
-                tc_fence_after();
-                const uint32_t bK = smem_u32(sK(s));
+            // Three in-order streams polled without blocking:
+            //   QK_n: K_n landed and S[n&1] reusable (PV_{n-2} issued: MMAs of one thread run
+            //         in issue order, so QK_n cannot overwrite P_{n-2} before PV_{n-2} read it)
+            //   HS_n: V_n/phi_n landed (only needs tiles)
+            //   PV_n: P_n written and HS_n issued (v_empty after PV covers both)
+            int nq = 0, nh = 0, np = 0;
+            while (np < nb) {
+                bool progress = false;
+                if (nq < nb && nq <= np + 1 && mbar_try_wait(&bar_k_full[nq % NSK], (nq / NSK) & 1)) {
+                    tc_fence_after();
+                    const int b = nq & 1;
+                    const uint32_t bK = smem_u32(sK(nq % NSK));
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t offk = (ks >> 2) * 8192 + (ks & 3) * 32;
-                    umma_bf16_ts(tmem + TM_S + b * 64, tmem + TM_Q + ks * 8, sdesc_sw128(bK + offk, 16, 1024), ID_QK,
-                                 ks > 0);
+                    for (int ks = 0; ks < 8; ++ks)
+                        umma_bf16_ts(tmem + TM_S + b * 64, tmem + TM_Q + ks * 8,
+                                     sdesc_sw128(bK + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024), ID_QK, ks > 0);
+                    umma_commit(&bar_s_full[b]);
+                    umma_commit(&bar_k_empty[nq % NSK]);
+                    ++nq;
+                    progress = true;
                 }
-                umma_commit(&bar_s_full[b]);
-            };
-            if (nb > 0) issue_qk(0);
-            for (int j = 0; j < nb; ++j) {
-                const int s = j % NS, b = j & 1;
-                if (j + 1 < nb) issue_qk(j + 1);
-                mbar_wait(&bar_p_full[b], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t bV = smem_u32(sV(s));
-#pragma unroll
-                for (int ks = 0; ks < 4; ++ks)
-                    umma_bf16_ts(tmem + TM_O, tmem + TM_S + b * 64 + ks * 8, sdesc_sw128(bV + ks * 2048, 8192, 1024),
-                                 ID_PV, (j > 0 || ks > 0));
-                if (!dense) {
-                    const uint32_t aH = smem_u32(sPh(s));
+                if (!dense && nh < nb && nh <= np + 1 && mbar_try_wait(&bar_v_full[nh % NSV], (nh / NSV) & 1)) {
+                    tc_fence_after();
+                    const uint32_t aH = smem_u32(sPh(nh % NSV)), bV = smem_u32(sV(nh % NSV));
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
                         umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
-                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (j > 0 || ks > 0));
+                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (nh > 0 || ks > 0));
+                    ++nh;
+                    progress = true;
                 }
-                umma_commit(&bar_pv_done[b]);
-                if (j < 16) SLA2_TR(34 + j);
-                umma_commit(&bar_kv_empty[s]);
+                if (np < nq && (dense || np < nh) && mbar_try_wait(&bar_p_full[np & 1], (np >> 1) & 1)) {
+                    if (dense) mbar_wait(&bar_v_full[np % NSV], (np / NSV) & 1);
+                    tc_fence_after();
+                    const int b = np & 1;
+                    const uint32_t bV = smem_u32(sV(np % NSV));
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        umma_bf16_ts(tmem + TM_O, tmem + TM_S + b * 64 + ks * 8,
+                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV, (np > 0 || ks > 0));
+                    umma_commit(&bar_pv_done[b]);
+                    if (np < 16) SLA2_TR(34 + np);
+                    umma_commit(&bar_v_empty[np % NSV]);
+                    ++np;
+                    progress = true;
+                }
+                (void)progress;
             }
             if (linear) {
                 // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
                 mbar_wait(&bar_lin_ready, 0);
+                mbar_wait(&bar_phiq, 0);
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ), bH = smem_u32(sHc);
 #pragma unroll
@@ -253,7 +285,7 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp == 3) {
-        // ===================== Zc = Ztot - sum_sel z_j =====================
+        // ===================== Zc, then phi(Q) in place over sQ and phi(Q) . Zc =====================
         if (linear) {
             // lane owns features 4*lane .. 4*lane+3; one coalesced 512-B row per kept block
             const float* zb = p.zblk + bh * (int64_t)p.tn * D + lane * 4;
@@ -288,18 +320,64 @@ __global__ void __launch_bounds__(256, 1)
             sZc[lane * 4 + 1] = zt.y - acc.y;
             sZc[lane * 4 + 2] = zt.z - acc.z;
             sZc[lane * 4 + 3] = zt.w - acc.w;
+            __syncwarp();
+            // Q has been copied into TMEM by the softmax warps: overwrite sQ with phi(Q)
+            // (row softmax over d, attention.hpp:456) in bf16, the A operand of the final MMA.
+            mbar_wait(&bar_qt, 0);
+            __syncwarp();
+            const uint32_t qb = smem_u32(sQ);
+            for (int u = 0; u < 4; ++u) {
+                const int r = lane + 32 * u;
+                float qv[128];
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {
+                    uint32_t w[4];
+                    ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                        qv[ch * 8 + 2 * e] = f2.x;
+                        qv[ch * 8 + 2 * e + 1] = f2.y;
+                    }
+                }
+                float qm = -INFINITY;
+#pragma unroll
+                for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
+                float qs = 0.0f;
+#pragma unroll
+                for (int f = 0; f < 128; ++f) {
+                    qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
+                    qs += qv[f];
+                }
+                const float qinv = 1.0f / qs;
+                float den = 0.0f;
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int f = ch * 8 + 2 * e;
+                        const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
+                        const float2 pr = __bfloat1622float2(pk);
+                        den += pr.x * sZc[f] + pr.y * sZc[f + 1];
+                        w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+                    }
+                    st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+                }
+                sDen[r] = den;
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&bar_phiq);
         }
-        __syncwarp();
-        named_bar_arrive(1, 160);
     } else if (warp >= 4) {
         // ===================== softmax / correction / epilogue =====================
         const int r = threadIdx.x - 128;  // query row within the block
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t qb = smem_u32(sQ);
         // Q row r -> TMEM lane r, columns TM_Q + c hold elements (2c, 2c+1)
         mbar_wait(&bar_q, 0);
         __syncwarp();
         {
+            const uint32_t qb = smem_u32(sQ);
             uint32_t w[32];
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -353,18 +431,17 @@ __global__ void __launch_bounds__(256, 1)
             }
             // P = exp2(s * scale - m2) as packed bf16 over S_j's first 32 columns
             uint32_t w[32];
-            float rs = 0.0f;
+            float rs0 = 0.0f, rs1 = 0.0f;
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
                 const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * e]), p.scale_log2, -m2));
                 const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * e + 1]), p.scale_log2, -m2));
-                const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
-                const float2 pr = __bfloat1622float2(pk);
-                rs += pr.x + pr.y;  // row sum of the probabilities actually multiplied
-                w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+                rs0 += p0;
+                rs1 += p1;
+                w[e] = pack_bf16(p0, p1);
             }
             tmem_st32(tmem + lane_base + TM_S + b * 64, w);
-            l += rs;
+            l += rs0 + rs1;
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&bar_p_full[b]);
@@ -409,54 +486,16 @@ __global__ void __launch_bounds__(256, 1)
                     st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
                 }
             }
-            // phi(Q) = row softmax over d of Q_r (attention.hpp:456), in place over sQ as bf16
-            named_bar_sync(1, 160);  // sZc ready
-            float qv[128];
-#pragma unroll
-            for (int ch = 0; ch < 16; ++ch) {
-                uint32_t w[4];
-                ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-                    qv[ch * 8 + 2 * e] = f2.x;
-                    qv[ch * 8 + 2 * e + 1] = f2.y;
-                }
-            }
-            float qm = -INFINITY;
-#pragma unroll
-            for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
-            float qs = 0.0f;
-#pragma unroll
-            for (int f = 0; f < 128; ++f) {
-                qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
-                qs += qv[f];
-            }
-            const float qinv = 1.0f / qs;
-            den = 0.0f;
-#pragma unroll
-            for (int ch = 0; ch < 16; ++ch) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int f = ch * 8 + 2 * e;
-                    const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
-                    const float2 pr = __bfloat1622float2(pk);
-                    den += pr.x * sZc[f] + pr.y * sZc[f + 1];
-                    w[e] = *reinterpret_cast<const uint32_t*>(&pk);
-                }
-                st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
-            }
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&bar_lin_ready);
             if (r == 0) SLA2_TR(51);
+            mbar_wait(&bar_phiq, 0);
+            den = sDen[r];
             mbar_wait(&bar_lin_done, 0);
             if (r == 0) SLA2_TR(52);
             __syncwarp();
             tc_fence_after();
-        } else {
-            named_bar_sync(1, 160);
         }
 
         // output: out = alpha * O / l + (1 - alpha) * num / den

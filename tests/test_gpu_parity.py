@@ -22,7 +22,10 @@ def _torch():
 
 # ----------------------------------------------------------------------------- router
 @pytest.mark.parametrize("N,k_percent,sigma,seed", [(4096, 3.0, 1.0, 1), (8192, 3.0, 1.0, 2), (8192, 10.0, 4.0, 3),
-                                                   (16384, 5.0, 1.0, 4)])
+                                                   (16384, 5.0, 1.0, 4),
+                                                   (16384, 30.0, 1.0, 8),    # kappa 77: bitonic top-k
+                                                   (65536, 3.0, 1.0, 9),     # tn 1024: 64-key register top-k
+                                                   (32768, 3.0, 1.0, 10)])   # the cfg2 geometry
 def test_router_bitexact_bf16(cuda, N, k_percent, sigma, seed):
     torch = _torch()
     B, H, d, bq, bk = 1, 3, 128, 128, 64
