@@ -158,6 +158,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank runs the full workload; strong: heads sharded over ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = dict(CONFIGS[args.config])
@@ -168,7 +170,9 @@ def main():
     kappa = max(1, min(tn, round(c["k_percent"] / 100.0 * tn)))
     cfg_out = {"workload": c["workload"], "B": c["B"], "H": c["H"], "N": c["N"], "d": c["d"], "bq": c["bq"],
                "bk": c["bk"], "k_percent": c["k_percent"], "kappa": kappa, "sparsity": 1 - kappa / tn,
-               "quant": "int8" if c["quant"] else "none", "parallelism": f"heads-replicated x{world} (weak)"}
+               "quant": "int8" if c["quant"] else "none",
+               "parallelism": (f"heads-replicated x{world} (weak)" if args.scaling == "weak"
+                               else f"heads sharded over {world} ranks (strong)")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -189,6 +193,7 @@ def main():
 
     import torch
     import paper_2602_12675_b200 as sla2
+    from paper_2602_12675_b200 import dist as sd
     import ctypes as C
 
     torch.cuda.set_device(local)
@@ -199,9 +204,12 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
 
-    # synthetic inputs, per-rank seed (weak scaling: each rank its own batch)
+    # synthetic inputs, per-rank seed. weak: every rank runs the full workload (its own batch);
+    # strong: the workload's heads are sharded over the ranks (contiguous, no data exchange)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    B, H, N, d = c["B"], c["H"], c["N"], c["d"]
+    B, H_total, N, d = c["B"], c["H"], c["N"], c["d"]
+    h0, h1 = sd.head_range(H_total, world, rank) if args.scaling == "strong" else (0, H_total)
+    H = h1 - h0
     dt = torch.bfloat16 if c["bf16"] else torch.float32
     q = torch.randn((B, H, N, d), generator=g, device=dev).to(dt)
     k = torch.randn((B, H, N, d), generator=g, device=dev).to(dt)
@@ -256,19 +264,13 @@ def main():
     wall = time.perf_counter() - wall0
     sampler.stop()
     total_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    t_max = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        # verification only: gather per-rank output checksums over NCCL (untimed)
-        cs = out.float().sum().reshape(1).double()
-        allcs = [torch.zeros_like(cs) for _ in range(world)]
-        dist.all_gather(allcs, cs)
-        finite = all(torch.isfinite(x).item() for x in allcs)
-    else:
-        finite = bool(torch.isfinite(out.float()).all().item())
-    ms_per_step = t_max.item() / args.steps
-    flops = eff_flops(c)
-    value = world * flops / (ms_per_step * 1e-3) / 1e12
+    t_max = sd.max_over_ranks(total_ms, device=dev)  # the job is as slow as its slowest rank
+    # verification only (untimed): all-gather per-rank output checksums over NCCL
+    finite = all(x == x and abs(x) != float("inf") for x in sd.gather_checksums(out.float(), device=dev))
+    ms_per_step = t_max / args.steps
+    flops = eff_flops(c)  # whole-workload flops of one rank's job (weak) / of the sharded job (strong)
+    value = (world if args.scaling == "weak" else 1) * flops / (ms_per_step * 1e-3) / 1e12
+    flops = eff_flops(dict(c, H=H))  # this rank's share, for the per-kernel roofline below
     clocks = sampler.summary()
 
     if rank != 0:
@@ -362,7 +364,7 @@ def main():
                "full_forward_ms_extrapolated": t * 1e3 * B * H}
 
     line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16" if c["bf16"] else "f32",
             "data": "synthetic (torch.randn N(0,1), proj = I + 0.05 N(0,1), rho ~ U(-1,1))",
             "config": dict(cfg_out, l2="flushed between timed steps (256 MiB write, outside the events)"),

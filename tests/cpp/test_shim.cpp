@@ -1,0 +1,181 @@
+// test_shim.cpp -- the reference's own forward-path tests (proj/tests/test_router.cpp,
+// test_quant.cpp, test_attention.cpp), re-expressed against the drop-in header
+// include/sla2_b200/sla2.hpp, with the CPU oracle (oracle/liboracle.so, TEST INFRASTRUCTURE)
+// as the checker. Built and run by tests/test_gpu_shim.py (needs an sm_100a GPU).
+#include <cstdio>
+#include <functional>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../oracle/sla2_oracle.h"
+#include "sla2_b200/sla2.hpp"
+
+using namespace sla2;
+
+static int g_fail = 0, g_pass = 0;
+#define EXPECT(cond)                                                                 \
+    do {                                                                             \
+        if (!(cond)) {                                                               \
+            std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);          \
+            ++g_fail;                                                                \
+        } else {                                                                     \
+            ++g_pass;                                                                \
+        }                                                                            \
+    } while (0)
+template <class E>
+static bool throws(const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static Matrix<float> gaussian(std::size_t r, std::size_t c, uint64_t seed, double sd = 1.0) {
+    Matrix<float> m(r, c);
+    sla2o_gaussian_matrix_f(m.data().data(), m.size(), seed, sd);
+    return m;
+}
+static Matrix<float> uniform(std::size_t r, std::size_t c, uint64_t seed) {
+    Matrix<float> m(r, c);
+    sla2o_random_matrix_f(m.data().data(), m.size(), seed, -1.0, 1.0);
+    return m;
+}
+static float max_abs_diff(const Matrix<float>& a, const Matrix<float>& b) {
+    float m = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a.data()[i] - b.data()[i]));
+    return m;
+}
+static float max_abs(const Matrix<float>& a) {
+    float m = 0;
+    for (float v : a.data()) m = std::max(m, std::fabs(v));
+    return m;
+}
+
+// test_router.cpp:58-89
+static void hard_topk_kats() {
+    BlockMask m = hard_topk(Matrix<float>(1, 4, {0.1f, 0.5f, 0.2f, 0.2f}), 25.0);
+    EXPECT(m.keep_per_row == 1 && m.at(0, 1) == 1 && m.at(0, 0) == 0 && m.at(0, 2) == 0);
+    m = hard_topk(Matrix<float>(1, 4, {0.3f, 0.3f, 0.2f, 0.2f}), 25.0);
+    EXPECT(m.at(0, 0) == 1 && m.at(0, 1) == 0);
+    Matrix<float> pc = uniform(8, 16, 111);
+    m = hard_topk(pc, 25.0);
+    std::vector<uint8_t> ref(8 * 16);
+    std::size_t kappa = 0;
+    sla2o_hard_topk_f(pc.data().data(), 8, 16, 25.0, ref.data(), &kappa);
+    EXPECT(m.bits == ref && kappa == 4);
+    EXPECT(throws<shape_error>([] { hard_topk(Matrix<float>(1, 4), 0.0); }));
+    EXPECT(throws<shape_error>([] { hard_topk(Matrix<float>(1, 4), 101.0); }));
+}
+
+// test_router.cpp:12-30 and the router bit-exactness vs the oracle
+static void block_scores_tests() {
+    Matrix<float> z(16, 4, 0.f);
+    Matrix<float> pc = block_scores(z, z, RouterParams<float>::identity(4), 4, 2);
+    bool uniform_ok = true;
+    for (float v : pc.data()) uniform_ok &= (v == 1.0f / 8.0f);
+    EXPECT(uniform_ok);
+    const std::size_t n = 512, d = 32, bq = 32, bk = 16;
+    Matrix<float> q = gaussian(n, d, 103), k = gaussian(n, d, 104);
+    RouterParams<float> rp{gaussian(d, d, 105), gaussian(d, d, 106), 0.1f};
+    Matrix<float> got = block_scores(q, k, rp, bq, bk);
+    Matrix<float> ref(n / bq, n / bk);
+    sla2o_block_scores_f(q.data().data(), k.data().data(), n, d, rp.proj_q.data().data(), rp.proj_k.data().data(),
+                         0.1f, bq, bk, ref.data().data());
+    EXPECT(got.data() == ref.data());  // bit-exact
+    EXPECT(throws<numeric_error>([&] { block_scores(q, k, RouterParams<float>{rp.proj_q, rp.proj_k, 0.f}, bq, bk); }));
+}
+
+// quant.hpp:88-96 / test_quant.cpp:87-112
+static void smooth_k_tests() {
+    Matrix<float> k = gaussian(4096, 64, 209);
+    auto [kt, mu] = smooth_k(k);
+    std::vector<float> rkt(k.size()), rmu(64);
+    sla2o_smooth_k_f(k.data().data(), 4096, 64, rkt.data(), rmu.data());
+    EXPECT(kt.data() == rkt && mu.data() == rmu);  // bit-exact serial column mean
+    auto [kc, mc] = smooth_k(Matrix<float>(6, 3, 2.5f));
+    EXPECT(max_abs(kc) == 0.0f && mc[0] == 2.5f);
+}
+
+// test_attention.cpp:215-241, 305-311 through the fp32 path
+static void blockwise_tests() {
+    for (uint64_t seed : {351u, 352u, 353u}) {
+        for (double kp : {10.0, 25.0, 50.0}) {
+            const std::size_t n = 64, d = 8, bq = 8, bk = 4;
+            AttentionInputs<float> in{gaussian(n, d, seed), gaussian(n, d, seed + 1), gaussian(n, d, seed + 2), bq, bk};
+            auto [kt, mu] = smooth_k(in.k);
+            BlockMask mask = hard_topk(block_scores(in.q, kt, RouterParams<float>::identity(d), bq, bk), kp);
+            MixRatio<float> mix = MixRatio<float>::zeros(in.tm());
+            auto [out, saved] = sla2_forward_blockwise(in, Routing<float>{mask}, mix);
+            Matrix<float> ref(n, d);
+            sla2o_forward_blockwise_f(in.q.data().data(), in.k.data().data(), in.v.data().data(), n, d, bq, bk,
+                                      mask.bits.data(), mix.rho.data().data(), 0, 1, ref.data().data(), nullptr, nullptr,
+                                      nullptr);
+            EXPECT(max_abs_diff(out, ref) <= 1e-4f);
+        }
+    }
+    // empty row -> shape_error; soft routing -> contract_error
+    AttentionInputs<float> in{gaussian(16, 4, 362), gaussian(16, 4, 363), gaussian(16, 4, 364), 4, 4};
+    BlockMask mask = BlockMask::zeros(4, 4);
+    mask.at(0, 0) = mask.at(1, 1) = mask.at(2, 2) = 1;
+    EXPECT(throws<shape_error>([&] { sla2_forward_blockwise(in, Routing<float>{mask}, MixRatio<float>::zeros(4)); }));
+    EXPECT(throws<contract_error>(
+        [&] { sla2_forward_blockwise(in, Routing<float>{SoftMask<float>{}}, MixRatio<float>::zeros(4)); }));
+    // full mask: alpha forced to 1 -> O_s
+    auto [o, s] = sla2_forward_blockwise(in, Routing<float>{BlockMask::ones(4, 4)}, MixRatio<float>::constant(4, -5.f));
+    EXPECT(max_abs_diff(o, s.o_s) == 0.0f);
+}
+
+// the Tape::sla2_attention composition, fp32 (cfg1 blocks) and bf16 (Wan blocks)
+static void attention_tests() {
+    {
+        const std::size_t n = 4096, d = 64, bq = 64, bk = 64;
+        Matrix<float> q = gaussian(n, d, 1), k = gaussian(n, d, 2), v = gaussian(n, d, 3);
+        RouterParams<float> rp = RouterParams<float>::identity(d);
+        MixRatio<float> mix{Vector<float>(n / bq, 0.25f)};
+        b200::precision() = b200::Precision::fp32;
+        BlockMask mask;
+        Matrix<float> out = sla2_attention(q, k, v, mix, rp, bq, bk, 10.0, nullptr, true, &mask);
+        Matrix<float> ref(n, d);
+        std::vector<uint8_t> rmask((n / bq) * (n / bk));
+        sla2o_attention_f(q.data().data(), k.data().data(), v.data().data(), n, d, bq, bk, rp.proj_q.data().data(),
+                          rp.proj_k.data().data(), mix.rho.data().data(), 10.0, 0, 1, ref.data().data(), rmask.data(),
+                          nullptr, nullptr, nullptr);
+        EXPECT(mask.bits == rmask);
+        EXPECT(max_abs_diff(out, ref) <= 1e-4f);
+    }
+    {
+        const std::size_t n = 2048, d = 128, bq = 128, bk = 64;
+        Matrix<float> q = gaussian(n, d, 4), k = gaussian(n, d, 5), v = gaussian(n, d, 6);
+        for (auto* m : {&q, &k, &v})  // the bf16 path sees bf16-valued inputs
+            for (float& x : m->data()) x = __bfloat162float(__float2bfloat16_rn(x));
+        RouterParams<float> rp = RouterParams<float>::identity(d);
+        MixRatio<float> mix{Vector<float>(n / bq, 0.5f)};
+        b200::precision() = b200::Precision::bf16;
+        BlockMask mask;
+        Matrix<float> out = sla2_attention(q, k, v, mix, rp, bq, bk, 5.0, nullptr, true, &mask);
+        Matrix<float> ref(n, d);
+        std::vector<uint8_t> rmask((n / bq) * (n / bk));
+        sla2o_attention_f(q.data().data(), k.data().data(), v.data().data(), n, d, bq, bk, rp.proj_q.data().data(),
+                          rp.proj_k.data().data(), mix.rho.data().data(), 5.0, 0, 1, ref.data().data(), rmask.data(),
+                          nullptr, nullptr, nullptr);
+        EXPECT(mask.bits == rmask);
+        EXPECT(max_abs_diff(out, ref) <= 1e-2f * max_abs(ref));
+        b200::precision() = b200::Precision::fp32;
+    }
+}
+
+int main() {
+    hard_topk_kats();
+    block_scores_tests();
+    smooth_k_tests();
+    blockwise_tests();
+    attention_tests();
+    std::printf("shim tests: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
