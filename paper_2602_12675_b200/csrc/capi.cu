@@ -280,7 +280,9 @@ int64_t sla2_topk_budget(double k_percent, int64_t tn) {
     return kappa < tn ? kappa : tn;
 }
 
-sla2_status sla2_check_params(const sla2_fwd_params* p) {
+// Checks the reference's own prologues make (shapes, budget, tau) plus the dtype/quant enums;
+// enough for the router entry points, which have no kernel-geometry limits.
+static sla2_status check_common(const sla2_fwd_params* p) {
     g_last_error.clear();
     if (!p) return fail(SLA2_CONTRACT_ERROR, "params is NULL");
     if (p->B <= 0 || p->H <= 0 || p->N <= 0 || p->d <= 0)
@@ -295,6 +297,12 @@ sla2_status sla2_check_params(const sla2_fwd_params* p) {
         return fail(SLA2_CONTRACT_ERROR, "unknown quant mode");
     if (p->N * p->B * p->H > (int64_t)INT32_MAX)
         return fail(SLA2_CONTRACT_ERROR, "B*H*N exceeds the 2^31 row limit of the TMA descriptors");
+    return SLA2_OK;
+}
+
+sla2_status sla2_check_params(const sla2_fwd_params* p) {
+    sla2_status s = check_common(p);
+    if (s != SLA2_OK) return s;
     if (p->dtype == SLA2_BF16) {
         if (p->d != 128 || p->bq != 128 || p->bk != 64)
             return fail(SLA2_CONTRACT_ERROR,
@@ -302,8 +310,8 @@ sla2_status sla2_check_params(const sla2_fwd_params* p) {
     } else {
         if (p->quant != SLA2_QUANT_NONE)
             return fail(SLA2_CONTRACT_ERROR, "INT8 QAT mode runs on the bf16 inputs path");
-        if (p->d > 128 || p->bk > 128 || p->bq > 256 || p->bq < 1 || (256 % p->bq) != 0 || 256 / p->bq > 32)
-            return fail(SLA2_CONTRACT_ERROR, "fp32 path: d <= 128, bk <= 128, bq a power of two in [8, 256]");
+        if (p->d > 128 || p->bk > 128 || p->bq > 256 || p->bq < 1 || (256 % p->bq) != 0)
+            return fail(SLA2_CONTRACT_ERROR, "fp32 path: d <= 128, bk <= 128, bq a power of two <= 256");
         if (sparse_f32_smem_bytes((int)p->d, (int)p->bq, (int)p->bk) > 227 * 1024)
             return fail(SLA2_CONTRACT_ERROR, "fp32 path: bq*d + 3*bk*d + bq*bk exceeds shared memory");
     }
@@ -311,7 +319,7 @@ sla2_status sla2_check_params(const sla2_fwd_params* p) {
 }
 
 size_t sla2_workspace_size(const sla2_fwd_params* p) {
-    if (sla2_check_params(p) != SLA2_OK) return 0;
+    if (check_common(p) != SLA2_OK) return 0;  // layout does not depend on kernel limits
     return carve(geometry(p), nullptr, nullptr);
 }
 
@@ -384,7 +392,44 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.tm_v = &mv;
         sa.tm_phik = &mphi;
         sa.tm_ht = &mht;
-        if (g.quant) return fail(SLA2_CONTRACT_ERROR, "INT8 QAT sparse kernel not available in this build");
+        if (g.quant) {
+            // INT8 QAT (QuantConfig, quant.hpp:15-19): per-tile codes + scales, then the kind::i8 kernel
+            QuantLaunch qa{};
+            qa.B = g.B;
+            qa.H = g.H;
+            qa.N = (int)g.N;
+            qa.d = (int)g.d;
+            qa.bq = (int)g.bq;
+            qa.bk = (int)g.bk;
+            qa.tm = (int)g.tm;
+            qa.tn = (int)g.tn;
+            qa.q = q;
+            qa.k = k;
+            qa.v = v;
+            qa.mu = w.mu;
+            qa.smooth = p->smooth;
+            qa.qc = w.qc;
+            qa.qs = w.qs;
+            qa.kc = w.kc;
+            qa.ks = w.ks;
+            qa.vct = w.vct;
+            qa.vs = w.vs;
+            SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+            CUtensorMap mqc, mkc, mvc;
+            if (!make_map(&mqc, w.qc, rows, g.d, 128, 128, 1) || !make_map(&mkc, w.kc, rows, g.d, 128, 64, 1) ||
+                !make_map(&mvc, w.vct, rows, g.d, 128, 64, 1))
+                return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (int8 codes)");
+            SparseI8Launch ia{};
+            ia.s = sa;
+            ia.qs = w.qs;
+            ia.ks = w.ks;
+            ia.vs = w.vs;
+            ia.tm_qc = &mqc;
+            ia.tm_kc = &mkc;
+            ia.tm_vct = &mvc;
+            SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
+            return SLA2_OK;
+        }
         SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
     } else {
         SLA2_CUDA_TRY(launch_sparse_f32(sa, st, &g_launches));
@@ -396,7 +441,7 @@ sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, 
                         const float* proj_k, float* pc_out, uint8_t* mask_out, int32_t* kv_idx_out, void* workspace,
                         size_t workspace_bytes, void* stream) {
     g_launches = 0;
-    sla2_status s = sla2_check_params(p);
+    sla2_status s = check_common(p);
     if (s != SLA2_OK) return s;
     if ((s = check_device()) != SLA2_OK) return s;
     const Geo g = geometry(p);
@@ -465,7 +510,7 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
 
 sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_out, float* ktilde_out, void* stream) {
     g_launches = 0;
-    sla2_status s = sla2_check_params(p);
+    sla2_status s = check_common(p);
     if (s != SLA2_OK) return s;
     if ((s = check_device()) != SLA2_OK) return s;
     if (!k || !mean_out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) sla2_sparse_f32_kernel(SparseLaunch a) {
     const int h = (int)(bh % a.H);
     const int tid = threadIdx.x;
     const int r = tid / TPR, q = tid % TPR;
+    const bool act = r < bq;  // bq < 8: the row groups past bq only help with the Hsel entries
     const bool dense = a.dense != 0;
     const int nb = dense ? a.tn : (a.kv_cnt ? a.kv_cnt[bh * a.tm + i] : a.kappa);
     const int32_t* idx = a.kv_idx + (bh * a.tm + i) * (int64_t)a.kstride;
@@ -65,14 +66,14 @@ __global__ void __launch_bounds__(256) sla2_sparse_f32_kernel(SparseLaunch a) {
 
     constexpr int MAXC = 64;  // O columns per thread (d / TPR <= 64)
     float o[MAXC];
-    const int nc = q < d ? (d - q + TPR - 1) / TPR : 0;  // O columns c = q + TPR*u of this thread
+    const int nc = (act && q < d) ? (d - q + TPR - 1) / TPR : 0;  // O columns c = q + TPR*u of this thread
     for (int u = 0; u < nc; ++u) o[u] = 0.0f;
     float hs[64];
     const int dd = d * d;
     const int nh = (dd + 255) / 256;
     for (int u = 0; u < nh; ++u) hs[u] = 0.0f;
     float m = -INFINITY, l = 0.0f;
-    const int ns = q < bk ? (bk - q + TPR - 1) / TPR : 0;  // S entries t = q + TPR*v of this thread
+    const int ns = (act && q < bk) ? (bk - q + TPR - 1) / TPR : 0;  // S entries t = q + TPR*v of this thread
 
     for (int jj = 0; jj < nb; ++jj) {
         const int kb = dense ? jj : idx[jj];
@@ -178,13 +179,13 @@ __global__ void __launch_bounds__(256) sla2_sparse_f32_kernel(SparseLaunch a) {
             if (a.o_l) a.o_l[grow * d + c] = 0.0f;
         }
     }
-    if (a.big_l && q == 0) a.big_l[grow] = m + logf(l);
+    if (act && a.big_l && q == 0) a.big_l[grow] = m + logf(l);
 }
 
 cudaError_t launch_sparse_f32(const SparseLaunch& a, cudaStream_t st, int* launches) {
     const size_t smem = sparse_f32_smem_bytes(a.d, a.bq, a.bk);
     dim3 grid(a.tm, (unsigned)(a.B * a.H));
-    const int tpr = 256 / a.bq;
+    const int tpr = a.bq >= 8 ? 256 / a.bq : 32;  // bq < 8: 8 row groups, the extra ones idle
 #define SLA2_F32_CASE(T)                                                                              \
     case T:                                                                                           \
         cudaFuncSetAttribute(sla2_sparse_f32_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

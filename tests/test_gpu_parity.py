@@ -96,9 +96,33 @@ def test_forward_bf16_batch_layout(cuda):
             assert rel_err(out[b, h], r)[0] <= BF16_TOL
 
 
+# ----------------------------------------------------------------------------- INT8 QAT forward
+@pytest.mark.parametrize("N,H,k_percent,seed", [(4096, 2, 3.0, 51), (8192, 1, 10.0, 52), (2048, 1, 100.0, 53)])
+def test_forward_qat_vs_oracle(cuda, N, H, k_percent, seed):
+    """QuantConfig INT8 on QK and PV (quant.hpp:15-19): codes, scales and S are the
+    reference's; output within the low-bit tolerance of the oracle's QAT forward."""
+    torch = _torch()
+    B, d, bq, bk = 1, 128, 128, 64
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, seed)
+    out, mask, sv = sla2.forward(to_dev(q, torch.bfloat16, cuda), to_dev(k, torch.bfloat16, cuda),
+                                 to_dev(v, torch.bfloat16, cuda), to_dev(pq, torch.float32, cuda),
+                                 to_dev(pk, torch.float32, cuda), to_dev(rho, torch.float32, cuda),
+                                 k_percent=k_percent, quant=True, return_mask=True, saved=True)
+    out = out.float().cpu().numpy()
+    for h in range(H):
+        r_out, r_mask, r_os, r_ol, r_l = oracle_head(q[0, h], k[0, h], v[0, h], pq[h], pk[h], rho[h], bq, bk,
+                                                     k_percent, quant=True)
+        assert np.array_equal(mask.cpu().numpy()[0, h], r_mask)
+        assert rel_err(out[0, h], r_out)[0] <= BF16_TOL
+        assert rel_err(sv["o_s"].cpu().numpy()[0, h], r_os)[0] <= BF16_TOL
+        np.testing.assert_allclose(sv["big_l"].cpu().numpy()[0, h], r_l, atol=1e-3, rtol=1e-4)
+
+
 # ----------------------------------------------------------------------------- fp32 forward
 @pytest.mark.parametrize("N,d,bq,bk,k_percent", [(4096, 64, 64, 64, 10.0), (1024, 32, 32, 16, 25.0),
-                                                 (64, 8, 8, 4, 10.0), (64, 8, 8, 4, 50.0)])
+                                                 (64, 8, 8, 4, 10.0), (64, 8, 8, 4, 50.0),
+                                                 (32, 8, 4, 4, 25.0), (32, 8, 4, 8, 25.0),   # bq < 8
+                                                 (2048, 128, 128, 64, 5.0)])                 # Wan blocks, fp32
 def test_forward_f32_vs_oracle(cuda, N, d, bq, bk, k_percent):
     torch = _torch()
     B, H = 1, 2
