@@ -5,13 +5,13 @@
 // helpers block_scores_qk / block_product_pv (attention.hpp:372-415), for bq = 128, bk = 64,
 // d = 128 (the paper's blocks), bf16 operands, fp32 accumulation.
 //
-// Per CTA (query block i of head bh, kept key blocks j_0 < j_1 < ... from the router):
-//   S_j   = Q_i K_j^T                      tcgen05 kind::f16 "TS": Q resident in TMEM (A),
-//                                          K_j from smem (B), M128 N64 K128 -> TMEM (2 buffers)
-//   P_j   = exp2(S_j*log2e/sqrt(d) - m)    softmax warps, online max with lazy rescale; P is
-//                                          written back over S_j in TMEM as packed bf16
-//   O    += P_j V_j                        TS: P from TMEM, V_j from smem, M128 N128 K64
-//   Hsel += phi(K~_j)^T V_j                SS, M128 N128 K64 (MN-major A and B)
+// Per CTA (query block i of head bh, kept key blocks j_0 < j_1 < ... from the router), key
+// blocks are processed in PAIRS (2p, 2p+1) in ascending order:
+//   S_pair = Q_i [K_2p; K_2p+1]^T          tcgen05 kind::f16 SS, M128 N128 K128 -> TMEM (2 pair buffers)
+//   P      = exp2(S*log2e/sqrt(d) - m)      softmax warps, lazily rescaled running max; P is
+//                                           written back over each block's S in TMEM as bf16
+//   O     += P_j V_j                        TS: P from TMEM, V_j from smem, M128 N128 K64
+//   Hsel  += phi(K~_j)^T V_j                SS, M128 N128 K64 (MN-major A and B)
 // epilogue (fused, attention.hpp:532-557):
 //   O_s = O / l
 //   Hc  = Htot - Hsel, Zc = Ztot - sum_sel z_j      ("total minus selected" = the
@@ -21,14 +21,13 @@
 // The raw K is used for Q K^T: smoothing shifts every score of a row by the same constant
 // (test_attention.cpp:270-279), so O_s is unchanged and K needs no bf16 re-rounding.
 //
-// Shared memory bandwidth (128 B/clk/SM) is the scarce resource: Q and P live in TMEM, so per
-// key block smem sees only the TMA writes of K, V, phi(K) and the B/A operand reads. K has its
-// own 4-deep ring released as soon as its QK MMA completes; V/phi(K) a 3-deep ring released
-// after PV/HS. The MMA thread polls (try_wait) so a late tile never blocks a ready MMA.
+// Why pairs: on B200 a kind::f16 M128 tcgen05.mma costs max(~96, N/2) cycles
+// (tools/umma_bench.py), so Q K^T over one 64-key block (N = 64) runs at a third of the
+// tensor rate; two blocks per instruction (N = 128) halve the QK instruction count.
 //
-// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K ring), w1 MMA issuer, w2 TMEM
-// allocator + TMA producer (V/phi(K) ring, Htot), w3 Zc then phi(Q) and its denominators
-// (overlapped with the main loop), w4-7 softmax / correction / epilogue (thread = query row).
+// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K pair ring), w1 MMA issuer, w2 TMEM
+// allocator + TMA producer (V / phi(K) ring, Htot), w3 Zc then phi(Q) and its denominators
+// (after the last Q K^T), w4-7 softmax / correction / epilogue (thread = query row).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -43,22 +42,22 @@ namespace sla2dev {
 
 namespace sp {
 constexpr int BQ = 128, BK = 64, D = 128;
-constexpr int NSK = 4, NSV = 3;
+constexpr int NKP = 2, NSV = 4;
 constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
-constexpr uint32_t HT_BYTES = D * D * 2;     // 32 KB Htot (bf16)
+constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // K pair: [k_atom 2][128 rows][128 B]
+constexpr uint32_t HT_BYTES = D * D * 2;     // 32 KB Htot (bf16), staged in a free V stage
 constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
-constexpr uint32_t OFF_V = OFF_K + NSK * TILE_BYTES;
-constexpr uint32_t OFF_HT = OFF_V + NSV * 2 * TILE_BYTES;
-constexpr uint32_t SMEM_BYTES = OFF_HT + HT_BYTES;  // 224 KB
+constexpr uint32_t OFF_V = OFF_K + NKP * KP_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_V + NSV * 2 * TILE_BYTES;  // 224 KB
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
 // TMEM columns (512 allocated)
-constexpr uint32_t TM_Q = 0;      // Q_i as the A operand: 128 lanes x 64 cols (bf16 pairs)
-constexpr uint32_t TM_S = 64;     // 2 x 64: S_j fp32, then P_j bf16 in its first 32 cols
-constexpr uint32_t TM_O = 192;    // 128: O accumulator
-constexpr uint32_t TM_H = 320;    // 128: Hsel accumulator
-constexpr uint32_t TM_L = TM_S;   // 128: phi(Q) Hc after the loop (S/P area is free then)
+constexpr uint32_t TM_S = 0;      // 2 pair buffers x 128: S fp32 (block 2p in cols 0-63,
+                                  // 2p+1 in 64-127), then each block's P bf16 in its first 32
+constexpr uint32_t TM_O = 256;    // 128: O accumulator
+constexpr uint32_t TM_H = 384;    // 128: Hsel accumulator
+constexpr uint32_t TM_L = 0;      // 128: phi(Q) Hc after the loop (S/P area is free then)
 constexpr float RESCALE_LOG2 = 8.0f;  // lazy rescale threshold (P <= 2^8)
 }  // namespace sp
 
@@ -108,7 +107,8 @@ __global__ void __launch_bounds__(256, 1)
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_qt, bar_phiq, bar_ht, bar_k_full[NSK], bar_k_empty[NSK], bar_v_full[NSV],
+    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_phiq, bar_ht, bar_k_full[NKP], bar_k_empty[NKP],
+        bar_v_full[NSV],
         bar_v_empty[NSV], bar_s_full[2], bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
@@ -120,16 +120,18 @@ __global__ void __launch_bounds__(256, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool dense = p.dense != 0;
     const int nb = dense ? p.tn : (p.kv_cnt ? p.kv_cnt[bh * p.tm + i] : p.kappa);
+    const int npair = (nb + 1) >> 1;
     const int32_t* idx = p.kv_idx + (bh * p.tm + i) * (int64_t)p.kstride;
     const bool full_row = dense || (nb == p.tn);
     const bool linear = !full_row;
 
     if (threadIdx.x == 0) {
         mbar_init(&bar_q, 1);
-        mbar_init(&bar_qt, 128);
+        mbar_init(&bar_qk_done, 1);
+        mbar_init(&bar_mma_done, 1);
         mbar_init(&bar_phiq, 32);
         mbar_init(&bar_ht, 1);
-        for (int s = 0; s < NSK; ++s) {
+        for (int s = 0; s < NKP; ++s) {
             mbar_init(&bar_k_full[s], 1);
             mbar_init(&bar_k_empty[s], 1);
         }
@@ -154,14 +156,17 @@ __global__ void __launch_bounds__(256, 1)
     if (threadIdx.x == 0) SLA2_TR(0);
 
     uint8_t* sQ = smem + OFF_Q;
-    uint8_t* sHt = smem + OFF_HT;
-    auto sK = [&](int s) { return smem + OFF_K + s * TILE_BYTES; };
+    auto sKp = [&](int s) { return smem + OFF_K + s * KP_BYTES; };
     auto sV = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES; };
     auto sPh = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES + TILE_BYTES; };
-    uint8_t* sHc = smem + OFF_V;  // epilogue alias of V/phi stage 0 (32 KB, free after the loop)
+    // epilogue buffers in V stages: Htot goes where block nb would have gone (loaded by the V
+    // producer once that stage drains), Hc into the next one (free once every PV is done)
+    uint8_t* sHt = sV(nb % NSV);
+    uint8_t* sHc = sV((nb + 1) % NSV);
+    auto kblock = [&](int j) { return dense ? j : idx[j]; };
 
     if (warp == 0) {
-        // ===================== TMA producer: Q, K ring =====================
+        // ===================== TMA producer: Q, K pair ring =====================
         if (lane == 0) {
             tma_prefetch_desc(&tmQ);
             tma_prefetch_desc(&tmK);
@@ -172,16 +177,19 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sQ + 8192, &tmQ, 0, qrow + 64, &bar_q);
             tma_load_2d(sQ + 16384, &tmQ, 64, qrow, &bar_q);
             tma_load_2d(sQ + 24576, &tmQ, 64, qrow + 64, &bar_q);
-            for (int j = 0; j < nb; ++j) {
-                const int s = j % NSK;
-                if (j >= NSK) mbar_wait(&bar_k_empty[s], ((j / NSK) - 1) & 1);
-                const int kb = dense ? j : idx[j];
-                const int krow = (int)(bh * p.N + (int64_t)kb * BK);
-                if (j == 0) SLA2_TR(54);
-                if (j == nb - 1) SLA2_TR(55);
-                mbar_arrive_expect_tx(&bar_k_full[s], TILE_BYTES);
-                tma_load_2d_hint(sK(s), &tmK, 0, krow, &bar_k_full[s], pol_keep);
-                tma_load_2d_hint(sK(s) + 8192, &tmK, 64, krow, &bar_k_full[s], pol_keep);
+            for (int n = 0; n < npair; ++n) {
+                const int s = n % NKP;
+                if (n >= NKP) mbar_wait(&bar_k_empty[s], ((n / NKP) - 1) & 1);
+                const int cnt = min(2, nb - 2 * n);
+                if (n == 0) SLA2_TR(54);
+                if (n == npair - 1) SLA2_TR(55);
+                mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
+                for (int b = 0; b < cnt; ++b) {
+                    const int krow = (int)(bh * p.N + (int64_t)kblock(2 * n + b) * BK);
+                    // rows b*64.. of each 128-row k-atom: [cols 0-63] then [cols 64-127]
+                    tma_load_2d_hint(sKp(s) + b * 8192, &tmK, 0, krow, &bar_k_full[s], pol_keep);
+                    tma_load_2d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, &bar_k_full[s], pol_keep);
+                }
             }
         }
     } else if (warp == 2) {
@@ -194,8 +202,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < nb; ++j) {
                 const int s = j % NSV;
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
-                const int kb = dense ? j : idx[j];
-                const int krow = (int)(bh * p.N + (int64_t)kb * BK);
+                const int krow = (int)(bh * p.N + (int64_t)kblock(j) * BK);
                 mbar_arrive_expect_tx(&bar_v_full[s], tx);
                 tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol_keep);
                 tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol_keep);
@@ -203,78 +210,89 @@ __global__ void __launch_bounds__(256, 1)
                     tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol_keep);
                     tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol_keep);
                 }
-                if (j == 0 && linear) {
-                    // Htot of this head, bf16 [f][c] as the MN-major B layout [c_atom][f][64]
-                    tma_prefetch_desc(&tmHt);
-                    mbar_arrive_expect_tx(&bar_ht, HT_BYTES);
-                    tma_load_2d_hint(sHt, &tmHt, 0, (int)(bh * D), &bar_ht, pol_keep);
-                    tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol_keep);
-                }
+            }
+            if (linear) {
+                // Htot of this head, bf16 [f][c] as the MN-major B layout [c_atom][f][64], into the
+                // stage block nb would use (same wait rule as a V load)
+                const int s = nb % NSV;
+                if (nb >= NSV) mbar_wait(&bar_v_empty[s], ((nb / NSV) - 1) & 1);
+                tma_prefetch_desc(&tmHt);
+                mbar_arrive_expect_tx(&bar_ht, HT_BYTES);
+                tma_load_2d_hint(sHt, &tmHt, 0, (int)(bh * D), &bar_ht, pol_keep);
+                tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol_keep);
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =====================
         if (lane == 0) {
-            constexpr uint32_t ID_QK = idesc_bf16(128, 64, false, false);
+            constexpr uint32_t ID_QK2 = idesc_bf16(128, 128, false, false);
+            constexpr uint32_t ID_QK1 = idesc_bf16(128, 64, false, false);
             constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
             constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
-            mbar_wait(&bar_qt, 0);  // Q resident in TMEM
+            const uint32_t aQ = smem_u32(sQ);
+            mbar_wait(&bar_q, 0);
             tc_fence_after();
             SLA2_TR(1);
-            // Three in-order streams polled without blocking:
-            //   QK_n: K_n landed and S[n&1] reusable (PV_{n-2} issued: MMAs of one thread run
-            //         in issue order, so QK_n cannot overwrite P_{n-2} before PV_{n-2} read it)
-            //   HS_n: V_n/phi_n landed (only needs tiles)
-            //   PV_n: P_n written and HS_n issued (v_empty after PV covers both)
-            int nq = 0, nh = 0, np = 0;
-            while (np < nb) {
-                bool progress = false;
-                if (nq < nb && nq <= np + 1 && mbar_try_wait(&bar_k_full[nq % NSK], (nq / NSK) & 1)) {
-                    tc_fence_after();
-                    const int b = nq & 1;
-                    const uint32_t bK = smem_u32(sK(nq % NSK));
+            // Static issue order. The tensor pipe runs one thread's MMAs in issue order, so the
+            // order is the schedule:
+            //   QK(0), QK(1); for each pair n: [P(n)] PV(n) -> QK(n+2) -> HS(n)
+            // PV(n) enters the pipe as soon as P(n) exists; QK(n+2) (which reuses S buffer n&1,
+            // safe because PV(n) precedes it) runs before the HS filler, so S(n+2) is ready when
+            // the softmax gets to it; HS(n) fills the pipe while the softmax works on n+1.
+            auto issue_qk = [&](int n) {
+                const int s = n % NKP, b = n & 1;
+                mbar_wait(&bar_k_full[s], (n / NKP) & 1);
+                tc_fence_after();
+                const bool two = 2 * n + 1 < nb;
+                const uint32_t bK = smem_u32(sKp(s));
 #pragma unroll
-                    for (int ks = 0; ks < 8; ++ks)
-                        umma_bf16_ts(tmem + TM_S + b * 64, tmem + TM_Q + ks * 8,
-                                     sdesc_sw128(bK + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024), ID_QK, ks > 0);
-                    umma_commit(&bar_s_full[b]);
-                    umma_commit(&bar_k_empty[nq % NSK]);
-                    ++nq;
-                    progress = true;
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+                    umma_bf16_ss(tmem + TM_S + b * 128, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(bK + off, 16, 1024),
+                                 two ? ID_QK2 : ID_QK1, ks > 0);
                 }
-                if (!dense && nh < nb && nh <= np + 1 && mbar_try_wait(&bar_v_full[nh % NSV], (nh / NSV) & 1)) {
+                umma_commit(&bar_s_full[b]);
+                umma_commit(&bar_k_empty[s]);
+                if (n == npair - 1) umma_commit(&bar_qk_done);
+            };
+            if (npair > 0) issue_qk(0);
+            if (npair > 1) issue_qk(1);
+            for (int n = 0; n < npair; ++n) {
+                const int j0 = 2 * n, j1 = min(nb, j0 + 2);
+                mbar_wait(&bar_p_full[n & 1], (n >> 1) & 1);
+                tc_fence_after();
+                for (int j = j0; j < j1; ++j) {
+                    mbar_wait(&bar_v_full[j % NSV], (j / NSV) & 1);
                     tc_fence_after();
-                    const uint32_t aH = smem_u32(sPh(nh % NSV)), bV = smem_u32(sV(nh % NSV));
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
-                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (nh > 0 || ks > 0));
-                    ++nh;
-                    progress = true;
-                }
-                if (np < nq && (dense || np < nh) && mbar_try_wait(&bar_p_full[np & 1], (np >> 1) & 1)) {
-                    if (dense) mbar_wait(&bar_v_full[np % NSV], (np / NSV) & 1);
-                    tc_fence_after();
-                    const int b = np & 1;
-                    const uint32_t bV = smem_u32(sV(np % NSV));
+                    const uint32_t bV = smem_u32(sV(j % NSV));
+                    const uint32_t aP = tmem + TM_S + (n & 1) * 128 + (j & 1) * 64;
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
-                        umma_bf16_ts(tmem + TM_O, tmem + TM_S + b * 64 + ks * 8,
-                                     sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV, (np > 0 || ks > 0));
-                    umma_commit(&bar_pv_done[b]);
-                    if (np < 16) SLA2_TR(34 + np);
-                    umma_commit(&bar_v_empty[np % NSV]);
-                    ++np;
-                    progress = true;
+                        umma_bf16_ts(tmem + TM_O, aP + ks * 8, sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV,
+                                     (j > 0 || ks > 0));
+                    if (dense) umma_commit(&bar_v_empty[j % NSV]);
                 }
-                (void)progress;
+                umma_commit(&bar_pv_done[n & 1]);
+                if (n < 16) SLA2_TR(34 + n);
+                if (n + 2 < npair) issue_qk(n + 2);
+                if (!dense) {
+                    for (int j = j0; j < j1; ++j) {
+                        const uint32_t aH = smem_u32(sPh(j % NSV)), bV = smem_u32(sV(j % NSV));
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
+                                         sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (j > 0 || ks > 0));
+                        umma_commit(&bar_v_empty[j % NSV]);  // after PV_j and HS_j
+                    }
+                }
             }
+            umma_commit(&bar_mma_done);  // every QK / PV / HS of the loop
             if (linear) {
                 // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
                 mbar_wait(&bar_lin_ready, 0);
                 mbar_wait(&bar_phiq, 0);
                 tc_fence_after();
-                const uint32_t aQ = smem_u32(sQ), bH = smem_u32(sHc);
+                const uint32_t bH = smem_u32(sHc);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
                     const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
@@ -321,9 +339,10 @@ __global__ void __launch_bounds__(256, 1)
             sZc[lane * 4 + 2] = zt.z - acc.z;
             sZc[lane * 4 + 3] = zt.w - acc.w;
             __syncwarp();
-            // Q has been copied into TMEM by the softmax warps: overwrite sQ with phi(Q)
-            // (row softmax over d, attention.hpp:456) in bf16, the A operand of the final MMA.
-            mbar_wait(&bar_qt, 0);
+            // Q is the A operand of every Q K^T: overwrite sQ with phi(Q) only after the last one
+            // (row softmax over d, attention.hpp:456, bf16 -- the A operand of the final MMA).
+            mbar_wait(&bar_q, 0);
+            mbar_wait(&bar_qk_done, 0);
             __syncwarp();
             const uint32_t qb = smem_u32(sQ);
             for (int u = 0; u < 4; ++u) {
@@ -373,47 +392,39 @@ __global__ void __launch_bounds__(256, 1)
         // ===================== softmax / correction / epilogue =====================
         const int r = threadIdx.x - 128;  // query row within the block
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        // Q row r -> TMEM lane r, columns TM_Q + c hold elements (2c, 2c+1)
-        mbar_wait(&bar_q, 0);
-        __syncwarp();
-        {
-            const uint32_t qb = smem_u32(sQ);
-            uint32_t w[32];
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
-                    ld_shared_v4(qb + half * 16384 + sw128_off(r, ch * 8), w[ch * 4 + 0], w[ch * 4 + 1], w[ch * 4 + 2],
-                                 w[ch * 4 + 3]);
-                tmem_st32(tmem + lane_base + TM_Q + half * 32, w);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&bar_qt);
-        }
         float m2 = -INFINITY, l = 0.0f;
-        for (int j = 0; j < nb; ++j) {
-            const int b = j & 1;
-            mbar_wait(&bar_s_full[b], (j >> 1) & 1);
+        for (int n = 0; n < npair; ++n) {
+            const int b = n & 1;
+            const bool two = 2 * n + 1 < nb;
+            mbar_wait(&bar_s_full[b], (n >> 1) & 1);
             __syncwarp();
-            if (r == 0 && j < 16) SLA2_TR(2 + j);
+            if (r == 0 && n < 16) SLA2_TR(2 + n);
             tc_fence_after();
-            uint32_t sr[64];
-            tmem_ld32(tmem + lane_base + TM_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_ld32(tmem + lane_base + TM_S + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            const uint32_t sbase = tmem + lane_base + TM_S + b * 128;
+            uint32_t sr[128];
+            tmem_ld32(sbase, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+            tmem_ld32(sbase + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            if (two) {
+                tmem_ld32(sbase + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+                tmem_ld32(sbase + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+            }
             tmem_ld_wait();
             float mx = -INFINITY;
 #pragma unroll
             for (int t = 0; t < 64; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
+            if (two) {
+#pragma unroll
+                for (int t = 64; t < 128; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
+            }
             mx *= p.scale_log2;
-            if (j == 0) {
+            if (n == 0) {
                 m2 = mx;
             } else {
                 const bool need = mx > m2 + RESCALE_LOG2;
                 if (__any_sync(0xffffffffu, need)) {
                     const float mnew = fmaxf(m2, mx);
                     const float corr = fast_exp2(m2 - mnew);
-                    mbar_wait(&bar_pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                    mbar_wait(&bar_pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);  // all PVs so far done
                     __syncwarp();
                     tc_fence_after();
 #pragma unroll
@@ -429,26 +440,30 @@ __global__ void __launch_bounds__(256, 1)
                     m2 = mnew;
                 }
             }
-            // P = exp2(s * scale - m2) as packed bf16 over S_j's first 32 columns
-            uint32_t w[32];
+            // P = exp2(s * scale - m2) as packed bf16 over each block's first 32 S columns
             float rs0 = 0.0f, rs1 = 0.0f;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * e]), p.scale_log2, -m2));
-                const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * e + 1]), p.scale_log2, -m2));
-                rs0 += p0;
-                rs1 += p1;
-                w[e] = pack_bf16(p0, p1);
+            for (int blk = 0; blk < 2; ++blk) {
+                if (blk == 1 && !two) break;
+                uint32_t w[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e]), p.scale_log2, -m2));
+                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e + 1]), p.scale_log2, -m2));
+                    rs0 += p0;
+                    rs1 += p1;
+                    w[e] = pack_bf16(p0, p1);
+                }
+                tmem_st32(sbase + blk * 64, w);
             }
-            tmem_st32(tmem + lane_base + TM_S + b * 64, w);
             l += rs0 + rs1;
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&bar_p_full[b]);
-            if (r == 0 && j < 16) SLA2_TR(18 + j);
+            if (r == 0 && n < 16) SLA2_TR(18 + n);
         }
-        // all MMAs of the main loop complete
-        if (nb > 0) mbar_wait(&bar_pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+        // all MMAs of the main loop complete (the last HS may come after the last PV)
+        mbar_wait(&bar_mma_done, 0);
         __syncwarp();
         tc_fence_after();
         if (r == 0) SLA2_TR(50);
