@@ -26,8 +26,9 @@
 // tensor rate; two blocks per instruction (N = 128) halve the QK instruction count.
 //
 // Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K pair ring), w1 MMA issuer, w2 TMEM
-// allocator + TMA producer (V / phi(K) ring, Htot), w3 Zc then phi(Q) and its denominators
-// (after the last Q K^T), w4-7 softmax / correction / epilogue (thread = query row).
+// allocator + TMA producer (V / phi(K) ring, Htot), w3 Zc; then w0, w2, w3 together compute
+// phi(Q) and its denominators after the last Q K^T (so it overlaps the loop's tail), w4-7
+// softmax / correction / epilogue (thread = query row).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -100,6 +101,48 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// phi(Q) for query row r, in place over the row of sQ (row softmax over d, attention.hpp:456,
+// rounded to bf16 -- it is the A operand of the final MMA), and den[r] = phi(Q)_r . Zc.
+__device__ __forceinline__ void phiq_row(uint32_t qb, int r, const float* sZc, float* sDen) {
+    float qv[128];
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) {
+        uint32_t w[4];
+        ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+            qv[ch * 8 + 2 * e] = f2.x;
+            qv[ch * 8 + 2 * e + 1] = f2.y;
+        }
+    }
+    float qm = -INFINITY;
+#pragma unroll
+    for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
+    float qs = 0.0f;
+#pragma unroll
+    for (int f = 0; f < 128; ++f) {
+        qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
+        qs += qv[f];
+    }
+    const float qinv = 1.0f / qs;
+    float den = 0.0f;
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int f = ch * 8 + 2 * e;
+            const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
+            const float2 pr = __bfloat1622float2(pk);
+            den += pr.x * sZc[f] + pr.y * sZc[f + 1];
+            w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+        }
+        st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
+    }
+    sDen[r] = den;
+}
+
 __global__ void __launch_bounds__(256, 1)
     sla2_sparse_bf16_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
@@ -107,12 +150,13 @@ __global__ void __launch_bounds__(256, 1)
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_phiq, bar_ht, bar_k_full[NKP], bar_k_empty[NKP],
+    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_phiq, bar_zc, bar_ht, bar_k_full[NKP], bar_k_empty[NKP],
         bar_v_full[NSV],
         bar_v_empty[NSV], bar_s_full[2], bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
     __shared__ float sDen[BQ];
+    __shared__ int phiq_ctr;
 
     const int i = blockIdx.x;       // query block
     const int64_t bh = blockIdx.y;  // (b, h)
@@ -129,7 +173,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(&bar_q, 1);
         mbar_init(&bar_qk_done, 1);
         mbar_init(&bar_mma_done, 1);
-        mbar_init(&bar_phiq, 32);
+        mbar_init(&bar_phiq, 96);
+        mbar_init(&bar_zc, 1);
+        phiq_ctr = 0;
         mbar_init(&bar_ht, 1);
         for (int s = 0; s < NKP; ++s) {
             mbar_init(&bar_k_full[s], 1);
@@ -164,6 +210,27 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sHt = sV(nb % NSV);
     uint8_t* sHc = sV((nb + 1) % NSV);
     auto kblock = [&](int j) { return dense ? j : idx[j]; };
+    // phi(Q) over sQ, shared by warps 0, 2 and 3 once their own work is issued: Q is the A
+    // operand of every Q K^T, so rows are overwritten only after the last one (bar_qk_done);
+    // warps claim 32-row chunks. Every thread of the three warps arrives on bar_phiq once.
+    auto phiq_share = [&]() {
+        if (!linear) return;
+        __syncwarp();
+        mbar_wait(&bar_q, 0);
+        mbar_wait(&bar_zc, 0);
+        mbar_wait(&bar_qk_done, 0);
+        __syncwarp();
+        const uint32_t qb = smem_u32(sQ);
+        for (;;) {
+            int c = 0;
+            if (lane == 0) c = atomicAdd(&phiq_ctr, 32);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c >= BQ) break;
+            phiq_row(qb, c + lane, sZc, sDen);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&bar_phiq);
+    };
 
     if (warp == 0) {
         // ===================== TMA producer: Q, K pair ring =====================
@@ -339,54 +406,7 @@ __global__ void __launch_bounds__(256, 1)
             sZc[lane * 4 + 2] = zt.z - acc.z;
             sZc[lane * 4 + 3] = zt.w - acc.w;
             __syncwarp();
-            // Q is the A operand of every Q K^T: overwrite sQ with phi(Q) only after the last one
-            // (row softmax over d, attention.hpp:456, bf16 -- the A operand of the final MMA).
-            mbar_wait(&bar_q, 0);
-            mbar_wait(&bar_qk_done, 0);
-            __syncwarp();
-            const uint32_t qb = smem_u32(sQ);
-            for (int u = 0; u < 4; ++u) {
-                const int r = lane + 32 * u;
-                float qv[128];
-#pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    uint32_t w[4];
-                    ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-                        qv[ch * 8 + 2 * e] = f2.x;
-                        qv[ch * 8 + 2 * e + 1] = f2.y;
-                    }
-                }
-                float qm = -INFINITY;
-#pragma unroll
-                for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
-                float qs = 0.0f;
-#pragma unroll
-                for (int f = 0; f < 128; ++f) {
-                    qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
-                    qs += qv[f];
-                }
-                const float qinv = 1.0f / qs;
-                float den = 0.0f;
-#pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int f = ch * 8 + 2 * e;
-                        const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
-                        const float2 pr = __bfloat1622float2(pk);
-                        den += pr.x * sZc[f] + pr.y * sZc[f + 1];
-                        w[e] = *reinterpret_cast<const uint32_t*>(&pk);
-                    }
-                    st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
-                }
-                sDen[r] = den;
-            }
-            fence_proxy_async_smem();
-            mbar_arrive(&bar_phiq);
+            if (lane == 0) mbar_arrive(&bar_zc);
         }
     } else if (warp >= 4) {
         // ===================== softmax / correction / epilogue =====================
@@ -562,6 +582,8 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
     }
+    // one call site, so the phi(Q) code exists once (the softmax loop keeps the I-cache)
+    if (warp == 0 || warp == 2 || warp == 3) phiq_share();
     __syncthreads();
     if (warp == 2) tmem_free(tmem, 512);
 }
