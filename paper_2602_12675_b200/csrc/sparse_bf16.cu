@@ -43,7 +43,13 @@ namespace sla2dev {
 
 namespace sp {
 constexpr int BQ = 128, BK = 64, D = 128;
-constexpr int NKP = 2, NSV = 4;
+#ifndef SLA2_NKP
+#define SLA2_NKP 2
+#endif
+#ifndef SLA2_NSV
+#define SLA2_NSV 4
+#endif
+constexpr int NKP = SLA2_NKP, NSV = SLA2_NSV;  // K pair ring (32 KB/stage), V+phi(K) ring (32 KB/stage)
 constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
 constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // K pair: [k_atom 2][128 rows][128 B]
@@ -90,7 +96,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define SLA2_TR(slot) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + (slot)] = gtimer()
+#define SLA2_TR(slot) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 128 + (slot)] = gtimer()
 #else
 #define SLA2_TR(slot)
 #endif
@@ -270,6 +276,7 @@ __global__ void __launch_bounds__(256, 1)
                 const int s = j % NSV;
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
                 const int krow = (int)(bh * p.N + (int64_t)kblock(j) * BK);
+                if (j < 16) SLA2_TR(64 + j);
                 mbar_arrive_expect_tx(&bar_v_full[s], tx);
                 tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol_keep);
                 tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol_keep);
@@ -289,85 +296,110 @@ __global__ void __launch_bounds__(256, 1)
                 tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol_keep);
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer (one thread) =====================
-        if (lane == 0) {
-            constexpr uint32_t ID_QK2 = idesc_bf16(128, 128, false, false);
-            constexpr uint32_t ID_QK1 = idesc_bf16(128, 64, false, false);
-            constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
-            constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
-            const uint32_t aQ = smem_u32(sQ);
-            mbar_wait(&bar_q, 0);
-            tc_fence_after();
-            SLA2_TR(1);
-            // Static issue order. The tensor pipe runs one thread's MMAs in issue order, so the
-            // order is the schedule:
-            //   QK(0), QK(1); for each pair n: [P(n)] PV(n) -> QK(n+2) -> HS(n)
-            // PV(n) enters the pipe as soon as P(n) exists; QK(n+2) (which reuses S buffer n&1,
-            // safe because PV(n) precedes it) runs before the HS filler, so S(n+2) is ready when
-            // the softmax gets to it; HS(n) fills the pipe while the softmax works on n+1.
-            auto issue_qk = [&](int n) {
-                const int s = n % NKP, b = n & 1;
-                mbar_wait(&bar_k_full[s], (n / NKP) & 1);
-                tc_fence_after();
-                const bool two = 2 * n + 1 < nb;
-                const uint32_t bK = smem_u32(sKp(s));
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-                    umma_bf16_ss(tmem + TM_S + b * 128, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(bK + off, 16, 1024),
-                                 two ? ID_QK2 : ID_QK1, ks > 0);
+#ifdef SLA2_TRACE
+        else if (lane == 1) {
+            // trace only: stamp each V/phi(K) stage's actual arrival
+            for (int j = 0; j < nb && j < 16; ++j) {
+                for (int it = 0; it < 1000000 && !mbar_try_wait(&bar_v_full[j % NSV], (j / NSV) & 1); ++it) {
                 }
-                umma_commit(&bar_s_full[b]);
-                umma_commit(&bar_k_empty[s]);
-                if (n == npair - 1) umma_commit(&bar_qk_done);
-            };
-            if (npair > 0) issue_qk(0);
-            if (npair > 1) issue_qk(1);
-            for (int n = 0; n < npair; ++n) {
-                const int j0 = 2 * n, j1 = min(nb, j0 + 2);
-                mbar_wait(&bar_p_full[n & 1], (n >> 1) & 1);
+                SLA2_TR(96 + j);
+            }
+        }
+#endif
+    } else if (warp == 1) {
+        // ===================== MMA issuer (whole warp, elect.sync issues) =====================
+        // All 32 lanes run this with warp-uniform values (counts and TMEM base via shfl), so
+        // the descriptors live in uniform registers and each MMA is a few instructions.
+        constexpr uint32_t ID_QK2 = idesc_bf16(128, 128, false, false);
+        constexpr uint32_t ID_QK1 = idesc_bf16(128, 64, false, false);
+        constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
+        const uint32_t tm = warp_uniform(tmem);
+        const int nbu = (int)warp_uniform((uint32_t)nb);
+        const int npu = (nbu + 1) >> 1;
+        const uint32_t sbase = warp_uniform(smem_u32(smem));
+        // descriptor bases; + (byte offset >> 4) advances the start address
+        const uint64_t dQ = sdesc_sw128(sbase + OFF_Q, 16, 1024);
+        const uint64_t dK0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
+        const uint64_t dVm = sdesc_sw128(sbase + OFF_V, 8192, 1024);  // MN-major V / phi(K) tiles
+        mbar_wait(&bar_q, 0);
+        tc_fence_after();
+        if (lane == 0) SLA2_TR(1);
+        // Static issue order. The tensor pipe runs the MMAs in issue order, so the order is
+        // the schedule:
+        //   QK(0), QK(1); for each pair n: [P(n)] PV(n) -> QK(n+2) -> HS(n)
+        // PV(n) enters the pipe as soon as P(n) exists; QK(n+2) (which reuses S buffer n&1,
+        // safe because PV(n) precedes it) runs before the HS filler, so S(n+2) is ready when
+        // the softmax gets to it; HS(n) fills the pipe while the softmax works on n+1.
+        auto issue_qk = [&](int n) {
+            const int s = n % NKP, b = n & 1;
+            mbar_wait(&bar_k_full[s], (n / NKP) & 1);
+            tc_fence_after();
+            if (lane == 0 && n < 8) SLA2_TR(56 + n);
+            const uint32_t idq = (2 * n + 1 < nbu) ? ID_QK2 : ID_QK1;
+            const uint64_t dK = dK0 + ((s * KP_BYTES) >> 4);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+                umma_bf16_ss_w(tm + TM_S + b * 128, dQ + off, dK + off, idq, ks > 0);
+            }
+            umma_commit_w(&bar_s_full[b]);
+            umma_commit_w(&bar_k_empty[s]);
+            if (n == npu - 1) umma_commit_w(&bar_qk_done);
+        };
+        if (npu > 0) issue_qk(0);
+        if (npu > 1) issue_qk(1);
+        for (int n = 0; n < npu; ++n) {
+            const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
+            mbar_wait(&bar_p_full[n & 1], (n >> 1) & 1);
+            tc_fence_after();
+            for (int j = j0; j < j1; ++j) {
+                const int sv = j % NSV;
+                mbar_wait(&bar_v_full[sv], (j / NSV) & 1);
                 tc_fence_after();
+                if (lane == 0 && j < 16) SLA2_TR(80 + j);
+                const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
+                const uint32_t aP = tm + TM_S + (n & 1) * 128 + (j & 1) * 64;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
+                if (dense) umma_commit_w(&bar_v_empty[sv]);
+            }
+            umma_commit_w(&bar_pv_done[n & 1]);
+            if (lane == 0 && n < 16) SLA2_TR(34 + n);
+#ifndef SLA2_HS_FIRST
+            if (n + 2 < npu) issue_qk(n + 2);
+#endif
+            if (!dense) {
                 for (int j = j0; j < j1; ++j) {
-                    mbar_wait(&bar_v_full[j % NSV], (j / NSV) & 1);
-                    tc_fence_after();
-                    const uint32_t bV = smem_u32(sV(j % NSV));
-                    const uint32_t aP = tmem + TM_S + (n & 1) * 128 + (j & 1) * 64;
+                    const int sv = j % NSV;
+                    const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
+                    const uint64_t dP = dV + (TILE_BYTES >> 4);  // phi(K) tile follows V in the stage
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
-                        umma_bf16_ts(tmem + TM_O, aP + ks * 8, sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_PV,
-                                     (j > 0 || ks > 0));
-                    if (dense) umma_commit(&bar_v_empty[j % NSV]);
-                }
-                umma_commit(&bar_pv_done[n & 1]);
-                if (n < 16) SLA2_TR(34 + n);
-                if (n + 2 < npair) issue_qk(n + 2);
-                if (!dense) {
-                    for (int j = j0; j < j1; ++j) {
-                        const uint32_t aH = smem_u32(sPh(j % NSV)), bV = smem_u32(sV(j % NSV));
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)
-                            umma_bf16_ss(tmem + TM_H, sdesc_sw128(aH + ks * 2048, 8192, 1024),
-                                         sdesc_sw128(bV + ks * 2048, 8192, 1024), ID_HS, (j > 0 || ks > 0));
-                        umma_commit(&bar_v_empty[j % NSV]);  // after PV_j and HS_j
-                    }
+                        umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
+                                       (j > 0 || ks > 0));
+                    umma_commit_w(&bar_v_empty[sv]);  // after PV_j and HS_j
                 }
             }
-            umma_commit(&bar_mma_done);  // every QK / PV / HS of the loop
-            if (linear) {
-                // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
-                mbar_wait(&bar_lin_ready, 0);
-                mbar_wait(&bar_phiq, 0);
-                tc_fence_after();
-                const uint32_t bH = smem_u32(sHc);
+            if (lane == 0 && n < 16) SLA2_TR(112 + n);
+#ifdef SLA2_HS_FIRST
+            if (n + 2 < npu) issue_qk(n + 2);
+#endif
+        }
+        umma_commit_w(&bar_mma_done);  // every QK / PV / HS of the loop
+        if (linear) {
+            // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
+            mbar_wait(&bar_lin_ready, 0);
+            mbar_wait(&bar_phiq, 0);
+            tc_fence_after();
+            const uint64_t dH = sdesc_sw128(warp_uniform(smem_u32(sHc)), 16384, 1024);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-                    umma_bf16_ss(tmem + TM_L, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(bH + ks * 2048, 16384, 1024),
-                                 ID_PV, ks > 0);
-                }
-                umma_commit(&bar_lin_done);
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+                umma_bf16_ss_w(tm + TM_L, dQ + off, dH + ((ks * 2048) >> 4), ID_PV, ks > 0);
             }
+            umma_commit_w(&bar_lin_done);
         }
     } else if (warp == 3) {
         // ===================== Zc, then phi(Q) in place over sQ and phi(Q) . Zc =====================

@@ -29,12 +29,12 @@ def main():
     pq = (eye + 0.05 * torch.randn((H, d, d), generator=g, device=dev)).contiguous()
     pk = (eye + 0.05 * torch.randn((H, d, d), generator=g, device=dev)).contiguous()
     rho = torch.zeros((H, tm), device=dev)
-    tr = torch.zeros(B * H * tm * 64, dtype=torch.int64, device=dev)
+    tr = torch.zeros(B * H * tm * 128, dtype=torch.int64, device=dev)
     L.sla2_trace_set_buffer(tr.data_ptr())
     for _ in range(3):
         sla2.forward(q, k, v, pq, pk, rho, k_percent=3.0)
     torch.cuda.synchronize()
-    t = tr.view(B * H * tm, 64).cpu().numpy().astype(np.int64)
+    t = tr.view(B * H * tm, 128).cpu().numpy().astype(np.int64)
     t0 = t[:, 0]
     rel = (t - t0[:, None]) / 1000.0  # us since CTA start
     kappa = 15
@@ -45,9 +45,14 @@ def main():
     print(f"per-CTA total (start -> output done): median {med(rel[:, 53]):.2f} us")
     print(f"  Q ready at MMA         {med(rel[:, 1]):7.2f}")
     print(f"  producer first/last kv {med(rel[:, 54]):7.2f} / {med(rel[:, 55]):7.2f}")
+    for j in range((kappa + 1) // 2):  # key-block pairs
+        print(f"  pair {j:2d}: K ready {med(rel[:, 56 + j]):7.2f}  S ready {med(rel[:, 2 + j]):7.2f}"
+              f"  P ready {med(rel[:, 18 + j]):7.2f}  PV issued {med(rel[:, 34 + j]):7.2f}")
     for j in range(kappa):
-        print(f"  block {j:2d}: S ready {med(rel[:, 2 + j]):7.2f}  P ready {med(rel[:, 18 + j]):7.2f}"
-              f"  PV issued {med(rel[:, 34 + j]):7.2f}")
+        print(f"  V {j:2d}: load issued {med(rel[:, 64 + j]):7.2f}  ready at MMA {med(rel[:, 80 + j]):7.2f}"
+              f"  (latency {med(rel[:, 80 + j] - rel[:, 64 + j]):5.2f})  arrived {med(rel[:, 96 + j]):7.2f}")
+    for n in range((kappa + 1) // 2):
+        print(f"  pair {n}: HS issued {med(rel[:, 112 + n]):7.2f}")
     print(f"  loop done (pv_done)    {med(rel[:, 50]):7.2f}")
     print(f"  lin_ready              {med(rel[:, 51]):7.2f}")
     print(f"  lin_done               {med(rel[:, 52]):7.2f}")
