@@ -104,26 +104,40 @@ __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__
     if (warp > NCW) return;
     const int col = warp * 32 + lane;
     float acc = 0.0f;
+    // The FADD chain (4 cycles per row) is the floor; every other instruction must hide
+    // under it. Rolling window: the load + convert of row r + W is issued right after the
+    // FADD of row r, so each FADD has two independent instructions beside it. The window
+    // runs across chunk boundaries (the next stage is waited for W rows early).
+    constexpr int W = 8;
+    float x[W];
+    {
+        mbar_wait(&full[0], 0);
+        const T* tile = ring + col;
+#pragma unroll
+        for (int u = 0; u < W; ++u) x[u] = to_f32(tile[u * COLS]);
+    }
     for (int c = 0; c < nchunk; ++c) {
         const int s = c % cm::NST;
-        mbar_wait(&full[s], (c / cm::NST) & 1);
         const T* tile = ring + (size_t)s * cm::ROWS * COLS + col;
-        float a[32], b[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[u * COLS]);
-#pragma unroll 1
-        for (int r0 = 0; r0 < cm::ROWS; r0 += 64) {
+        for (int r = 0; r < cm::ROWS - W; r += W) {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) b[u] = to_f32(tile[(r0 + 32 + u) * COLS]);
-#pragma unroll
-            for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, a[u]);
-            if (r0 + 64 < cm::ROWS) {
-#pragma unroll
-                for (int u = 0; u < 32; ++u) a[u] = to_f32(tile[(r0 + 64 + u) * COLS]);
+            for (int u = 0; u < W; ++u) {
+                acc = __fadd_rn(acc, x[u]);
+                x[u] = to_f32(tile[(r + W + u) * COLS]);
             }
-#pragma unroll
-            for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, b[u]);
         }
+        // last W rows of this chunk; prefetch the first W of the next
+        const bool more = c + 1 < nchunk;
+        const int s1 = (c + 1) % cm::NST;
+        if (more) mbar_wait(&full[s1], ((c + 1) / cm::NST) & 1);
+        const T* nt = ring + (size_t)s1 * cm::ROWS * COLS + col;
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+            acc = __fadd_rn(acc, x[u]);
+            if (more) x[u] = to_f32(nt[u * COLS]);
+        }
+        __syncwarp();
         mbar_arrive(&empty[s]);
     }
     const float inv = __fdiv_rn(1.0f, (float)N);
@@ -215,8 +229,10 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
 // per output, f ascending from 0, separate mul and add), for a tile of 32 pooled rows per CTA.
 // P (d x d) and the xbar tile live in shared memory; each thread owns a 4 x 4 register tile
 // of outputs (16 independent chains). grid (ceil(nrows/32), BH), block 256. Requires d % 16 == 0.
+// With xp_t the output is written transposed, [BH][d][nrows] (the router's key side: lanes
+// of router_rows_kernel then read consecutive keys of one feature, coalesced).
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ xbar, const float* __restrict__ proj,
-                                                      float* __restrict__ xp, int nrows, int d, int H) {
+                                                      float* __restrict__ xp, int nrows, int d, int H, int xp_t) {
     extern __shared__ __align__(16) float psh[];
     float* sP = psh;           // [d][d]
     float* sX = psh + d * d;   // [32][d]
@@ -254,12 +270,26 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
                 acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(xv, pv.w));
             }
         }
+        if (xp_t) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = rg * 4 + a;
-            if (r < nr)
-                *reinterpret_cast<float4*>(xp + (bh * nrows + r0 + r) * (int64_t)d + cg * 4) =
-                    make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+            for (int b = 0; b < 4; ++b) {
+                float* dst = xp + (bh * d + cg * 4 + b) * (int64_t)nrows + r0 + rg * 4;
+                if (rg * 4 + 4 <= nr && (nrows & 3) == 0) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+                        if (rg * 4 + a < nr) dst[a] = acc[a][b];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int r = rg * 4 + a;
+                if (r < nr)
+                    *reinterpret_cast<float4*>(xp + (bh * nrows + r0 + r) * (int64_t)d + cg * 4) =
+                        make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+            }
         }
     }
 }
@@ -490,7 +520,7 @@ __device__ void warp_topk_row(const float* __restrict__ vals, int tn, int kappa,
 constexpr int RROWS = 8;
 template <int TK>  // 0: bitonic top-k; otherwise register top-k with TK keys per lane
 __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
-                                                          float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
+                                                          int kp_t, float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
                                                           float* __restrict__ pc_out, uint8_t* __restrict__ mask_out,
                                                           int32_t* __restrict__ idx_out) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -508,7 +538,42 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
     }
     __syncthreads();
     const float* kpb = kp + bh * (int64_t)tn * d;
-    if ((tn & 3) == 0 && (d & 3) == 0) {
+    if (kp_t) {
+        // same 4 x 4 register tile over the transposed keys [d][tn]: for each feature c the
+        // lanes read 4 consecutive keys each (one coalesced 512-B row per warp); each chain
+        // still accumulates over c ascending with separate mul and add
+        const int rg = tid >> 7;
+        for (int jg = tid & 127; jg * 4 < tn; jg += 128) {
+            float acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+            const float* k0 = kpb + jg * 4;
+            for (int c = 0; c < d; c += 4) {
+                float4 kv[4], qv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) kv[u] = __ldg(reinterpret_cast<const float4*>(k0 + (int64_t)(c + u) * tn));
+#pragma unroll
+                for (int a = 0; a < 4; ++a) qv[a] = *reinterpret_cast<const float4*>(sq + (rg * 4 + a) * d + c);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const float qa[4] = {qv[a].x, qv[a].y, qv[a].z, qv[a].w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(qa[u], kv[u].x));
+                        acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(qa[u], kv[u].y));
+                        acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(qa[u], kv[u].z));
+                        acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(qa[u], kv[u].w));
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
+        }
+    } else if ((tn & 3) == 0 && (d & 3) == 0) {
         // register tile: 4 rows x 4 columns per thread, 16 independent serial chains; each
         // loaded qp / kp value feeds 4 products (shared-memory traffic 1/4 of the naive loop)
         const int rg = tid >> 7;  // rows rg*4 .. rg*4+3
@@ -669,9 +734,12 @@ static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, 
 // Pool then project. With d % 16 == 0 (every shipped config) pooling writes xbar to `scratch`
 // and project_kernel reuses P from shared memory across 32 rows; otherwise the per-block
 // kernel projects in place.
+// Returns true when xp was written transposed ([BH][d][nrows]; only with want_t and the
+// split path).
 template <typename T>
-static void launch_pool_project(const T* x, const float* mu, const float* proj, float* xp, int N, int d, int H,
-                                int block, int BH, float* scratch, cudaStream_t st, int* launches) {
+static bool launch_pool_project(const T* x, const float* mu, const float* proj, float* xp, int N, int d, int H,
+                                int block, int BH, float* scratch, cudaStream_t st, int* launches,
+                                bool want_t = false) {
     const size_t smem = ((d * sizeof(float) + 15) & ~size_t(15)) + (size_t)block * d * sizeof(T);
     if (smem > 48 * 1024) cudaFuncSetAttribute(pool_project_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const bool split = scratch && (d % 16 == 0) && ((size_t)d * d + 32 * d) * 4 <= 200 * 1024;
@@ -682,9 +750,11 @@ static void launch_pool_project(const T* x, const float* mu, const float* proj, 
         const int nrows = N / block;
         const size_t ps = ((size_t)d * d + 32 * d) * 4;
         cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
-        project_kernel<<<dim3((nrows + 31) / 32, BH), 256, ps, st>>>(scratch, proj, xp, nrows, d, H);
+        project_kernel<<<dim3((nrows + 31) / 32, BH), 256, ps, st>>>(scratch, proj, xp, nrows, d, H, want_t ? 1 : 0);
         ++*launches;
+        return want_t;
     }
+    return false;
 }
 
 template <typename T>
@@ -718,17 +788,18 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
     const int tm = a.N / a.bq, tn = a.N / a.bk;
     launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
     if (forked) cudaStreamWaitEvent(st, ev_join, 0);
-    launch_pool_project<T>((const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d, a.H, a.bk, BH,
-                           a.kbar, st, launches);
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
     const size_t rsm = router_rows_smem(tn, a.d);
+    const bool tile_ok = rsm <= 220 * 1024 && (tn & 3) == 0 && (a.d & 3) == 0;
+    const bool kp_t = launch_pool_project<T>((const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d,
+                                             a.H, a.bk, BH, a.kbar, st, launches, tile_ok);
     if (rsm <= 220 * 1024) {
         const dim3 grid((tm + RROWS - 1) / RROWS, BH);
         auto go = [&](auto kern) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-            kern<<<grid, 256, rsm, st>>>(a.qp, a.kp, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2, a.pc_out, a.mask_out,
-                                         a.idx_out);
+            kern<<<grid, 256, rsm, st>>>(a.qp, a.kp, kp_t ? 1 : 0, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2,
+                                         a.pc_out, a.mask_out, a.idx_out);
         };
         if (a.kappa <= 64 && tn <= 32 * 16) go(router_rows_kernel<16>);
         else if (a.kappa <= 64 && tn <= 32 * 64) go(router_rows_kernel<64>);
