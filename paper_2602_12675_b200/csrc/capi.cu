@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -26,6 +27,8 @@ thread_local int g_launches = 0;
 thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 thread_local bool g_ev_recorded = false;
+// set by sla2_forward around its sla2_router call: the router records it once mu is ready
+thread_local cudaEvent_t g_mu_ready = nullptr;
 void mark(int i, cudaStream_t st) {
     if (!g_timing) return;
     if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
@@ -323,10 +326,24 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
     return carve(geometry(p), nullptr, nullptr);
 }
 
+// How the linear-branch precompute is scheduled (sla2_forward):
+//   dep     fork it onto a second stream off this event (it needs only mu), concurrently with
+//           whatever st is still doing; st joins it before the sparse kernel
+//   kprep   first run launch_kprep on st (phi(K~), z_j and the router's pooled keys in one
+//           pass over K), then fork the rest (Htot partials + reduction) off it
+//   between run on st right after the fork (the router's back half)
+struct LinPlan {
+    cudaEvent_t dep = nullptr;
+    bool kprep = false;
+    float* kbar = nullptr;
+    std::function<sla2_status()> between;
+};
+
+// Linear-branch precompute then the sparse kernel.
 static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g, const Workspace& w, const void* q,
                                          const void* k, const void* v, const float* rho, const int32_t* idx,
                                          const int32_t* cnt, int kstride, void* out, const sla2_fwd_saved* saved,
-                                         cudaStream_t st) {
+                                         cudaStream_t st, const LinPlan& plan = LinPlan{}) {
     const float isd = inv_sqrt(g.d);
     CUtensorMap mq, mk, mv, mphi, mht;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
@@ -354,7 +371,37 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.nchunk = g.nchunk;
     la.tm_phik = &mphi;
     la.tm_v = &mv;
-    SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+    cudaEvent_t dep = plan.dep;
+    if (plan.kprep) {
+        thread_local cudaEvent_t ev_k = nullptr;
+        if (!ev_k) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming));
+        SLA2_CUDA_TRY(launch_kprep(la, plan.kbar, st, &g_launches));
+        la.phik_ready = true;
+        SLA2_CUDA_TRY(cudaEventRecord(ev_k, st));
+        dep = ev_k;
+    }
+    if (dep) {
+        thread_local cudaStream_t lin = nullptr;
+        thread_local cudaEvent_t lin_done = nullptr;
+        if (!lin) {
+            SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&lin, cudaStreamNonBlocking));
+            SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
+        }
+        SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
+        SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
+        SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
+        if (plan.between) {
+            const sla2_status bs = plan.between();
+            if (bs != SLA2_OK) {
+                cudaStreamWaitEvent(st, lin_done, 0);
+                return bs;
+            }
+        }
+        mark(1, st);  // router done (the linear precompute overlapped it)
+        SLA2_CUDA_TRY(cudaStreamWaitEvent(st, lin_done, 0));
+    } else {
+        SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+    }
     mark(2, st);
 
     SparseLaunch sa{};
@@ -437,6 +484,38 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     return SLA2_OK;
 }
 
+// Router launch description shared by sla2_router and sla2_forward.
+static void fill_router(const sla2_fwd_params* p, const Geo& g, const Workspace& w, const void* q, const void* k,
+                        const float* proj_q, const float* proj_k, float* pc_out, uint8_t* mask_out, int32_t* idx,
+                        CUtensorMap* mcol, RouterLaunch* ra) {
+    *ra = RouterLaunch{};
+    ra->q = q;
+    ra->k = k;
+    ra->bf16 = g.bf16;
+    ra->B = g.B;
+    ra->H = g.H;
+    ra->N = (int)g.N;
+    ra->d = (int)g.d;
+    ra->bq = (int)g.bq;
+    ra->bk = (int)g.bk;
+    ra->kappa = (int)g.kappa;
+    ra->smooth = p->smooth;
+    ra->exact_mu = p->exact_mu;
+    ra->inv_sqrt_d = inv_sqrt(g.d);
+    ra->proj_q = proj_q;
+    ra->proj_k = proj_k;
+    ra->tm_kcol = colmean_map(mcol, k, g.bf16, g.BH, g.N, g.d);
+    ra->mu_out = w.mu;
+    ra->mu_part = w.mu_part;
+    ra->qp = w.qp;
+    ra->kp = w.kp;
+    ra->qbar = w.qbar;
+    ra->kbar = w.kbar;
+    ra->pc_out = pc_out;
+    ra->mask_out = mask_out;
+    ra->idx_out = idx ? idx : w.idx;
+}
+
 sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, const float* proj_q,
                         const float* proj_k, float* pc_out, uint8_t* mask_out, int32_t* kv_idx_out, void* workspace,
                         size_t workspace_bytes, void* stream) {
@@ -450,33 +529,10 @@ sla2_status sla2_router(const sla2_fwd_params* p, const void* q, const void* k, 
     if (!q || !k || !proj_q || !proj_k) return fail(SLA2_CONTRACT_ERROR, "NULL input pointer");
     Workspace w;
     carve(g, workspace, &w);
-    RouterLaunch ra{};
-    ra.q = q;
-    ra.k = k;
-    ra.bf16 = g.bf16;
-    ra.B = g.B;
-    ra.H = g.H;
-    ra.N = (int)g.N;
-    ra.d = (int)g.d;
-    ra.bq = (int)g.bq;
-    ra.bk = (int)g.bk;
-    ra.kappa = (int)g.kappa;
-    ra.smooth = p->smooth;
-    ra.exact_mu = p->exact_mu;
-    ra.inv_sqrt_d = inv_sqrt(g.d);
-    ra.proj_q = proj_q;
-    ra.proj_k = proj_k;
+    RouterLaunch ra;
     CUtensorMap mcol;
-    ra.tm_kcol = colmean_map(&mcol, k, g.bf16, g.BH, g.N, g.d);
-    ra.mu_out = w.mu;
-    ra.mu_part = w.mu_part;
-    ra.qp = w.qp;
-    ra.kp = w.kp;
-    ra.qbar = w.qbar;
-    ra.kbar = w.kbar;
-    ra.pc_out = pc_out;
-    ra.mask_out = mask_out;
-    ra.idx_out = kv_idx_out ? kv_idx_out : w.idx;
+    fill_router(p, g, w, q, k, proj_q, proj_k, pc_out, mask_out, kv_idx_out, &mcol, &ra);
+    ra.mu_ready = g_mu_ready;
     SLA2_CUDA_TRY(launch_router(ra, (cudaStream_t)stream, &g_launches));
     return SLA2_OK;
 }
@@ -498,11 +554,42 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
     int32_t* idx = kv_idx_out ? kv_idx_out : w.idx;
     cudaStream_t st = (cudaStream_t)stream;
     mark(0, st);
+    // the linear precompute needs only mu: the router records mu_ready and the precompute
+    // forks off it, overlapping the router's key side (pooling, projection, scores, top-k)
+    thread_local cudaEvent_t ev_mu = nullptr;
+    if (!ev_mu && cudaEventCreateWithFlags(&ev_mu, cudaEventDisableTiming) != cudaSuccess)
+        return fail(SLA2_CUDA_ERROR, "cudaEventCreate failed");
+    if (g.d == 128 && 4 * g.bk * 128 * (g.bf16 ? 2 : 4) <= 200 * 1024) {
+        // router front (mu, query side) -> kprep (phi(K~), z_j, pooled keys: one pass over K)
+        // -> fork Htot partials + reduction || router back (key projection, scores, top-k)
+        RouterLaunch ra;
+        CUtensorMap mcol;
+        fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);
+        ra.kbar_ready = true;
+        SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
+        LinPlan plan;
+        plan.kprep = true;
+        plan.kbar = w.kbar;
+        plan.between = [&]() -> sla2_status {
+            SLA2_CUDA_TRY(launch_router_back(ra, st, &g_launches));
+            return SLA2_OK;
+        };
+        s = run_linear_and_sparse(p, g, w, q, k, v, rho, idx, nullptr, (int)g.kappa, out, saved, st, plan);
+        mark(3, st);
+        return s;
+    }
+    if (p->smooth) {
+        g_mu_ready = ev_mu;
+    } else if (cudaEventRecord(ev_mu, st) != cudaSuccess) {  // phi(K) on raw K: fork at once
+        return fail(SLA2_CUDA_ERROR, "cudaEventRecord failed");
+    }
     s = sla2_router(p, q, k, proj_q, proj_k, nullptr, mask_out, idx, workspace, workspace_bytes, stream);
+    g_mu_ready = nullptr;
     const int router_launches = g_launches;
     if (s != SLA2_OK) return s;
-    mark(1, st);
-    s = run_linear_and_sparse(p, g, w, q, k, v, rho, idx, nullptr, (int)g.kappa, out, saved, st);
+    LinPlan plan;
+    plan.dep = ev_mu;
+    s = run_linear_and_sparse(p, g, w, q, k, v, rho, idx, nullptr, (int)g.kappa, out, saved, st, plan);
     mark(3, st);
     g_launches += router_launches;
     return s;

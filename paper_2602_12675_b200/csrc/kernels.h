@@ -28,8 +28,15 @@ struct RouterLaunch {
     float* pc_out;    // optional [BH][tm][tn]
     uint8_t* mask_out;
     int32_t* idx_out;  // [BH][tm][kappa]
+    cudaEvent_t mu_ready;  // optional: recorded once mu_out is complete (lets the caller fork
+                           // the linear-branch precompute off it)
+    bool kbar_ready;       // kbar already holds the pooled keys (launch_kprep): back half only projects
 };
 cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches);
+// The two halves of launch_router: front = mu (side stream, joined into st) + query-side
+// pooling/projection; back = key-side pooling (unless kbar_ready)/projection + scores/top-k.
+cudaError_t launch_router_front(const RouterLaunch& a, cudaStream_t st, int* launches);
+cudaError_t launch_router_back(const RouterLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
                            cudaStream_t st, int* launches);
 cudaError_t launch_topk_only(const float* pc, int BH, int tm, int tn, int kappa, uint8_t* mask, int32_t* idx,
@@ -54,8 +61,12 @@ struct LinearLaunch {
     int nchunk;       // key-block chunks per head for the H partials
     const CUtensorMap* tm_phik;  // bf16 path: TMA maps (box 64x64, SW128) over [BH*N][d]
     const CUtensorMap* tm_v;
+    bool phik_ready;  // phi(K~) and z_j already written by launch_kprep
 };
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches);
+// Fused key-side prep (d = 128): phi(K~) + z_j (as phik_kernel) and the router's pooled keys
+// kbar [BH][tn][d] (as pool_project_kernel's pooling), reading K once.
+cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches);
 
 // ---- sparse / dense attention (sparse_bf16.cu, sparse_f32.cu)
 struct SparseLaunch {

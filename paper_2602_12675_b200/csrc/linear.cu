@@ -275,12 +275,176 @@ __global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* 
     }
 }
 
+// Fused key-side prep for d = 128 (one key block per warp, its bk rows in order):
+//   kbar[j][c] = float( (sum_r (double)(K[r][c] - mu[c])) / (double)bk )
+//       exactly pool_project_kernel's pooled row (matrix.hpp:180-192: r ascending, fp64 sum,
+//       fp32 subtraction first) -- the router's key side then only projects it;
+//   phi(K~) rows (row softmax over d, attention.hpp:456) -> bf16 / fp32 store, and
+//   z_j = column sum of the stored (rounded) rows.
+// K is read once for both (phik_kernel + pool_project_kernel read it twice). The exponential
+// is ex2.approx: phi(K~) feeds only the linear branch (tolerance 1e-2) and is rounded to bf16;
+// each warp stages its key block in shared memory with one bulk copy (the loop is then free of
+// DRAM latency), and the row max is one redux.sync.max.f32;
+// Htot and the selected-block sums use the same stored values, so "total minus selected" stays
+// consistent. Lane l owns features 4l .. 4l+3. grid (ceil(tn/4), BH), block 128.
+template <typename T>
+struct kp_vec;
+template <>
+struct kp_vec<__nv_bfloat16> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&x)[4]) {
+        const uint2 w = *reinterpret_cast<const uint2*>(p);
+        x[0] = __uint_as_float(w.x << 16);
+        x[1] = __uint_as_float(w.x & 0xffff0000u);
+        x[2] = __uint_as_float(w.y << 16);
+        x[3] = __uint_as_float(w.y & 0xffff0000u);
+    }
+    static __device__ __forceinline__ void store(__nv_bfloat16* p, float (&x)[4]) {
+        const __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]), b = __floats2bfloat162_rn(x[2], x[3]);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&a);
+        w.y = *reinterpret_cast<const uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(p) = w;
+        const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+        x[0] = fa.x;
+        x[1] = fa.y;
+        x[2] = fb.x;
+        x[3] = fb.y;
+    }
+};
+template <>
+struct kp_vec<float> {
+    static __device__ __forceinline__ void load(const float* p, float (&x)[4]) {
+        const float4 w = *reinterpret_cast<const float4*>(p);
+        x[0] = w.x;
+        x[1] = w.y;
+        x[2] = w.z;
+        x[3] = w.w;
+    }
+    static __device__ __forceinline__ void store(float* p, float (&x)[4]) {
+        *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    }
+};
+
+__device__ __forceinline__ float warp_max_f32(float x) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, const float* __restrict__ mu,
+                                                    T* __restrict__ phik, float* __restrict__ zblk,
+                                                    float* __restrict__ kbar, int N, int bk, int tn) {
+    constexpr int D = 128;
+    extern __shared__ __align__(128) uint8_t kps[];
+    __shared__ uint64_t bar[4];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * 4 + warp;
+    const int64_t bh = blockIdx.y;
+    const uint32_t blk_bytes = (uint32_t)bk * D * sizeof(T);
+    T* tile = reinterpret_cast<T*>(kps + (size_t)warp * blk_bytes);
+    const int64_t row0 = bh * N + (int64_t)j * bk;
+    // the warp's whole key block (bk rows, contiguous in global) in one bulk copy
+    if (lane == 0) {
+        mbar_init(&bar[warp], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    if (j >= tn) return;
+    if (lane == 0) {
+        mbar_arrive_expect_tx(&bar[warp], blk_bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(tile)),
+            "l"(k + row0 * D), "r"(blk_bytes), "r"(smem_u32(&bar[warp]))
+            : "memory");
+    }
+    float m[4] = {0.f, 0.f, 0.f, 0.f};
+    if (mu) {
+        const float4 t = *reinterpret_cast<const float4*>(mu + bh * D + lane * 4);
+        m[0] = t.x;
+        m[1] = t.y;
+        m[2] = t.z;
+        m[3] = t.w;
+    }
+    double pool[4] = {0.0, 0.0, 0.0, 0.0};
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    T* pr = phik + row0 * D + lane * 4;
+    mbar_wait(&bar[warp], 0);
+    const T* tr = tile + lane * 4;
+    constexpr int U = 4;  // rows interleaved (independent reductions)
+    for (int r0 = 0; r0 < bk; r0 += U) {
+        float xs[U][4], mx[U], sum[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            kp_vec<T>::load(tr + (r0 + u) * D, xs[u]);
+            mx[u] = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (mu) xs[u][e] = __fsub_rn(xs[u][e], m[e]);
+                pool[e] = __dadd_rn(pool[e], (double)xs[u][e]);  // rows in order (exact pooling)
+                mx[u] = fmaxf(mx[u], xs[u][e]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            mx[u] = warp_max_f32(mx[u]);
+            sum[u] = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float y;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"((xs[u][e] - mx[u]) * 1.4426950408889634f));
+                xs[u][e] = y;
+                sum[u] += y;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < U; ++u) sum[u] += __shfl_xor_sync(0xffffffffu, sum[u], o);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float inv = __fdividef(1.0f, sum[u]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) xs[u][e] *= inv;
+            kp_vec<T>::store(pr + (int64_t)(r0 + u) * D, xs[u]);  // rounds xs to the stored values
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z[e] += xs[u][e];
+        }
+    }
+    float* kb = kbar + (bh * tn + j) * D + lane * 4;
+    float* zb = zblk + (bh * tn + j) * D + lane * 4;
+    float kv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) kv[e] = __double2float_rn(__ddiv_rn(pool[e], (double)bk));
+    *reinterpret_cast<float4*>(kb) = make_float4(kv[0], kv[1], kv[2], kv[3]);
+    *reinterpret_cast<float4*>(zb) = make_float4(z[0], z[1], z[2], z[3]);
+}
+
+cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches) {
+    const int tn = a.N / a.bk;
+    const dim3 g((tn + 3) / 4, (unsigned)a.BH);
+    const size_t smem = (size_t)4 * a.bk * 128 * (a.bf16 ? 2 : 4);
+    if (a.bf16) {
+        cudaFuncSetAttribute(kprep_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kprep_kernel<__nv_bfloat16><<<g, 128, smem, st>>>((const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik,
+                                                          a.zblk, kbar, a.N, a.bk, tn);
+    } else {
+        cudaFuncSetAttribute(kprep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kprep_kernel<float><<<g, 128, smem, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, kbar, a.N,
+                                                  a.bk, tn);
+    }
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches) {
     const int tn = a.N / a.bk;
     dim3 g1(tn, (unsigned)a.BH);
     if (a.bf16) {
-        phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(
-            (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.N, a.d, a.bk);
+        if (!a.phik_ready)
+            phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(
+                (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.N, a.d, a.bk);
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(htot_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ht::SMEM);
@@ -290,8 +454,9 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
         htot_umma_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 128, ht::SMEM, st>>>(*a.tm_phik, *a.tm_v, a.hpart, a.N,
                                                                                  per, a.nchunk);
     } else {
-        phik_kernel<float, float><<<g1, 128, 0, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, a.N, a.d,
-                                                      a.bk);
+        if (!a.phik_ready)
+            phik_kernel<float, float><<<g1, 128, 0, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, a.N,
+                                                          a.d, a.bk);
         const int rows = (a.N + a.nchunk - 1) / a.nchunk;
         const size_t smem = 2 * 32 * a.d * sizeof(float);
         htot_simt_kernel<float><<<dim3(a.nchunk, (unsigned)a.BH), 256, smem, st>>>(
@@ -300,7 +465,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
     const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
     lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
         a.hpart, a.zblk, a.htot, a.bf16 ? (__nv_bfloat16*)a.htot16 : nullptr, a.ztot, a.nchunk, a.d, tn);
-    *launches += 3;
+    *launches += a.phik_ready ? 2 : 3;
     return cudaGetLastError();
 }
 

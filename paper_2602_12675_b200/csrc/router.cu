@@ -758,14 +758,18 @@ static bool launch_pool_project(const T* x, const float* mu, const float* proj, 
 }
 
 template <typename T>
-static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
+static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
     const int BH = (int)(a.B * a.H);
     // The exact column mean is a serial chain on a few SMs: run it on a side stream,
     // concurrently with the query-side pooling/projection, and join before the key side.
     thread_local cudaStream_t side = nullptr;
     thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (!side) {
-        cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+        // highest priority: the block scheduler must place the colmean CTAs (the critical
+        // path) ahead of the query-side pooling grid launched right after them
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
     }
@@ -776,6 +780,7 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
             cudaStreamWaitEvent(side, ev_fork, 0);
             colmean_t<T>(a.k, a.tm_kcol, a.mu_out, BH, a.N, a.d, side, launches);
             cudaEventRecord(ev_join, side);
+            if (a.mu_ready) cudaEventRecord(a.mu_ready, side);
             forked = true;
         } else {
             const int rows_per = 256;
@@ -783,17 +788,35 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
             colmean_partial_kernel<T><<<dim3(nch, BH), a.d, 0, st>>>((const T*)a.k, a.mu_part, a.N, a.d, rows_per);
             colmean_finish_kernel<<<BH, a.d, 0, st>>>(a.mu_part, a.mu_out, nch, a.N, a.d);
             *launches += 2;
+            if (a.mu_ready) cudaEventRecord(a.mu_ready, st);
         }
     }
-    const int tm = a.N / a.bq, tn = a.N / a.bk;
     launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
     if (forked) cudaStreamWaitEvent(st, ev_join, 0);
+    return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t router_back_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
+    const int BH = (int)(a.B * a.H);
+    const int tm = a.N / a.bq, tn = a.N / a.bk;
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
     const size_t rsm = router_rows_smem(tn, a.d);
     const bool tile_ok = rsm <= 220 * 1024 && (tn & 3) == 0 && (a.d & 3) == 0;
-    const bool kp_t = launch_pool_project<T>((const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d,
-                                             a.H, a.bk, BH, a.kbar, st, launches, tile_ok);
+    bool kp_t;
+    if (a.kbar_ready) {
+        // pooled keys already in kbar (launch_kprep, d = 128): project only
+        const size_t ps = ((size_t)a.d * a.d + 32 * a.d) * 4;
+        cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+        project_kernel<<<dim3((tn + 31) / 32, BH), 256, ps, st>>>(a.kbar, a.proj_k, a.kp, tn, a.d, a.H,
+                                                                  tile_ok ? 1 : 0);
+        ++*launches;
+        kp_t = tile_ok;
+    } else {
+        kp_t = launch_pool_project<T>((const T*)a.k, a.smooth ? a.mu_out : nullptr, a.proj_k, a.kp, a.N, a.d, a.H,
+                                      a.bk, BH, a.kbar, st, launches, tile_ok);
+    }
     if (rsm <= 220 * 1024) {
         const dim3 grid((tm + RROWS - 1) / RROWS, BH);
         auto go = [&](auto kern) {
@@ -814,8 +837,15 @@ static cudaError_t launch_router_t(const RouterLaunch& a, cudaStream_t st, int* 
     return cudaGetLastError();
 }
 
+cudaError_t launch_router_front(const RouterLaunch& a, cudaStream_t st, int* launches) {
+    return a.bf16 ? router_front_t<__nv_bfloat16>(a, st, launches) : router_front_t<float>(a, st, launches);
+}
+cudaError_t launch_router_back(const RouterLaunch& a, cudaStream_t st, int* launches) {
+    return a.bf16 ? router_back_t<__nv_bfloat16>(a, st, launches) : router_back_t<float>(a, st, launches);
+}
 cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches) {
-    return a.bf16 ? launch_router_t<__nv_bfloat16>(a, st, launches) : launch_router_t<float>(a, st, launches);
+    const cudaError_t e = launch_router_front(a, st, launches);
+    return e != cudaSuccess ? e : launch_router_back(a, st, launches);
 }
 
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
