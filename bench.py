@@ -236,9 +236,11 @@ def main():
     for _ in range(min(args.steps, 20)):
         flush.zero_()
         step()
-        stages.append(sla2.last_stage_ms())
+        stages.append(sla2.last_stage_ms(timeline=True))
     sla2.enable_stage_timing(False)
-    st_med = [statistics.median(s[i] for s in stages) for i in range(4)]
+    st_med = [statistics.median(s[i] for s in stages) for i in range(len(stages[0]))]
+    timeline = dict(zip(("mu_ready", "query_side_done", "key_prep_done", "router_back_done", "linear_prep_done"),
+                        st_med[4:9]))
 
     # clock pre-roll (~1 s of back-to-back steps), then the timed region
     t_end = time.time() + 1.0
@@ -372,6 +374,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "stages_ms": {"router": st_med[0], "linear_prep": st_med[1], "sparse_kernel": sparse_ms,
                           "total": st_med[3]},
+            "timeline_ms": timeline,
             "wall_s_timed_region": wall, "output_finite": finite, **extra}
     print(json.dumps(line), flush=True)
     if world > 1:

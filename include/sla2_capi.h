@@ -155,8 +155,11 @@ int32_t sla2_last_launch_count(void);
 /* Stage timing (off by default). When enabled, sla2_forward records CUDA events on its
  * stream around its stages; sla2_last_stage_ms waits for the last call's events and writes
  * up to n durations in ms: [0] router (smooth_k + block_scores + hard_topk), [1] linear
- * precompute (phi(K~), z, Htot), [2] sparse+linear+blend kernel, [3] whole call. Returns the
- * number written. */
+ * precompute (phi(K~), z, Htot), [2] sparse+linear+blend kernel, [3] whole call; then the
+ * timeline in ms since the call started (-1 when the path did not pass the point): [4] mu
+ * ready, [5] query side done, [6] key prep done, [7] router back half done, [8] linear
+ * precompute done. The router and the linear precompute overlap on two streams, so [1] is
+ * only the wait for the latter. Returns the number written (<= 9). */
 void sla2_enable_stage_timing(int32_t enable);
 int32_t sla2_last_stage_ms(float* out, int32_t n);
 

@@ -127,10 +127,12 @@ def enable_stage_timing(on: bool = True):
     lib().sla2_enable_stage_timing(1 if on else 0)
 
 
-def last_stage_ms():
-    """(router, linear precompute, sparse kernel, total) ms of the last forward (CUDA events)."""
-    buf = (C.c_float * 4)()
-    n = lib().sla2_last_stage_ms(buf, 4)
+def last_stage_ms(timeline=False):
+    """(router, linear precompute, sparse kernel, total) ms of the last forward (CUDA events);
+    with timeline=True also (mu ready, query side done, key prep done, router back done,
+    linear precompute done), ms since the call started (-1: not on this path)."""
+    buf = (C.c_float * 9)()
+    n = lib().sla2_last_stage_ms(buf, 9 if timeline else 4)
     return tuple(float(buf[i]) for i in range(n))
 
 

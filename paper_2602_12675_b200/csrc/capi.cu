@@ -23,16 +23,22 @@ namespace {
 thread_local std::string g_last_error;
 thread_local int g_launches = 0;
 
-// optional stage timing: events [0] start, [1] after router, [2] after linear prep, [3] end
+// optional stage timing: events [0] start, [1] after router, [2] after linear prep, [3] end,
+// and timeline points on whichever stream reaches them: [4] mu ready, [5] query side done,
+// [6] key prep done, [7] router back half done, [8] linear precompute done
+constexpr int NEV = 9;
 thread_local bool g_timing = false;
-thread_local cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local cudaEvent_t g_ev[NEV] = {};
 thread_local bool g_ev_recorded = false;
+thread_local unsigned g_ev_mask = 0;
 // set by sla2_forward around its sla2_router call: the router records it once mu is ready
 thread_local cudaEvent_t g_mu_ready = nullptr;
 void mark(int i, cudaStream_t st) {
     if (!g_timing) return;
     if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
     cudaEventRecord(g_ev[i], st);
+    if (i == 0) g_ev_mask = 0;
+    g_ev_mask |= 1u << i;
     if (i == 3) g_ev_recorded = true;
 }
 
@@ -238,6 +244,10 @@ float inv_sqrt(int64_t d) {
 
 }  // namespace
 
+namespace sla2dev {
+void timeline_mark(int slot, cudaStream_t st) { mark(slot, st); }
+}  // namespace sla2dev
+
 // =============================================================================================
 extern "C" {
 
@@ -250,12 +260,19 @@ void sla2_enable_stage_timing(int32_t enable) { g_timing = enable != 0; }
 int32_t sla2_last_stage_ms(float* out, int32_t n) {
     if (!g_ev_recorded || !out || n <= 0) return 0;
     cudaEventSynchronize(g_ev[3]);
-    float ms[4] = {0, 0, 0, 0};
+    float ms[4 + NEV - 4] = {};
     cudaEventElapsedTime(&ms[0], g_ev[0], g_ev[1]);
     cudaEventElapsedTime(&ms[1], g_ev[1], g_ev[2]);
     cudaEventElapsedTime(&ms[2], g_ev[2], g_ev[3]);
     cudaEventElapsedTime(&ms[3], g_ev[0], g_ev[3]);
-    const int m = n < 4 ? n : 4;
+    for (int i = 4; i < NEV; ++i) {
+        ms[i] = -1.0f;
+        if (g_ev_mask & (1u << i)) {
+            cudaEventSynchronize(g_ev[i]);
+            cudaEventElapsedTime(&ms[i], g_ev[0], g_ev[i]);
+        }
+    }
+    const int m = n < NEV ? n : NEV;
     for (int i = 0; i < m; ++i) out[i] = ms[i];
     return m;
 }
@@ -376,6 +393,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         thread_local cudaEvent_t ev_k = nullptr;
         if (!ev_k) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming));
         SLA2_CUDA_TRY(launch_kprep(la, plan.kbar, st, &g_launches));
+        mark(6, st);
         la.phik_ready = true;
         SLA2_CUDA_TRY(cudaEventRecord(ev_k, st));
         dep = ev_k;
@@ -389,6 +407,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         }
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
         SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
+        mark(8, lin);
         SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
         if (plan.between) {
             const sla2_status bs = plan.between();
@@ -396,6 +415,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
                 cudaStreamWaitEvent(st, lin_done, 0);
                 return bs;
             }
+            mark(7, st);
         }
         mark(1, st);  // router done (the linear precompute overlapped it)
         SLA2_CUDA_TRY(cudaStreamWaitEvent(st, lin_done, 0));

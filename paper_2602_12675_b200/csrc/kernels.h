@@ -32,6 +32,8 @@ struct RouterLaunch {
                            // the linear-branch precompute off it)
     bool kbar_ready;       // kbar already holds the pooled keys (launch_kprep): back half only projects
 };
+// stage-timing hook (capi.cu): records timeline event `slot` on st when timing is enabled
+void timeline_mark(int slot, cudaStream_t st);
 cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches);
 // The two halves of launch_router: front = mu (side stream, joined into st) + query-side
 // pooling/projection; back = key-side pooling (unless kbar_ready)/projection + scores/top-k.

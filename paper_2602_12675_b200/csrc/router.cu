@@ -32,6 +32,15 @@ __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) {
     return __bfloat162float(x);
 }
 
+// acc + float(x), rounded once: for bf16 the sm_100 mixed-precision add (FHADD.BF16) -- the
+// bf16 -> f32 widening is exact, so the result equals __fadd_rn(acc, float(x)) bit for bit,
+// without a separate convert between the shared-memory load and the add chain.
+__device__ __forceinline__ float add_widen(float acc, float x) { return __fadd_rn(acc, x); }
+__device__ __forceinline__ float add_widen(float acc, __nv_bfloat16 x) {
+    asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"(*reinterpret_cast<const unsigned short*>(&x)));
+    return acc;
+}
+
 // ---------------------------------------------------------------------------------------------
 // K0: mu[bh][c] = colmean(K[bh]) with the reference's serial row order (matrix.hpp:235-244):
 // out[c] += x(i, c) for i ascending, then out[c] *= float(1) / float(rows). One lane per column:
@@ -68,6 +77,11 @@ __global__ void __launch_bounds__(32) colmean_exact_kernel(const T* __restrict__
 namespace cm {
 constexpr int ROWS = 128, NST = 8;
 }
+#ifdef SLA2_TRACE
+// trace build only: per-chunk %globaltimer stamps of CTA (0, 0)'s first consumer thread
+__device__ unsigned long long* g_cm_trace = nullptr;
+extern "C" void sla2_cm_trace_set(unsigned long long* p) { cudaMemcpyToSymbol(g_cm_trace, &p, sizeof(p)); }
+#endif
 template <typename T>
 __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__ CUtensorMap tmK, float* __restrict__ mu,
                                                          int N, int d) {
@@ -108,13 +122,13 @@ __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__
     // under it. Rolling window: the load + convert of row r + W is issued right after the
     // FADD of row r, so each FADD has two independent instructions beside it. The window
     // runs across chunk boundaries (the next stage is waited for W rows early).
-    constexpr int W = 8;
-    float x[W];
+    constexpr int W = 16;
+    T x[W];  // raw elements: the add widens them (add_widen)
     {
         mbar_wait(&full[0], 0);
         const T* tile = ring + col;
 #pragma unroll
-        for (int u = 0; u < W; ++u) x[u] = to_f32(tile[u * COLS]);
+        for (int u = 0; u < W; ++u) x[u] = tile[u * COLS];
     }
     for (int c = 0; c < nchunk; ++c) {
         const int s = c % cm::NST;
@@ -123,19 +137,26 @@ __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__
         for (int r = 0; r < cm::ROWS - W; r += W) {
 #pragma unroll
             for (int u = 0; u < W; ++u) {
-                acc = __fadd_rn(acc, x[u]);
-                x[u] = to_f32(tile[(r + W + u) * COLS]);
+                acc = add_widen(acc, x[u]);
+                x[u] = tile[(r + W + u) * COLS];
             }
         }
         // last W rows of this chunk; prefetch the first W of the next
         const bool more = c + 1 < nchunk;
         const int s1 = (c + 1) % cm::NST;
         if (more) mbar_wait(&full[s1], ((c + 1) / cm::NST) & 1);
+#ifdef SLA2_TRACE
+        if (g_cm_trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && c < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            g_cm_trace[c] = t;
+        }
+#endif
         const T* nt = ring + (size_t)s1 * cm::ROWS * COLS + col;
 #pragma unroll
         for (int u = 0; u < W; ++u) {
-            acc = __fadd_rn(acc, x[u]);
-            if (more) x[u] = to_f32(nt[u * COLS]);
+            acc = add_widen(acc, x[u]);
+            if (more) x[u] = nt[u * COLS];
         }
         __syncwarp();
         mbar_arrive(&empty[s]);
@@ -780,6 +801,7 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
             cudaStreamWaitEvent(side, ev_fork, 0);
             colmean_t<T>(a.k, a.tm_kcol, a.mu_out, BH, a.N, a.d, side, launches);
             cudaEventRecord(ev_join, side);
+            timeline_mark(4, side);
             if (a.mu_ready) cudaEventRecord(a.mu_ready, side);
             forked = true;
         } else {
@@ -792,6 +814,7 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
         }
     }
     launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
+    timeline_mark(5, st);
     if (forked) cudaStreamWaitEvent(st, ev_join, 0);
     return cudaGetLastError();
 }
