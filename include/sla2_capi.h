@@ -141,6 +141,9 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
  * Host-buffer forward: the reference's call shape (inputs and outputs in host memory).
  * Copies q/k/v/proj/rho host->device, runs sla2_forward on an internal stream with an
  * internally cached workspace, copies out (and the optional mask) back, synchronizes.
+ * Pipelined per (b, h): the H2D of head c+1 and the D2H of head c-1 overlap the compute of
+ * head c on three streams (pinned host buffers make the copies asynchronous). Results are
+ * identical to one sla2_forward over all heads.
  */
 sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
                               const float* proj_q, const float* proj_k, const float* rho, void* out,

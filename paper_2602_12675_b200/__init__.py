@@ -262,6 +262,25 @@ def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant
     return res[0] if len(res) == 1 else tuple(res)
 
 
+def forward_host(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant=False, smooth=True,
+                 exact_mu=True, return_mask=False):
+    """The reference's call shape: host (CPU) tensors in, host tensors out, through
+    sla2_forward_host (copies pipelined per head against the compute). Pin the inputs
+    (tensor.pin_memory()) for asynchronous copies."""
+    import torch
+    _check_like(q, k, v)
+    if q.device.type != "cpu":
+        raise ContractError("forward_host takes host tensors")
+    p = _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu)
+    cp = p.c()
+    out = torch.empty_like(q, pin_memory=q.is_pinned())
+    mask = torch.empty((p.B, p.H, p.tm, p.tn), dtype=torch.uint8, pin_memory=q.is_pinned()) if return_mask else None
+    rc = lib().sla2_forward_host(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(proj_q.contiguous()),
+                                 _ptr(proj_k.contiguous()), _ptr(rho.contiguous()), _ptr(out), _ptr(mask))
+    _raise(rc)
+    return (out, mask) if return_mask else out
+
+
 def router(q, k, proj_q, proj_k, *, k_percent=3.0, bq=128, bk=64, smooth=True, exact_mu=True, tau=0.1,
            return_pc=True):
     """smooth_k + block_scores + hard_topk on device -> (pc fp32, mask u8, idx i32)."""

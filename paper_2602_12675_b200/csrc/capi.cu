@@ -191,6 +191,7 @@ struct Workspace {
     float* hpart;
     float* htot;
     void* htot16;
+    void* phiq;  // bf16 non-QAT path: phi(Q) rows, TMA-loaded by the sparse kernel
     int8_t *qc, *kc, *vct;
     float *qs, *ks, *vs;
     int32_t* cnt;
@@ -215,6 +216,7 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.hpart = c.take<float>(g.BH * g.nchunk * g.d * g.d);
     t.htot = c.take<float>(g.BH * g.d * g.d);
     t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
+    t.phiq = (g.bf16 && !g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
@@ -352,6 +354,7 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 struct LinPlan {
     cudaEvent_t dep = nullptr;
     bool kprep = false;
+    bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
     float* kbar = nullptr;
     std::function<sla2_status()> between;
 };
@@ -362,13 +365,15 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
                                          const int32_t* cnt, int kstride, void* out, const sla2_fwd_saved* saved,
                                          cudaStream_t st, const LinPlan& plan = LinPlan{}) {
     const float isd = inv_sqrt(g.d);
-    CUtensorMap mq, mk, mv, mphi, mht;
+    CUtensorMap mq, mk, mv, mphi, mht, mpq, mo;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
     if (g.bf16) {
         if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
             !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mphi, w.phik, rows, g.d, 64, 64, 2) ||
-            !make_map(&mht, w.htot16, (uint64_t)(g.BH * g.d), g.d, 64, 128, 2))
+            !make_map(&mht, w.htot16, (uint64_t)(g.BH * g.d), g.d, 64, 128, 2) ||
+            (w.phiq && !make_map(&mpq, w.phiq, rows, g.d, 64, 64, 2)) || !make_map(&mo, out, rows, g.d, 64, 64, 2))
             return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (pointers must be 16-byte aligned)");
+        if (w.phiq && !plan.phiq_ready) SLA2_CUDA_TRY(launch_phiq(q, w.phiq, (int64_t)rows, st, &g_launches));
     }
     LinearLaunch la{};
     la.k = k;
@@ -459,6 +464,8 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.tm_v = &mv;
         sa.tm_phik = &mphi;
         sa.tm_ht = &mht;
+        sa.tm_phiq = w.phiq ? &mpq : nullptr;
+        sa.tm_out = &mo;
         if (g.quant) {
             // INT8 QAT (QuantConfig, quant.hpp:15-19): per-tile codes + scales, then the kind::i8 kernel
             QuantLaunch qa{};
@@ -586,9 +593,11 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         CUtensorMap mcol;
         fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);
         ra.kbar_ready = true;
+        ra.phiq_out = w.phiq;  // phi(Q) on the query side, beside the serial column mean
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         LinPlan plan;
         plan.kprep = true;
+        plan.phiq_ready = w.phiq != nullptr;
         plan.kbar = w.kbar;
         plan.between = [&]() -> sla2_status {
             SLA2_CUDA_TRY(launch_router_back(ra, st, &g_launches));
@@ -691,8 +700,9 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
     (void)workspace_bytes;
     CUtensorMap mq, mk, mv;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
+    CUtensorMap mo;
     if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
-        !make_map(&mv, v, rows, g.d, 64, 64, 2))
+        !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mo, out, rows, g.d, 64, 64, 2))
         return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
     SparseLaunch sa{};
     sa.B = g.B;
@@ -712,6 +722,7 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
     sa.tm_k = &mk;
     sa.tm_v = &mv;
     sa.tm_phik = &mk;
+    sa.tm_out = &mo;
     SLA2_CUDA_TRY(launch_sparse_bf16(sa, (cudaStream_t)stream, &g_launches));
     return SLA2_OK;
 }
@@ -722,17 +733,27 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
     sla2_status s = sla2_check_params(p);
     if (s != SLA2_OK) return s;
     if ((s = check_device()) != SLA2_OK) return s;
+    if (!q || !k || !v || !proj_q || !proj_k || !rho || !out)
+        return fail(SLA2_CONTRACT_ERROR, "NULL input/output pointer");
+    // Every (b, h) slice is independent, so the call is pipelined per head: the
+    // copy engine brings head c+1 in while head c computes and head c-1 goes back out.
+    // PCIe, not the GPU, bounds this path; the pipeline hides the compute and the D2H tail.
     const Geo g = geometry(p);
     const size_t esz = g.bf16 ? 2 : 4;
-    const size_t tensor = (size_t)(g.BH * g.N * g.d) * esz;
+    const size_t head = (size_t)(g.N * g.d) * esz;
+    const size_t tensor = (size_t)g.BH * head;
     const size_t projb = (size_t)(g.H * g.d * g.d) * 4, rhob = (size_t)(g.H * g.tm) * 4;
-    const size_t maskb = (size_t)(g.BH * g.tm * g.tn);
-    const size_t wsb = carve(g, nullptr, nullptr);
-    // one cached device arena per thread, grown on demand
+    const size_t head_mask = (size_t)(g.tm * g.tn), maskb = (size_t)g.BH * head_mask;
+    sla2_fwd_params hp = *p;  // one head per call
+    hp.B = 1;
+    hp.H = 1;
+    const size_t wsb = carve(geometry(&hp), nullptr, nullptr);
+    // one cached device arena and three streams per thread
     thread_local void* arena = nullptr;
     thread_local size_t arena_bytes = 0;
-    thread_local cudaStream_t st = nullptr;
-    const size_t need = 4 * tensor + 2 * projb + rhob + maskb + wsb + 8 * 256;
+    thread_local cudaStream_t st = nullptr, up = nullptr, down = nullptr;
+    thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    const size_t need = 4 * tensor + 2 * projb + rhob + maskb + wsb + 10 * 256;
     if (need > arena_bytes) {
         if (arena) cudaFree(arena);
         arena = nullptr;
@@ -740,27 +761,54 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
         SLA2_CUDA_TRY(cudaMalloc(&arena, need));
         arena_bytes = need;
     }
-    if (!st) SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (!st) {
+        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    }
     Carver c{reinterpret_cast<uint8_t*>(arena)};
-    void* dq = c.take<uint8_t>(tensor);
-    void* dk = c.take<uint8_t>(tensor);
-    void* dv = c.take<uint8_t>(tensor);
-    void* dout = c.take<uint8_t>(tensor);
+    uint8_t* dq = c.take<uint8_t>(tensor);
+    uint8_t* dk = c.take<uint8_t>(tensor);
+    uint8_t* dv = c.take<uint8_t>(tensor);
+    uint8_t* dout = c.take<uint8_t>(tensor);
     float* dpq = c.take<float>(projb / 4);
     float* dpk = c.take<float>(projb / 4);
     float* drho = c.take<float>(rhob / 4);
     uint8_t* dmask = c.take<uint8_t>(maskb);
     void* dws = c.take<uint8_t>(wsb);
-    SLA2_CUDA_TRY(cudaMemcpyAsync(dq, q, tensor, cudaMemcpyHostToDevice, st));
-    SLA2_CUDA_TRY(cudaMemcpyAsync(dk, k, tensor, cudaMemcpyHostToDevice, st));
-    SLA2_CUDA_TRY(cudaMemcpyAsync(dv, v, tensor, cudaMemcpyHostToDevice, st));
-    SLA2_CUDA_TRY(cudaMemcpyAsync(dpq, proj_q, projb, cudaMemcpyHostToDevice, st));
-    SLA2_CUDA_TRY(cudaMemcpyAsync(dpk, proj_k, projb, cudaMemcpyHostToDevice, st));
-    SLA2_CUDA_TRY(cudaMemcpyAsync(drho, rho, rhob, cudaMemcpyHostToDevice, st));
-    s = sla2_forward(p, dq, dk, dv, dpq, dpk, drho, dout, mask_out ? dmask : nullptr, nullptr, nullptr, dws, wsb, st);
-    if (s != SLA2_OK) return s;
-    SLA2_CUDA_TRY(cudaMemcpyAsync(out, dout, tensor, cudaMemcpyDeviceToHost, st));
-    if (mask_out) SLA2_CUDA_TRY(cudaMemcpyAsync(mask_out, dmask, maskb, cudaMemcpyDeviceToHost, st));
+    const uint8_t *hq = static_cast<const uint8_t*>(q), *hk = static_cast<const uint8_t*>(k),
+                  *hv = static_cast<const uint8_t*>(v);
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dpq, proj_q, projb, cudaMemcpyHostToDevice, up));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(dpk, proj_k, projb, cudaMemcpyHostToDevice, up));
+    SLA2_CUDA_TRY(cudaMemcpyAsync(drho, rho, rhob, cudaMemcpyHostToDevice, up));
+    int launches = 0;
+    for (int64_t bh = 0; bh < g.BH; ++bh) {
+        const size_t o = (size_t)bh * head;
+        const int64_t h = bh % g.H;
+        // K first: the column mean, the head's latency-bound first stage, needs only K
+        SLA2_CUDA_TRY(cudaMemcpyAsync(dk + o, hk + o, head, cudaMemcpyHostToDevice, up));
+        SLA2_CUDA_TRY(cudaMemcpyAsync(dq + o, hq + o, head, cudaMemcpyHostToDevice, up));
+        SLA2_CUDA_TRY(cudaMemcpyAsync(dv + o, hv + o, head, cudaMemcpyHostToDevice, up));
+        SLA2_CUDA_TRY(cudaEventRecord(ev_in, up));
+        SLA2_CUDA_TRY(cudaStreamWaitEvent(st, ev_in, 0));
+        uint8_t* hm = mask_out ? dmask + (size_t)bh * head_mask : nullptr;
+        s = sla2_forward(&hp, dq + o, dk + o, dv + o, dpq + h * g.d * g.d, dpk + h * g.d * g.d, drho + h * g.tm,
+                         dout + o, hm, nullptr, nullptr, dws, wsb, st);
+        if (s != SLA2_OK) {
+            cudaStreamSynchronize(st);
+            return s;
+        }
+        launches += g_launches;
+        SLA2_CUDA_TRY(cudaEventRecord(ev_out, st));
+        SLA2_CUDA_TRY(cudaStreamWaitEvent(down, ev_out, 0));
+        SLA2_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(out) + o, dout + o, head, cudaMemcpyDeviceToHost, down));
+        if (mask_out)
+            SLA2_CUDA_TRY(cudaMemcpyAsync(mask_out + (size_t)bh * head_mask, hm, head_mask, cudaMemcpyDeviceToHost, down));
+    }
+    g_launches = launches;
+    SLA2_CUDA_TRY(cudaStreamSynchronize(down));
     SLA2_CUDA_TRY(cudaStreamSynchronize(st));
     return SLA2_OK;
 }

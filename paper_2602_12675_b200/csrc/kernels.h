@@ -31,6 +31,7 @@ struct RouterLaunch {
     cudaEvent_t mu_ready;  // optional: recorded once mu_out is complete (lets the caller fork
                            // the linear-branch precompute off it)
     bool kbar_ready;       // kbar already holds the pooled keys (launch_kprep): back half only projects
+    void* phiq_out;        // optional: the front half also writes phi(Q) here (launch_phiq, bf16 d = 128)
 };
 // stage-timing hook (capi.cu): records timeline event `slot` on st when timing is enabled
 void timeline_mark(int slot, cudaStream_t st);
@@ -69,6 +70,8 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
 // Fused key-side prep (d = 128): phi(K~) + z_j (as phik_kernel) and the router's pooled keys
 // kbar [BH][tn][d] (as pool_project_kernel's pooling), reading K once.
 cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches);
+// phi(Q) rows (bf16, d = 128) for the sparse kernel's linear-branch MMA: [rows][128] -> [rows][128]
+cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches);
 
 // ---- sparse / dense attention (sparse_bf16.cu, sparse_f32.cu)
 struct SparseLaunch {
@@ -95,6 +98,8 @@ struct SparseLaunch {
     const CUtensorMap* tm_v;
     const CUtensorMap* tm_phik;
     const CUtensorMap* tm_ht;  // Htot bf16 as [BH*d][d], box 64 x 128, SW128
+    const CUtensorMap* tm_phiq;  // phi(Q) bf16 as [BH*N][d] (launch_phiq), box 64 x 64, SW128
+    const CUtensorMap* tm_out;   // out bf16 as [BH*N][d], box 64 x 64, SW128 (TMA-stored blocks)
     // f32 path
     const float* q;
     const float* k;

@@ -101,6 +101,52 @@ __global__ void __launch_bounds__(128) phik_kernel(const InT* __restrict__ k, co
         zblk[(bh * tn + j) * d + f] = ((zpart[0][f] + zpart[1][f]) + zpart[2][f]) + zpart[3][f];
 }
 
+// phi(Q) = row softmax of Q over the d = 128 features (attention.hpp:456), rounded to bf16 [BH*N][128]:
+// the A operand of the sparse kernel's phi(Q) Hc MMA, which TMA-loads it over its Q tile once
+// the last Q K^T has read Q. Runs on the query side of the router, off the critical path.
+// 16 lanes per row, 8 features (one 16-byte load / store) per lane.
+__global__ void __launch_bounds__(256) phiq_kernel(const __nv_bfloat16* __restrict__ q,
+                                                   __nv_bfloat16* __restrict__ phiq, int64_t rows) {
+    const int64_t row = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
+    const int sub = threadIdx.x & 15;
+    if (row >= rows) return;  // rows is a multiple of 16 (N % 128 == 0): whole half-warps exit
+    const uint4 w = *reinterpret_cast<const uint4*>(q + row * 128 + sub * 8);
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+        x[2 * e] = f.x;
+        x[2 * e + 1] = f.y;
+    }
+    float mx = fmaxf(fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3])), fmaxf(fmaxf(x[4], x[5]), fmaxf(x[6], x[7])));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float s = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        float y;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"((x[e] - mx) * 1.4426950408889634f));
+        x[e] = y;
+        s += y;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float inv = 1.0f / s;
+    uint4 r;
+    r.x = pack_bf16(x[0] * inv, x[1] * inv);
+    r.y = pack_bf16(x[2] * inv, x[3] * inv);
+    r.z = pack_bf16(x[4] * inv, x[5] * inv);
+    r.w = pack_bf16(x[6] * inv, x[7] * inv);
+    *reinterpret_cast<uint4*>(phiq + row * 128 + sub * 8) = r;
+}
+
+cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches) {
+    phiq_kernel<<<(unsigned)((rows + 15) / 16), 256, 0, st>>>((const __nv_bfloat16*)q, (__nv_bfloat16*)phiq, rows);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // tcgen05 partial Htot for the bf16 path (d = 128, bk = 64): CTA per (chunk, bh) covering
 // `per` key blocks; phi(K~)^T V accumulated in 128 TMEM columns; 4 warps read the 128x128
 // fp32 partial back (lane = feature f) and store it.

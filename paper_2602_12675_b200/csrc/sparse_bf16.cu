@@ -25,10 +25,11 @@
 // (tools/umma_bench.py), so Q K^T over one 64-key block (N = 64) runs at a third of the
 // tensor rate; two blocks per instruction (N = 128) halve the QK instruction count.
 //
-// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K pair ring), w1 MMA issuer, w2 TMEM
-// allocator + TMA producer (V / phi(K) ring, Htot), w3 Zc; then w0, w2, w3 together compute
-// phi(Q) and its denominators after the last Q K^T (so it overlaps the loop's tail), w4-7
-// softmax / correction / epilogue (thread = query row).
+// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer (Q, K pair ring, then phi(Q) over Q once
+// the last Q K^T has read Q), w1 MMA issuer, w2 TMEM allocator + TMA producer (V / phi(K) ring,
+// Htot), w3 Zc; then w0, w2, w3 together form the denominators phi(Q) . Zc, w4-7 softmax /
+// correction / epilogue (thread = query row). phi(Q) itself is computed on the router's query
+// side (launch_phiq), off the critical path, and arrives by TMA.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -60,11 +61,11 @@ constexpr uint32_t OFF_V = OFF_K + NKP * KP_BYTES;
 constexpr uint32_t SMEM_BYTES = OFF_V + NSV * 2 * TILE_BYTES;  // 224 KB
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
 // TMEM columns (512 allocated)
-constexpr uint32_t TM_S = 0;      // 2 pair buffers x 128: S fp32 (block 2p in cols 0-63,
-                                  // 2p+1 in 64-127), then each block's P bf16 in its first 32
-constexpr uint32_t TM_O = 256;    // 128: O accumulator
-constexpr uint32_t TM_H = 384;    // 128: Hsel accumulator
-constexpr uint32_t TM_L = 0;      // 128: phi(Q) Hc after the loop (S/P area is free then)
+constexpr uint32_t TM_S = 0;    // 128: S fp32 of the current pair (block 2p in cols 0-63, 2p+1 in 64-127)
+constexpr uint32_t TM_P = 128;  // 2 x 64: P bf16 of pairs n & 1 (block 2p in the first 32, 2p+1 next)
+constexpr uint32_t TM_O = 256;  // 128: O accumulator
+constexpr uint32_t TM_H = 384;  // 128: Hsel accumulator
+constexpr uint32_t TM_L = 0;    // 128: phi(Q) Hc after the loop (the S columns are free then)
 constexpr float RESCALE_LOG2 = 8.0f;  // lazy rescale threshold (P <= 2^8)
 }  // namespace sp
 
@@ -107,10 +108,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
-// phi(Q) for query row r, in place over the row of sQ (row softmax over d, attention.hpp:456,
-// rounded to bf16 -- it is the A operand of the final MMA), and den[r] = phi(Q)_r . Zc.
-__device__ __forceinline__ void phiq_row(uint32_t qb, int r, const float* sZc, float* sDen) {
-    float qv[128];
+// den[r] = phi(Q)_r . Zc for query row r, from the bf16 phi(Q) tile (the A operand of the final
+// MMA, so numerator and denominator see the same rounded phi(Q)); four partial sums.
+__device__ __forceinline__ void den_row(uint32_t qb, int r, const float* sZc, float* sDen) {
+    float d4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int ch = 0; ch < 16; ++ch) {
         uint32_t w[4];
@@ -118,51 +119,29 @@ __device__ __forceinline__ void phiq_row(uint32_t qb, int r, const float* sZc, f
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-            qv[ch * 8 + 2 * e] = f2.x;
-            qv[ch * 8 + 2 * e + 1] = f2.y;
-        }
-    }
-    float qm = -INFINITY;
-#pragma unroll
-    for (int f = 0; f < 128; ++f) qm = fmaxf(qm, qv[f]);
-    float qs = 0.0f;
-#pragma unroll
-    for (int f = 0; f < 128; ++f) {
-        qv[f] = fast_exp2((qv[f] - qm) * 1.4426950408889634f);
-        qs += qv[f];
-    }
-    const float qinv = 1.0f / qs;
-    float den = 0.0f;
-#pragma unroll
-    for (int ch = 0; ch < 16; ++ch) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
             const int f = ch * 8 + 2 * e;
-            const __nv_bfloat162 pk = __floats2bfloat162_rn(qv[f] * qinv, qv[f + 1] * qinv);
-            const float2 pr = __bfloat1622float2(pk);
-            den += pr.x * sZc[f] + pr.y * sZc[f + 1];
-            w[e] = *reinterpret_cast<const uint32_t*>(&pk);
+            d4[e] = fmaf(f2.y, sZc[f + 1], fmaf(f2.x, sZc[f], d4[e]));
         }
-        st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[0], w[1], w[2], w[3]);
     }
-    sDen[r] = den;
+    sDen[r] = (d4[0] + d4[1]) + (d4[2] + d4[3]);
 }
 
 __global__ void __launch_bounds__(256, 1)
     sla2_sparse_bf16_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
-                            const __grid_constant__ CUtensorMap tmHt, const SparseBf16Params p) {
+                            const __grid_constant__ CUtensorMap tmHt, const __grid_constant__ CUtensorMap tmPq,
+                            const __grid_constant__ CUtensorMap tmO, const SparseBf16Params p) {
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_phiq, bar_zc, bar_ht, bar_k_full[NKP], bar_k_empty[NKP],
+    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_pq, bar_den, bar_zc, bar_ht, bar_k_full[NKP],
+        bar_k_empty[NKP],
         bar_v_full[NSV],
-        bar_v_empty[NSV], bar_s_full[2], bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
+        bar_v_empty[NSV], bar_s_full, bar_s_free, bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
     __shared__ float sDen[BQ];
-    __shared__ int phiq_ctr;
+    __shared__ int den_ctr;
 
     const int i = blockIdx.x;       // query block
     const int64_t bh = blockIdx.y;  // (b, h)
@@ -179,9 +158,10 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(&bar_q, 1);
         mbar_init(&bar_qk_done, 1);
         mbar_init(&bar_mma_done, 1);
-        mbar_init(&bar_phiq, 96);
+        mbar_init(&bar_pq, 1);
+        mbar_init(&bar_den, 96);
         mbar_init(&bar_zc, 1);
-        phiq_ctr = 0;
+        den_ctr = 0;
         mbar_init(&bar_ht, 1);
         for (int s = 0; s < NKP; ++s) {
             mbar_init(&bar_k_full[s], 1);
@@ -192,10 +172,11 @@ __global__ void __launch_bounds__(256, 1)
             mbar_init(&bar_v_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&bar_s_full[b], 1);
             mbar_init(&bar_p_full[b], 128);
             mbar_init(&bar_pv_done[b], 1);
         }
+        mbar_init(&bar_s_full, 1);
+        mbar_init(&bar_s_free, 128);
         mbar_init(&bar_lin_ready, 128);
         mbar_init(&bar_lin_done, 1);
         fence_barrier_init();
@@ -216,26 +197,24 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sHt = sV(nb % NSV);
     uint8_t* sHc = sV((nb + 1) % NSV);
     auto kblock = [&](int j) { return dense ? j : idx[j]; };
-    // phi(Q) over sQ, shared by warps 0, 2 and 3 once their own work is issued: Q is the A
-    // operand of every Q K^T, so rows are overwritten only after the last one (bar_qk_done);
-    // warps claim 32-row chunks. Every thread of the three warps arrives on bar_phiq once.
-    auto phiq_share = [&]() {
+    // phi(Q) . Zc, shared by warps 0, 2 and 3 once their own work is issued: phi(Q) replaces
+    // Q in sQ (TMA, bar_pq) after the last Q K^T; warps claim 32-row chunks. Every thread of
+    // the three warps arrives on bar_den once.
+    auto den_share = [&]() {
         if (!linear) return;
         __syncwarp();
-        mbar_wait(&bar_q, 0);
         mbar_wait(&bar_zc, 0);
-        mbar_wait(&bar_qk_done, 0);
+        mbar_wait(&bar_pq, 0);
         __syncwarp();
         const uint32_t qb = smem_u32(sQ);
         for (;;) {
             int c = 0;
-            if (lane == 0) c = atomicAdd(&phiq_ctr, 32);
+            if (lane == 0) c = atomicAdd(&den_ctr, 32);
             c = __shfl_sync(0xffffffffu, c, 0);
             if (c >= BQ) break;
-            phiq_row(qb, c + lane, sZc, sDen);
+            den_row(qb, c + lane, sZc, sDen);
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&bar_phiq);
+        mbar_arrive(&bar_den);
     };
 
     if (warp == 0) {
@@ -264,6 +243,16 @@ __global__ void __launch_bounds__(256, 1)
                     tma_load_2d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, &bar_k_full[s], pol_keep);
                 }
             }
+            if (linear) {
+                // phi(Q) over Q once every Q K^T has read it (same layout as the Q tile)
+                tma_prefetch_desc(&tmPq);
+                mbar_wait(&bar_qk_done, 0);
+                mbar_arrive_expect_tx(&bar_pq, Q_BYTES);
+                tma_load_2d(sQ, &tmPq, 0, qrow, &bar_pq);
+                tma_load_2d(sQ + 8192, &tmPq, 0, qrow + 64, &bar_pq);
+                tma_load_2d(sQ + 16384, &tmPq, 64, qrow, &bar_pq);
+                tma_load_2d(sQ + 24576, &tmPq, 64, qrow + 64, &bar_pq);
+            }
         }
     } else if (warp == 2) {
         // ===================== TMA producer: V / phi(K) ring, Htot =====================
@@ -271,7 +260,12 @@ __global__ void __launch_bounds__(256, 1)
             tma_prefetch_desc(&tmV);
             if (!dense) tma_prefetch_desc(&tmPhi);
             const uint64_t pol_keep = policy_evict_last();
-            const uint32_t tx = dense ? TILE_BYTES : 2 * TILE_BYTES;
+#ifdef SLA2_EXP_NOPHIK
+            const bool ldphi = false;  // experiment: no phi(K) traffic (with SLA2_EXP_NOHS)
+#else
+            const bool ldphi = !dense;
+#endif
+            const uint32_t tx = ldphi ? 2 * TILE_BYTES : TILE_BYTES;
             for (int j = 0; j < nb; ++j) {
                 const int s = j % NSV;
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
@@ -280,7 +274,7 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_arrive_expect_tx(&bar_v_full[s], tx);
                 tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol_keep);
                 tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol_keep);
-                if (!dense) {
+                if (ldphi) {
                     tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol_keep);
                     tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol_keep);
                 }
@@ -325,14 +319,13 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&bar_q, 0);
         tc_fence_after();
         if (lane == 0) SLA2_TR(1);
-        // Static issue order. The tensor pipe runs the MMAs in issue order, so the order is
-        // the schedule:
-        //   QK(0), QK(1); for each pair n: [P(n)] PV(n) -> QK(n+2) -> HS(n)
-        // PV(n) enters the pipe as soon as P(n) exists; QK(n+2) (which reuses S buffer n&1,
-        // safe because PV(n) precedes it) runs before the HS filler, so S(n+2) is ready when
-        // the softmax gets to it; HS(n) fills the pipe while the softmax works on n+1.
+        // Static issue order (the tensor pipe runs MMAs in issue order):
+        //   QK(0); for each pair n: [S(n) read] QK(n+1); [P(n)] PV(n), HS(n)
+        // S has one buffer and P its own two, so QK(n+1) enters the pipe as soon as the softmax
+        // has loaded S(n) into registers and runs under the softmax of pair n; PV(n) and HS(n)
+        // run under the softmax of pair n+1.
         auto issue_qk = [&](int n) {
-            const int s = n % NKP, b = n & 1;
+            const int s = n % NKP;
             mbar_wait(&bar_k_full[s], (n / NKP) & 1);
             tc_fence_after();
             if (lane == 0 && n < 8) SLA2_TR(56 + n);
@@ -341,25 +334,31 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
-                umma_bf16_ss_w(tm + TM_S + b * 128, dQ + off, dK + off, idq, ks > 0);
+                umma_bf16_ss_w(tm + TM_S, dQ + off, dK + off, idq, ks > 0);
             }
-            umma_commit_w(&bar_s_full[b]);
+            umma_commit_w(&bar_s_full);
             umma_commit_w(&bar_k_empty[s]);
             if (n == npu - 1) umma_commit_w(&bar_qk_done);
         };
         if (npu > 0) issue_qk(0);
-        if (npu > 1) issue_qk(1);
         for (int n = 0; n < npu; ++n) {
             const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
+            if (n + 1 < npu) {
+                mbar_wait(&bar_s_free, n & 1);  // the softmax holds S(n) in registers
+                tc_fence_after();
+                issue_qk(n + 1);
+            }
             mbar_wait(&bar_p_full[n & 1], (n >> 1) & 1);
             tc_fence_after();
+            // PV(n), then HS(n) (the V/phi(K) stages are released after it).
+            // (Interleaving PV and HS k-steps measured slower: 1.50 vs 1.28 us per pair.)
             for (int j = j0; j < j1; ++j) {
                 const int sv = j % NSV;
                 mbar_wait(&bar_v_full[sv], (j / NSV) & 1);
                 tc_fence_after();
                 if (lane == 0 && j < 16) SLA2_TR(80 + j);
                 const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
-                const uint32_t aP = tm + TM_S + (n & 1) * 128 + (j & 1) * 64;
+                const uint32_t aP = tm + TM_P + (n & 1) * 64 + (j & 1) * 32;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
                     umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
@@ -367,31 +366,29 @@ __global__ void __launch_bounds__(256, 1)
             }
             umma_commit_w(&bar_pv_done[n & 1]);
             if (lane == 0 && n < 16) SLA2_TR(34 + n);
-#ifndef SLA2_HS_FIRST
-            if (n + 2 < npu) issue_qk(n + 2);
-#endif
             if (!dense) {
                 for (int j = j0; j < j1; ++j) {
                     const int sv = j % NSV;
                     const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
                     const uint64_t dP = dV + (TILE_BYTES >> 4);  // phi(K) tile follows V in the stage
+#ifndef SLA2_EXP_NOHS
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
                         umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
                                        (j > 0 || ks > 0));
+#else
+                    (void)dP;
+#endif
                     umma_commit_w(&bar_v_empty[sv]);  // after PV_j and HS_j
                 }
             }
             if (lane == 0 && n < 16) SLA2_TR(112 + n);
-#ifdef SLA2_HS_FIRST
-            if (n + 2 < npu) issue_qk(n + 2);
-#endif
         }
         umma_commit_w(&bar_mma_done);  // every QK / PV / HS of the loop
         if (linear) {
             // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
             mbar_wait(&bar_lin_ready, 0);
-            mbar_wait(&bar_phiq, 0);
+            mbar_wait(&bar_pq, 0);
             tc_fence_after();
             const uint64_t dH = sdesc_sw128(warp_uniform(smem_u32(sHc)), 16384, 1024);
 #pragma unroll
@@ -444,15 +441,16 @@ __global__ void __launch_bounds__(256, 1)
         // ===================== softmax / correction / epilogue =====================
         const int r = threadIdx.x - 128;  // query row within the block
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const float rho_i = linear ? p.rho[(int64_t)h * p.tm + i] : 0.0f;  // loaded now, used after the loop
         float m2 = -INFINITY, l = 0.0f;
         for (int n = 0; n < npair; ++n) {
             const int b = n & 1;
             const bool two = 2 * n + 1 < nb;
-            mbar_wait(&bar_s_full[b], (n >> 1) & 1);
+            mbar_wait(&bar_s_full, n & 1);
             __syncwarp();
             if (r == 0 && n < 16) SLA2_TR(2 + n);
             tc_fence_after();
-            const uint32_t sbase = tmem + lane_base + TM_S + b * 128;
+            const uint32_t sbase = tmem + lane_base + TM_S;
             uint32_t sr[128];
             tmem_ld32(sbase, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
             tmem_ld32(sbase + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
@@ -461,13 +459,34 @@ __global__ void __launch_bounds__(256, 1)
                 tmem_ld32(sbase + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
             }
             tmem_ld_wait();
-            float mx = -INFINITY;
+            tc_fence_before();
+            mbar_arrive(&bar_s_free);  // QK(n+1) may overwrite S now
+#ifdef SLA2_EXP_NOSOFTMAX
+            // experiment: MMA / TMA pipeline alone (P is garbage)
+            if (n >= 2) mbar_wait(&bar_pv_done[b], ((n - 2) >> 1) & 1);
+            m2 = 0.0f;
+            l = 1.0f;
+            tc_fence_before();
+            mbar_arrive(&bar_p_full[b]);
+            continue;
+#endif
+            // row max as four independent FMNMX3 chains (one 64-long chain was ~0.13 us a pair)
+            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int t = 0; t < 64; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
+            for (int t = 0; t < 64; t += 8) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(sr[t + 2 * u]), __uint_as_float(sr[t + 2 * u + 1])));
+            }
             if (two) {
 #pragma unroll
-                for (int t = 64; t < 128; ++t) mx = fmaxf(mx, __uint_as_float(sr[t]));
+                for (int t = 64; t < 128; t += 8) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(sr[t + 2 * u]), __uint_as_float(sr[t + 2 * u + 1])));
+                }
             }
+            float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
             mx *= p.scale_log2;
             if (n == 0) {
                 m2 = mx;
@@ -492,7 +511,13 @@ __global__ void __launch_bounds__(256, 1)
                     m2 = mnew;
                 }
             }
-            // P = exp2(s * scale - m2) as packed bf16 over each block's first 32 S columns
+            // P = exp2(s * scale - m2) as packed bf16 into P buffer n & 1, last read by PV(n-2)
+            if (n >= 2) {
+                mbar_wait(&bar_pv_done[b], ((n - 2) >> 1) & 1);
+                __syncwarp();
+                tc_fence_after();
+            }
+            const uint32_t pbase = tmem + lane_base + TM_P + b * 64;
             float rs0 = 0.0f, rs1 = 0.0f;
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) {
@@ -506,7 +531,7 @@ __global__ void __launch_bounds__(256, 1)
                     rs1 += p1;
                     w[e] = pack_bf16(p0, p1);
                 }
-                tmem_st32(sbase + blk * 64, w);
+                tmem_st32(pbase + blk * 32, w);
             }
             l += rs0 + rs1;
             tmem_st_wait();
@@ -524,7 +549,7 @@ __global__ void __launch_bounds__(256, 1)
         float den = 1.0f;
         if (linear) {
             // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
-            const float x = p.rho[(int64_t)h * p.tm + i];
+            const float x = rho_i;
             float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
             a = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
             alpha = a;
@@ -533,31 +558,28 @@ __global__ void __launch_bounds__(256, 1)
             __syncwarp();
             const uint32_t hb = smem_u32(sHc), htb = smem_u32(sHt);
             fence_proxy_async_smem();
+            uint32_t hs[128];  // the whole Hsel row: four loads, one wait
 #pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                uint32_t hs[32];
-                tmem_ld32(tmem + lane_base + TM_H + c0, hs);
-                tmem_ld_wait();
+            for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(tmem + lane_base + TM_H + c0, *reinterpret_cast<uint32_t(*)[32]>(&hs[c0]));
+            tmem_ld_wait();
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    const int c = c0 + ch * 8;
-                    const uint32_t off = (c >> 6) * 16384 + sw128_off(r, c & 63);
-                    uint32_t t[4], o4[4];
-                    ld_shared_v4(htb + off, t[0], t[1], t[2], t[3]);
+            for (int ch = 0; ch < 16; ++ch) {
+                const int c = ch * 8;
+                const uint32_t off = (c >> 6) * 16384 + sw128_off(r, c & 63);
+                uint32_t t[4], o4[4];
+                ld_shared_v4(htb + off, t[0], t[1], t[2], t[3]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t[e]));
-                        o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
-                                          tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
-                    }
-                    st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t[e]));
+                    o4[e] = pack_bf16(tf.x - __uint_as_float(hs[c + 2 * e]), tf.y - __uint_as_float(hs[c + 2 * e + 1]));
                 }
+                st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
             }
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&bar_lin_ready);
             if (r == 0) SLA2_TR(51);
-            mbar_wait(&bar_phiq, 0);
+            mbar_wait(&bar_den, 0);
             den = sDen[r];
             mbar_wait(&bar_lin_done, 0);
             if (r == 0) SLA2_TR(52);
@@ -570,17 +592,21 @@ __global__ void __launch_bounds__(256, 1)
         const float inv_den = 1.0f / den;
         const float beta = 1.0f - alpha;
         const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
-        __nv_bfloat16* orow = p.out + grow * D;
+        const uint32_t ob = smem_u32(sQ);  // every MMA reading sQ (Q K^T, phi(Q) Hc) is complete
         const bool want_saved = p.o_s != nullptr;
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            uint32_t o[32], ln[32];
-            tmem_ld32(tmem + lane_base + TM_O + c0, o);
-            if (linear) tmem_ld32(tmem + lane_base + TM_L + c0, ln);
+        for (int c0 = 0; c0 < 128; c0 += 64) {
+            uint32_t o[64], ln[64];  // 64 columns of O and of phi(Q) Hc: four loads, one wait
+            tmem_ld32(tmem + lane_base + TM_O + c0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+            tmem_ld32(tmem + lane_base + TM_O + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+            if (linear) {
+                tmem_ld32(tmem + lane_base + TM_L + c0, *reinterpret_cast<uint32_t(*)[32]>(&ln[0]));
+                tmem_ld32(tmem + lane_base + TM_L + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ln[32]));
+            }
             tmem_ld_wait();
-            float res[32];
+            float res[64];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
+            for (int c = 0; c < 64; ++c) {
                 const float os = __uint_as_float(o[c]) * inv_l;
                 const float ol = linear ? __uint_as_float(ln[c]) * inv_den : 0.0f;
                 res[c] = linear ? alpha * os + beta * ol : os;
@@ -589,15 +615,22 @@ __global__ void __launch_bounds__(256, 1)
                     p.o_l[grow * D + c0 + c] = ol;
                 }
             }
+            // bf16 row into the (now free) Q tile, SW128 layout: one TMA store writes the block
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                uint4 w;
-                w.x = pack_bf16(res[ch * 8 + 0], res[ch * 8 + 1]);
-                w.y = pack_bf16(res[ch * 8 + 2], res[ch * 8 + 3]);
-                w.z = pack_bf16(res[ch * 8 + 4], res[ch * 8 + 5]);
-                w.w = pack_bf16(res[ch * 8 + 6], res[ch * 8 + 7]);
-                *reinterpret_cast<uint4*>(orow + c0 + ch * 8) = w;
-            }
+            for (int ch = 0; ch < 8; ++ch)
+                st_shared_v4(ob + (c0 >> 6) * 16384 + sw128_off(r, ch * 8), pack_bf16(res[ch * 8 + 0], res[ch * 8 + 1]),
+                             pack_bf16(res[ch * 8 + 2], res[ch * 8 + 3]), pack_bf16(res[ch * 8 + 4], res[ch * 8 + 5]),
+                             pack_bf16(res[ch * 8 + 6], res[ch * 8 + 7]));
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (r == 0) {
+            const int orow0 = (int)(bh * p.N + (int64_t)i * BQ);
+            tma_store_2d(&tmO, 0, orow0, sQ);
+            tma_store_2d(&tmO, 0, orow0 + 64, sQ + 8192);
+            tma_store_2d(&tmO, 64, orow0, sQ + 16384);
+            tma_store_2d(&tmO, 64, orow0 + 64, sQ + 24576);
+            tma_store_commit();
         }
         if (r == 0) SLA2_TR(53);
         if (p.big_l) {
@@ -612,10 +645,11 @@ __global__ void __launch_bounds__(256, 1)
             }
             p.big_l[grow] = m2 / 1.4426950408889634f + logf(l) - shift;
         }
+        if (r == 0) tma_store_wait_read();  // sQ must stay valid until the store has read it
         tc_fence_before();
     }
-    // one call site, so the phi(Q) code exists once (the softmax loop keeps the I-cache)
-    if (warp == 0 || warp == 2 || warp == 3) phiq_share();
+    // one call site, so the denominator code exists once (the softmax loop keeps the I-cache)
+    if (warp == 0 || warp == 2 || warp == 3) den_share();
     __syncthreads();
     if (warp == 2) tmem_free(tmem, 512);
 }
@@ -657,9 +691,11 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
     }
     if (a.o_s == nullptr && a.o_l != nullptr) return cudaErrorInvalidValue;
     dim3 grid(a.tm, (unsigned)(a.B * a.H));
+    if ((!a.dense && !a.tm_phiq) || !a.tm_out) return cudaErrorInvalidValue;
     sla2_sparse_bf16_kernel<<<grid, 256, sp::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v,
                                                                 a.dense ? *a.tm_k : *a.tm_phik,
-                                                                a.dense ? *a.tm_k : *a.tm_ht, p);
+                                                                a.dense ? *a.tm_k : *a.tm_ht,
+                                                                a.dense ? *a.tm_k : *a.tm_phiq, *a.tm_out, p);
     ++*launches;
     return cudaGetLastError();
 }

@@ -96,6 +96,24 @@ def test_forward_bf16_batch_layout(cuda):
             assert rel_err(out[b, h], r)[0] <= BF16_TOL
 
 
+@pytest.mark.parametrize("quant", [False, True])
+def test_forward_host_matches_device(cuda, quant):
+    """sla2_forward_host (host buffers, per-head copy/compute pipeline) returns exactly what
+    one device-side sla2_forward over all heads returns, mask included."""
+    torch = _torch()
+    B, H, N, d = 2, 3, 4096, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 22)
+    hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    hpq, hpk, hrho = (torch.from_numpy(x) for x in (pq, pk, rho))
+    out_h, mask_h = sla2.forward_host(hq, hk, hv, hpq, hpk, hrho, k_percent=3.0, quant=quant, return_mask=True)
+    out_d, mask_d = sla2.forward(hq.to(cuda), hk.to(cuda), hv.to(cuda), hpq.to(cuda), hpk.to(cuda), hrho.to(cuda),
+                                 k_percent=3.0, quant=quant, return_mask=True)
+    assert torch.equal(mask_h, mask_d.cpu())
+    assert torch.equal(out_h, out_d.cpu())
+    r = oracle_head(q[1, 2], k[1, 2], v[1, 2], pq[2], pk[2], rho[2], 128, 64, 3.0, quant=quant)[0]
+    assert rel_err(out_h.float().numpy()[1, 2], r)[0] <= BF16_TOL
+
+
 # ----------------------------------------------------------------------------- INT8 QAT forward
 @pytest.mark.parametrize("N,H,k_percent,seed", [(4096, 2, 3.0, 51), (8192, 1, 10.0, 52), (2048, 1, 100.0, 53)])
 def test_forward_qat_vs_oracle(cuda, N, H, k_percent, seed):
