@@ -348,8 +348,8 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 // How the linear-branch precompute is scheduled (sla2_forward):
 //   dep     fork it onto a second stream off this event (it needs only mu), concurrently with
 //           whatever st is still doing; st joins it before the sparse kernel
-//   kprep   first run launch_kprep on st (phi(K~), z_j and the router's pooled keys in one
-//           pass over K), then fork the rest (Htot partials + reduction) off it
+//   kprep   fork at mu: phi(K~) and z_j (launch_kphi), Htot partials and reduction on the
+//           linear stream; the router's pooled keys (launch_kpool) then run on st
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
@@ -393,13 +393,14 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.nchunk = g.nchunk;
     la.tm_phik = &mphi;
     la.tm_v = &mv;
+    la.tm_k = (g.bf16 && g.d == 128 && g.bk == 64) ? &mk : nullptr;
     cudaEvent_t dep = plan.dep;
     if (plan.kprep) {
         thread_local cudaEvent_t ev_k = nullptr;
         if (!ev_k) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming));
-        SLA2_CUDA_TRY(launch_kprep(la, plan.kbar, st, &g_launches));
-        mark(6, st);
-        la.phik_ready = true;
+        // fork at mu: phi(K~), z_j and Htot on the linear stream, beside the router's pooled
+        // keys (launch_kpool, below) and back half on st
+        la.phik_ready = !(la.tm_k && la.mu);  // the fused kernel computes phi(K~) itself
         SLA2_CUDA_TRY(cudaEventRecord(ev_k, st));
         dep = ev_k;
     }
@@ -411,9 +412,14 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
         }
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
+        if (plan.kprep && la.phik_ready) SLA2_CUDA_TRY(launch_kphi(la, lin, &g_launches));
         SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
         mark(8, lin);
         SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
+        if (plan.kprep) {
+            SLA2_CUDA_TRY(launch_kpool(la, plan.kbar, st, &g_launches));
+            mark(6, st);
+        }
         if (plan.between) {
             const sla2_status bs = plan.between();
             if (bs != SLA2_OK) {
@@ -587,8 +593,8 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
     if (!ev_mu && cudaEventCreateWithFlags(&ev_mu, cudaEventDisableTiming) != cudaSuccess)
         return fail(SLA2_CUDA_ERROR, "cudaEventCreate failed");
     if (g.d == 128 && 4 * g.bk * 128 * (g.bf16 ? 2 : 4) <= 200 * 1024) {
-        // router front (mu, query side) -> kprep (phi(K~), z_j, pooled keys: one pass over K)
-        // -> fork Htot partials + reduction || router back (key projection, scores, top-k)
+        // router front (mu, query side) -> pooled keys -> router back (projection, scores, top-k),
+        // with phi(K~), z_j and Htot forked beside the router's back half
         RouterLaunch ra;
         CUtensorMap mcol;
         fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);

@@ -64,12 +64,17 @@ struct LinearLaunch {
     int nchunk;       // key-block chunks per head for the H partials
     const CUtensorMap* tm_phik;  // bf16 path: TMA maps (box 64x64, SW128) over [BH*N][d]
     const CUtensorMap* tm_v;
+    const CUtensorMap* tm_k;  // bf16 path: K map (box 64x64, SW128); with mu set, phi(K~) is fused
+                              // into the Htot partial kernel (kphi_htot_kernel)
     bool phik_ready;  // phi(K~) and z_j already written by launch_kprep
 };
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches);
 // Fused key-side prep (d = 128): phi(K~) + z_j (as phik_kernel) and the router's pooled keys
 // kbar [BH][tn][d] (as pool_project_kernel's pooling), reading K once.
 cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches);
+// the two halves of launch_kprep: pooled keys only (router critical path) / phi(K~) and z_j only
+cudaError_t launch_kpool(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches);
+cudaError_t launch_kphi(const LinearLaunch& a, cudaStream_t st, int* launches);
 // phi(Q) rows (bf16, d = 128) for the sparse kernel's linear-branch MMA: [rows][128] -> [rows][128]
 cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches);
 

@@ -235,6 +235,194 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0) tmem_free(tmem, 128);
 }
 
+// Fused phi(K~) + partial Htot for the bf16 path (d = 128, bk = 64): CTA per (chunk of `per`
+// key blocks, bh). TMA brings K and V tiles; four warps turn the K tile into phi(K~) in place
+// (the same instructions as kprep_kernel: fp32 K - mu, redux max, ex2.approx, shuffle sum,
+// __fdividef, bf16 round) and store the rows to global for the sparse kernel; the tcgen05 MMA
+// then reads phi(K~) straight from shared memory (no global round trip: K + V read once,
+// phi(K~) written once). z_j: the four row-group partials summed in fixed order.
+// Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2-5 phi(K~) then the partial's TMEM read-back.
+namespace kh {
+constexpr int D = 128, BK = 64, NS = 3;
+constexpr uint32_t TILE = BK * D * 2;            // 16 KB
+constexpr uint32_t SMEM = NS * 2 * TILE + 1024;  // [K -> phi(K~)][V] per stage
+}  // namespace kh
+
+__global__ void __launch_bounds__(192, 1)
+    kphi_htot_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                     const float* __restrict__ mu, __nv_bfloat16* __restrict__ phik, float* __restrict__ zblk,
+                     float* __restrict__ hpart, int N, int per, int nchunk) {
+    using namespace kh;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[NS], phi_ready[NS], empty[NS], done;
+    __shared__ uint32_t tbase;
+    __shared__ __align__(16) float zpart[4][D];
+    const int chunk = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tn = N / BK;
+    const int j0 = chunk * per;
+    const int nblk = min(per, tn - j0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&phi_ready[s], 128);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&tbase, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tbase;
+    auto sK = [&](int s) { return smem + s * 2 * TILE; };
+    auto sV = [&](int s) { return smem + s * 2 * TILE + TILE; };
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmK);
+            tma_prefetch_desc(&tmV);
+            for (int b = 0; b < nblk; ++b) {
+                const int s = b % NS;
+                if (b >= NS) mbar_wait(&empty[s], ((b / NS) - 1) & 1);
+                const int row = (int)(bh * N + (int64_t)(j0 + b) * BK);
+                mbar_arrive_expect_tx(&full[s], 2 * TILE);
+                tma_load_2d(sK(s), &tmK, 0, row, &full[s]);
+                tma_load_2d(sK(s) + 8192, &tmK, 64, row, &full[s]);
+                tma_load_2d(sV(s), &tmV, 0, row, &full[s]);
+                tma_load_2d(sV(s) + 8192, &tmV, 64, row, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t ID = idesc_bf16(128, 128, true, true);
+            for (int b = 0; b < nblk; ++b) {
+                const int s = b % NS;
+                mbar_wait(&phi_ready[s], (b / NS) & 1);
+                tc_fence_after();
+                const uint32_t a = smem_u32(sK(s)), bb = smem_u32(sV(s));
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    umma_bf16_ss(tmem, sdesc_sw128(a + ks * 2048, 8192, 1024),
+                                 sdesc_sw128(bb + ks * 2048, 8192, 1024), ID, (b > 0 || ks > 0));
+                umma_commit(&empty[s]);
+            }
+            umma_commit(&done);
+        }
+    } else {
+        // phi(K~): warp g = warp - 2 owns rows 16g .. 16g + 15; lane l owns features 4l .. 4l + 3
+        const int g = warp - 2;
+        float m[4];
+        {
+            const float4 t = *reinterpret_cast<const float4*>(mu + bh * D + lane * 4);
+            m[0] = t.x;
+            m[1] = t.y;
+            m[2] = t.z;
+            m[3] = t.w;
+        }
+        // SW128 position of the lane's 8 bytes in row r: atom (l / 16), 16-byte chunk (l % 16) / 2
+        const uint32_t atom = (uint32_t)(lane >> 4) * 8192u, ch = (uint32_t)((lane & 15) >> 1),
+                       half = (uint32_t)(lane & 1) * 8u;
+        for (int b = 0; b < nblk; ++b) {
+            const int s = b % NS;
+            mbar_wait(&full[s], (b / NS) & 1);
+            const uint32_t kb = smem_u32(sK(s));
+            const int64_t grow0 = bh * N + (int64_t)(j0 + b) * BK;
+            float z[4] = {0.f, 0.f, 0.f, 0.f};
+            constexpr int U = 4;
+            for (int r0 = g * 16; r0 < g * 16 + 16; r0 += U) {
+                float xs[U][4], mx[U], sum[U];
+                uint32_t addr[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = r0 + u;
+                    addr[u] = kb + atom + (uint32_t)r * 128u + ((ch ^ (uint32_t)(r & 7)) << 4) + half;
+                    uint32_t w0, w1;
+                    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(addr[u]));
+                    xs[u][0] = __uint_as_float(w0 << 16);
+                    xs[u][1] = __uint_as_float(w0 & 0xffff0000u);
+                    xs[u][2] = __uint_as_float(w1 << 16);
+                    xs[u][3] = __uint_as_float(w1 & 0xffff0000u);
+                    mx[u] = -INFINITY;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        xs[u][e] = __fsub_rn(xs[u][e], m[e]);
+                        mx[u] = fmaxf(mx[u], xs[u][e]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mx[u]) : "f"(mx[u]));
+                    sum[u] = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float y;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"((xs[u][e] - mx[u]) * 1.4426950408889634f));
+                        xs[u][e] = y;
+                        sum[u] += y;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) sum[u] += __shfl_xor_sync(0xffffffffu, sum[u], o);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const float inv = __fdividef(1.0f, sum[u]);
+                    const uint32_t w0 = pack_bf16(xs[u][0] * inv, xs[u][1] * inv);
+                    const uint32_t w1 = pack_bf16(xs[u][2] * inv, xs[u][3] * inv);
+                    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr[u]), "r"(w0), "r"(w1) : "memory");
+                    *reinterpret_cast<uint2*>(phik + (grow0 + r0 + u) * D + lane * 4) = make_uint2(w0, w1);
+                    z[0] += __uint_as_float(w0 << 16);
+                    z[1] += __uint_as_float(w0 & 0xffff0000u);
+                    z[2] += __uint_as_float(w1 << 16);
+                    z[3] += __uint_as_float(w1 & 0xffff0000u);
+                }
+            }
+            fence_proxy_async_smem();  // phi(K~) written by threads, read by the tensor core
+            mbar_arrive(&phi_ready[s]);
+            // z_j = ((z_0 + z_1) + z_2) + z_3 over the four row groups
+            *reinterpret_cast<float4*>(&zpart[g][lane * 4]) = make_float4(z[0], z[1], z[2], z[3]);
+            named_bar_sync(1, 128);
+            if (g == 0) {
+                float4 zz;
+                float* zo = &zz.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int f = lane * 4 + e;
+                    zo[e] = ((zpart[0][f] + zpart[1][f]) + zpart[2][f]) + zpart[3][f];
+                }
+                *reinterpret_cast<float4*>(zblk + (bh * tn + j0 + b) * D + lane * 4) = zz;
+            }
+            named_bar_sync(1, 128);
+        }
+        // the chunk's partial phi(K~)^T V: lane = feature f
+        mbar_wait(&done, 0);
+        __syncwarp();
+        tc_fence_after();
+        const int q = warp & 3;  // TMEM lane quarter of this warp
+        const int f = q * 32 + lane;
+        float* dst = hpart + ((bh * nchunk + chunk) * (int64_t)D + f) * D;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 64) {
+            uint32_t r[64];
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 64; c += 4)
+                *reinterpret_cast<float4*>(dst + c0 + c) =
+                    make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                                __uint_as_float(r[c + 3]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_free(tmem, 128);
+}
+
 // SIMT partial Htot for the fp32 path: CTA per (chunk of `rows` tokens, bh); thread owns
 // entries e = tid, tid+256, ... of the d x d matrix; tokens staged through smem.
 template <typename InT>
@@ -377,7 +565,10 @@ __device__ __forceinline__ float warp_max_f32(float x) {
     return r;
 }
 
-template <typename T>
+// POOL / PHI select the halves: the pooled keys are on the router's critical path (mu -> pooled
+// keys -> projection -> scores), phi(K~) / z_j only feed the linear branch, so sla2_forward runs
+// the pool-only instance on the router's stream and the phi-only one beside the router's back half.
+template <typename T, bool POOL, bool PHI>
 __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, const float* __restrict__ mu,
                                                     T* __restrict__ phik, float* __restrict__ zblk,
                                                     float* __restrict__ kbar, int N, int bk, int tn) {
@@ -428,10 +619,11 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (mu) xs[u][e] = __fsub_rn(xs[u][e], m[e]);
-                pool[e] = __dadd_rn(pool[e], (double)xs[u][e]);  // rows in order (exact pooling)
+                if (POOL) pool[e] = __dadd_rn(pool[e], (double)xs[u][e]);  // rows in order (exact pooling)
                 mx[u] = fmaxf(mx[u], xs[u][e]);
             }
         }
+        if (!PHI) continue;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             mx[u] = warp_max_f32(mx[u]);
@@ -460,26 +652,44 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
     }
     float* kb = kbar + (bh * tn + j) * D + lane * 4;
     float* zb = zblk + (bh * tn + j) * D + lane * 4;
-    float kv[4];
+    if (POOL) {
+        float kv[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) kv[e] = __double2float_rn(__ddiv_rn(pool[e], (double)bk));
-    *reinterpret_cast<float4*>(kb) = make_float4(kv[0], kv[1], kv[2], kv[3]);
-    *reinterpret_cast<float4*>(zb) = make_float4(z[0], z[1], z[2], z[3]);
+        for (int e = 0; e < 4; ++e) kv[e] = __double2float_rn(__ddiv_rn(pool[e], (double)bk));
+        *reinterpret_cast<float4*>(kb) = make_float4(kv[0], kv[1], kv[2], kv[3]);
+    }
+    if (PHI) *reinterpret_cast<float4*>(zb) = make_float4(z[0], z[1], z[2], z[3]);
 }
 
-cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches) {
+template <bool POOL, bool PHI>
+static void kprep_go(const LinearLaunch& a, float* kbar, cudaStream_t st) {
     const int tn = a.N / a.bk;
     const dim3 g((tn + 3) / 4, (unsigned)a.BH);
     const size_t smem = (size_t)4 * a.bk * 128 * (a.bf16 ? 2 : 4);
     if (a.bf16) {
-        cudaFuncSetAttribute(kprep_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kprep_kernel<__nv_bfloat16><<<g, 128, smem, st>>>((const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik,
-                                                          a.zblk, kbar, a.N, a.bk, tn);
+        cudaFuncSetAttribute(kprep_kernel<__nv_bfloat16, POOL, PHI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        kprep_kernel<__nv_bfloat16, POOL, PHI><<<g, 128, smem, st>>>(
+            (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, kbar, a.N, a.bk, tn);
     } else {
-        cudaFuncSetAttribute(kprep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kprep_kernel<float><<<g, 128, smem, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, kbar, a.N,
-                                                  a.bk, tn);
+        cudaFuncSetAttribute(kprep_kernel<float, POOL, PHI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kprep_kernel<float, POOL, PHI><<<g, 128, smem, st>>>((const float*)a.k, a.mu, (float*)a.phik, a.zblk, kbar,
+                                                             a.N, a.bk, tn);
     }
+}
+
+cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches) {
+    kprep_go<true, true>(a, kbar, st);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_kpool(const LinearLaunch& a, float* kbar, cudaStream_t st, int* launches) {
+    kprep_go<true, false>(a, kbar, st);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_kphi(const LinearLaunch& a, cudaStream_t st, int* launches) {
+    kprep_go<false, true>(a, nullptr, st);
     ++*launches;
     return cudaGetLastError();
 }
@@ -487,7 +697,17 @@ cudaError_t launch_kprep(const LinearLaunch& a, float* kbar, cudaStream_t st, in
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches) {
     const int tn = a.N / a.bk;
     dim3 g1(tn, (unsigned)a.BH);
-    if (a.bf16) {
+    if (a.bf16 && a.tm_k && !a.phik_ready && a.mu) {
+        // phi(K~), z_j and the Htot partials in one pass over K and V
+        static bool attr_f = false;
+        if (!attr_f) {
+            cudaFuncSetAttribute(kphi_htot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kh::SMEM);
+            attr_f = true;
+        }
+        const int per = (tn + a.nchunk - 1) / a.nchunk;
+        kphi_htot_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 192, kh::SMEM, st>>>(
+            *a.tm_k, *a.tm_v, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.hpart, a.N, per, a.nchunk);
+    } else if (a.bf16) {
         if (!a.phik_ready)
             phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(
                 (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.N, a.d, a.bk);
@@ -511,7 +731,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
     const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
     lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
         a.hpart, a.zblk, a.htot, a.bf16 ? (__nv_bfloat16*)a.htot16 : nullptr, a.ztot, a.nchunk, a.d, tn);
-    *launches += a.phik_ready ? 2 : 3;
+    *launches += (a.phik_ready || (a.bf16 && a.tm_k && a.mu)) ? 2 : 3;
     return cudaGetLastError();
 }
 

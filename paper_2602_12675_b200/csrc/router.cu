@@ -165,6 +165,122 @@ __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__
     mu[bh * d + cg * COLS + col] = __fmul_rn(acc, inv);
 }
 
+// K0 for bf16, transposed staging. The one-column-per-thread chain above loads one element per
+// row (LDS.U16 -> FHADD): measured 7.4 cycles per row against the 4.5-cycle FADD latency
+// (profiles/lat_bench_r01.txt), the per-load scoreboard wait being the difference. Here two
+// transposer warps turn each TMA tile [128 rows][64 cols] into [64 cols][128 rows] (8x8 blocks:
+// 8 x LDS.128, 32 PRMT, 8 x STS.128), so a chain thread gets 8 consecutive rows of its column
+// from one LDS.128 and runs 8 FHADDs on registers. Same serial order, same bits.
+// Transposed row of column c: 16 chunks of 8 rows, chunk rc at ((rc ^ key(c)) * 16): the XOR
+// key spreads both the transposer's stores and the chain threads' loads over all banks.
+namespace cmt {
+constexpr int ROWS = 128, COLS = 64, NST = 4, NTS = 4;
+constexpr int TILE = ROWS * COLS * 2;  // 16 KB (both layouts)
+__device__ __forceinline__ uint32_t tpos(int c, int rc) {
+    return (uint32_t)c * 256u + (uint32_t)((rc ^ ((c ^ (c >> 3)) & 7)) * 16);
+}
+}  // namespace cmt
+
+__device__ __forceinline__ float add2_bf16(float acc, uint32_t w) {
+    // acc + row(lo) then + row(hi): two FHADD.BF16, each rounded once (= fp32 add of the widened value)
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
+        "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %0, hi, %0;\n\t}"
+        : "+f"(acc)
+        : "r"(w));
+    return acc;
+}
+
+__global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__ CUtensorMap tmK, float* __restrict__ mu,
+                                                         int N, int d) {
+    using namespace cmt;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* ring = smem_raw;                   // [NST][128 rows][128 B]  (TMA)
+    uint8_t* tring = smem_raw + NST * TILE;     // [NTS][64 cols][256 B]   (transposed)
+    __shared__ uint64_t full[NST], empty[NST], tfull[NTS], tempty[NTS];
+    const int cg = blockIdx.x;
+    const int64_t bh = blockIdx.y;
+    const int warp = threadIdx.x >> 5;
+    const int nchunk = N / ROWS;  // N % 128 == 0 is checked by the launcher
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 64);
+        }
+        for (int s = 0; s < NTS; ++s) {
+            mbar_init(&tfull[s], 64);
+            mbar_init(&tempty[s], 64);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 4) {  // TMA producer
+        if ((threadIdx.x & 31) == 0) {
+            tma_prefetch_desc(&tmK);
+            for (int c = 0; c < nchunk; ++c) {
+                const int s = c % NST;
+                if (c >= NST) mbar_wait(&empty[s], ((c / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], TILE);
+                tma_load_2d(ring + s * TILE, &tmK, cg * COLS, (int)(bh * N + (int64_t)c * ROWS), &full[s]);
+            }
+        }
+        return;
+    }
+    if (warp >= 2) {  // transposers: thread t owns 8x8 blocks (rb, cb) = (t/8 + 8k, t%8), k = 0, 1
+        const int t = threadIdx.x - 64;
+        const int cb = t & 7;
+        for (int c = 0; c < nchunk; ++c) {
+            const int s = c % NST, ts = c % NTS;
+            mbar_wait(&full[s], (c / NST) & 1);
+            if (c >= NTS) mbar_wait(&tempty[ts], ((c / NTS) - 1) & 1);
+            const uint32_t src = smem_u32(ring + s * TILE), dst = smem_u32(tring + ts * TILE);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int rb = (t >> 3) + 8 * k;
+                uint32_t w[8][4];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    ld_shared_v4(src + (rb * 8 + i) * 128 + cb * 16, w[i][0], w[i][1], w[i][2], w[i][3]);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {  // columns 2a, 2a+1
+                    uint32_t lo[4], hi[4];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {  // rows 2b, 2b+1
+                        lo[b] = __byte_perm(w[2 * b][a], w[2 * b + 1][a], 0x5410);
+                        hi[b] = __byte_perm(w[2 * b][a], w[2 * b + 1][a], 0x7632);
+                    }
+                    const int c0 = cb * 8 + 2 * a;
+                    st_shared_v4(dst + cmt::tpos(c0, rb), lo[0], lo[1], lo[2], lo[3]);
+                    st_shared_v4(dst + cmt::tpos(c0 + 1, rb), hi[0], hi[1], hi[2], hi[3]);
+                }
+            }
+            mbar_arrive(&empty[s]);
+            mbar_arrive(&tfull[ts]);
+        }
+        return;
+    }
+    // chain threads: column col, 8 rows per LDS.128, next load issued before the 8 adds
+    const int col = threadIdx.x;
+    float acc = 0.0f;
+    for (int c = 0; c < nchunk; ++c) {
+        const int ts = c % NTS;
+        mbar_wait(&tfull[ts], (c / NTS) & 1);
+        const uint32_t base = smem_u32(tring + ts * TILE);
+        uint32_t cur[4], nxt[4];
+        ld_shared_v4(base + cmt::tpos(col, 0), cur[0], cur[1], cur[2], cur[3]);
+#pragma unroll
+        for (int rc = 0; rc < 16; ++rc) {
+            if (rc + 1 < 16) ld_shared_v4(base + cmt::tpos(col, rc + 1), nxt[0], nxt[1], nxt[2], nxt[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc = add2_bf16(acc, cur[e]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
+        }
+        mbar_arrive(&tempty[ts]);
+    }
+    const float inv = __fdiv_rn(1.0f, (float)N);
+    mu[bh * d + cg * COLS + col] = __fmul_rn(acc, inv);
+}
+
 // K0 (fast variant, exact_mu = 0): column sums in double over row chunks, then the same
 // final scaling. Not the reference's order: the mask can differ at fp32 ties.
 template <typename T>
@@ -738,7 +854,15 @@ template <typename T>
 static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, int N, int d, cudaStream_t st,
                       int* launches) {
     constexpr int COLS = 128 / sizeof(T);
-    if (tmk && N % cm::ROWS == 0 && d % COLS == 0) {
+    if (sizeof(T) == 2 && tmk && N % cmt::ROWS == 0 && d % cmt::COLS == 0) {
+        const int smem = (cmt::NST + cmt::NTS) * cmt::TILE;
+        static bool attr_t = false;
+        if (!attr_t) {
+            cudaFuncSetAttribute(colmean_tr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr_t = true;
+        }
+        colmean_tr_kernel<<<dim3(d / cmt::COLS, BH), 160, smem, st>>>(*tmk, mu, N, d);
+    } else if (tmk && N % cm::ROWS == 0 && d % COLS == 0) {
         const int smem = cm::NST * cm::ROWS * 128;
         static bool attr = false;
         if (!attr) {
