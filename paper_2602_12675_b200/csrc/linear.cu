@@ -485,19 +485,23 @@ __global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* 
         if (htot16) htot16[bh * dd + e] = __float2bfloat16_rn(s);
     }
     if (blockIdx.x == 0) {
-        // Ztot[f] = sum_j z_j[f]: blockDim/ d threads per feature over strided j, then combined
+        // Ztot[f] = sum_j z_j[f]: blockDim / d threads per feature over strided j (16 loads in
+        // flight per thread), then combined in part order
         __shared__ float zs[1024];
         const int parts = blockDim.x / d;
         const int f = threadIdx.x % d, part = threadIdx.x / d;
         float s = 0.0f;
         if (part < parts) {
-            int j = part;
-            for (; j + 3 * parts < tn; j += 4 * parts) {
-                const float a0 = zblk[(bh * tn + j) * d + f], a1 = zblk[(bh * tn + j + parts) * d + f];
-                const float a2 = zblk[(bh * tn + j + 2 * parts) * d + f], a3 = zblk[(bh * tn + j + 3 * parts) * d + f];
-                s += (a0 + a1) + (a2 + a3);
+            for (int j0 = part; j0 < tn; j0 += 16 * parts) {
+                float t[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int j = j0 + u * parts;
+                    t[u] = j < tn ? zblk[(bh * tn + j) * d + f] : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) s += t[u];
             }
-            for (; j < tn; j += parts) s += zblk[(bh * tn + j) * d + f];
         }
         zs[threadIdx.x] = s;
         __syncthreads();

@@ -258,22 +258,38 @@ __global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__
         }
         return;
     }
-    // chain threads: column col, 8 rows per LDS.128, next load issued before the 8 adds
+    // chain threads: column col, 8 rows per LDS.128. Loads run two groups (16 rows, ~72 cycles
+    // of adds) ahead of the chain, across chunk boundaries, so no add waits on shared memory.
     const int col = threadIdx.x;
     float acc = 0.0f;
+    uint32_t g0[4], g1[4];
+    mbar_wait(&tfull[0], 0);
+    {
+        const uint32_t b0 = smem_u32(tring);
+        ld_shared_v4(b0 + cmt::tpos(col, 0), g0[0], g0[1], g0[2], g0[3]);
+        ld_shared_v4(b0 + cmt::tpos(col, 1), g1[0], g1[1], g1[2], g1[3]);
+    }
     for (int c = 0; c < nchunk; ++c) {
         const int ts = c % NTS;
-        mbar_wait(&tfull[ts], (c / NTS) & 1);
         const uint32_t base = smem_u32(tring + ts * TILE);
-        uint32_t cur[4], nxt[4];
-        ld_shared_v4(base + cmt::tpos(col, 0), cur[0], cur[1], cur[2], cur[3]);
+        const bool more = c + 1 < nchunk;
+        const uint32_t nbase = smem_u32(tring + ((c + 1) % NTS) * TILE);
 #pragma unroll
         for (int rc = 0; rc < 16; ++rc) {
-            if (rc + 1 < 16) ld_shared_v4(base + cmt::tpos(col, rc + 1), nxt[0], nxt[1], nxt[2], nxt[3]);
+            uint32_t g2[4] = {0u, 0u, 0u, 0u};
+            if (rc + 2 < 16) {
+                ld_shared_v4(base + cmt::tpos(col, rc + 2), g2[0], g2[1], g2[2], g2[3]);
+            } else if (more) {
+                if (rc == 14) mbar_wait(&tfull[(c + 1) % NTS], ((c + 1) / NTS) & 1);
+                ld_shared_v4(nbase + cmt::tpos(col, rc - 14), g2[0], g2[1], g2[2], g2[3]);
+            }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc = add2_bf16(acc, cur[e]);
+            for (int e = 0; e < 4; ++e) acc = add2_bf16(acc, g0[e]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
+            for (int e = 0; e < 4; ++e) {
+                g0[e] = g1[e];
+                g1[e] = g2[e];
+            }
         }
         mbar_arrive(&tempty[ts]);
     }
@@ -686,13 +702,19 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
-            const float* k0 = kpb + jg * 4;
+            // pointer-stepped (d and tn are run-time: recomputing 64-bit addresses per step
+            // cost more instructions than the FP work, ncu source page)
+            const float4* kq = reinterpret_cast<const float4*>(kpb + jg * 4);
+            const size_t kstep = (size_t)tn / 4;  // one feature row of keys, in float4
+            const float* sqr = sq + rg * 4 * d;
+#pragma unroll 2
             for (int c = 0; c < d; c += 4) {
                 float4 kv[4], qv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) kv[u] = __ldg(reinterpret_cast<const float4*>(k0 + (int64_t)(c + u) * tn));
+                for (int u = 0; u < 4; ++u) kv[u] = __ldg(kq + u * kstep);
+                kq += 4 * kstep;
 #pragma unroll
-                for (int a = 0; a < 4; ++a) qv[a] = *reinterpret_cast<const float4*>(sq + (rg * 4 + a) * d + c);
+                for (int a = 0; a < 4; ++a) qv[a] = *reinterpret_cast<const float4*>(sqr + a * d + c);
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
                     const float qa[4] = {qv[a].x, qv[a].y, qv[a].z, qv[a].w};
