@@ -30,12 +30,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SLA2 attn fwd ms & effective TFLOPS at Wan2.1 shape, 97% sparsity, 1-8 GPU"
 CONFIGS = {
-    # configs[1]: Wan2.1-1.3B attention shape, N = 32760 padded to 32768
-    "cfg2": dict(workload="wan2.1-1.3B-480p attention (BASELINE configs[1])", B=1, H=12, N=32768, d=128, bq=128,
+    # configs[1]: the true Wan2.1-1.3B attention shape, N = 32760 (ragged: the last query block
+    # has 120 rows and the last key block 56 keys; tests/test_ragged.py)
+    "cfg2": dict(workload="wan2.1-1.3B-480p attention (BASELINE configs[1])", B=1, H=12, N=32760, d=128, bq=128,
                  bk=64, k_percent=3.0, bf16=True, quant=False),
+    # the same padded to the block multiple (the reference's own shape rule), for comparison
+    "cfg2pad": dict(workload="wan2.1-1.3B-480p attention, N padded to 32768", B=1, H=12, N=32768, d=128, bq=128,
+                    bk=64, k_percent=3.0, bf16=True, quant=False),
+    # the INT8 QAT path keeps the reference's divisibility rule (N padded to 32768)
     "cfg3": dict(workload="wan2.1-1.3B-480p attention, INT8 QAT (BASELINE configs[2])", B=1, H=12, N=32768,
                  d=128, bq=128, bk=64, k_percent=3.0, bf16=True, quant=True),
-    "cfg4": dict(workload="wan2.1-14B-720p attention (BASELINE configs[3])", B=1, H=40, N=75648, d=128, bq=128,
+    "cfg4": dict(workload="wan2.1-14B-720p attention (BASELINE configs[3])", B=1, H=40, N=75600, d=128, bq=128,
                  bk=64, k_percent=3.0, bf16=True, quant=False),
     "cfg1": dict(workload="fp32 CPU-oracle case (BASELINE configs[0])", B=1, H=2, N=4096, d=64, bq=64, bk=64,
                  k_percent=10.0, bf16=False, quant=False),
@@ -135,7 +140,11 @@ def cpu_reference_run(c, steps, warmup, threads=None):
         o = oc.port()
         o.set_threads(threads) if hasattr(o, "set_threads") else o._set_threads(threads)
         kind = "port"
-    q, k, v, pq, pk, rho = make_inputs(1, 1, c["N"], c["d"], seed=7, bf16=c["bf16"], bq=c["bq"], bk=c["bk"])
+    # the reference rejects N % block != 0 (attention.hpp:39-41): a ragged N is timed at the next
+    # multiple of the blocks (0.02% more work at 32760 -> 32768)
+    blk = max(c["bq"], c["bk"])
+    n_ref = -(-c["N"] // blk) * blk
+    q, k, v, pq, pk, rho = make_inputs(1, 1, n_ref, c["d"], seed=7, bf16=c["bf16"], bq=c["bq"], bk=c["bk"])
     times = []
     for s in range(warmup + steps):
         t0 = time.perf_counter()
@@ -144,7 +153,7 @@ def cpu_reference_run(c, steps, warmup, threads=None):
         dt = time.perf_counter() - t0
         if s >= warmup:
             times.append(dt)
-    return times, kind, threads
+    return times, kind, threads, n_ref
 
 
 # ------------------------------------------------------------------------------ main
@@ -166,7 +175,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    tm, tn = c["N"] // c["bq"], c["N"] // c["bk"]
+    tm, tn = -(-c["N"] // c["bq"]), -(-c["N"] // c["bk"])  # ceil: ragged N has a partial last block
     kappa = max(1, min(tn, round(c["k_percent"] / 100.0 * tn)))
     cfg_out = {"workload": c["workload"], "B": c["B"], "H": c["H"], "N": c["N"], "d": c["d"], "bq": c["bq"],
                "bk": c["bk"], "k_percent": c["k_percent"], "kappa": kappa, "sparsity": 1 - kappa / tn,
@@ -177,11 +186,12 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        times, kind, cores = cpu_reference_run(c, args.steps, args.warmup)
+        times, kind, cores, n_ref = cpu_reference_run(c, args.steps, args.warmup)
         t = statistics.median(times)
-        val = 4.0 * c["N"] ** 2 * c["d"] / t / 1e12
+        val = 4.0 * n_ref ** 2 * c["d"] / t / 1e12
         sample = (f"1 of {c['B'] * c['H']} (b,h) heads per step: smooth_k + block_scores + hard_topk + "
-                  f"sla2_forward_blockwise<float>, SLA2_THREADS={cores}")
+                  f"sla2_forward_blockwise<float>, SLA2_THREADS={cores}"
+                  + (f", N={n_ref} (the reference rejects N={c['N']})" if n_ref != c["N"] else ""))
         line = {"metric": METRIC, "value": val, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg_out, "impl": "reference",
@@ -358,11 +368,12 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        times, kind, cores = cpu_reference_run(c, 1, 0)
+        times, kind, cores, n_ref = cpu_reference_run(c, 1, 0)
         t = statistics.median(times)
-        cpu = {"value": 4.0 * N ** 2 * d / t / 1e12, "unit": "TFLOPS", "cores": cores, "kind": kind,
+        cpu = {"value": 4.0 * n_ref ** 2 * d / t / 1e12, "unit": "TFLOPS", "cores": cores, "kind": kind,
                "sample": f"1 of {B * H} heads ({t:.2f} s): Tape::sla2_attention forward composition, "
-                         f"SLA2_THREADS={cores}", "ms_per_head": t * 1e3,
+                         f"SLA2_THREADS={cores}" + (f", N={n_ref} (the reference rejects N={N})" if n_ref != N else ""),
+               "ms_per_head": t * 1e3,
                "full_forward_ms_extrapolated": t * 1e3 * B * H}
 
     line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,

@@ -49,7 +49,11 @@ typedef enum { SLA2_F32 = 0, SLA2_BF16 = 1 } sla2_dtype;
 typedef enum { SLA2_QUANT_NONE = 0, SLA2_QUANT_INT8 = 1 } sla2_quant;
 
 typedef struct {
-    int64_t B, H, N, d; /* batch, heads, tokens (N % bq == N % bk == 0), head dim */
+    int64_t B, H, N, d; /* batch, heads, tokens, head dim. N % bq == N % bk == 0 as the reference
+                         * requires (attention.hpp:39-41), except on the bf16 non-QAT path, which
+                         * also takes a ragged N (e.g. Wan's 32760 / 75600): the last query / key
+                         * block is partial, pooled over its own rows, and keys past N are masked
+                         * (the oracle's sla2o_*_ragged extension). tm = ceil(N/bq), tn = ceil(N/bk). */
     int64_t bq, bk;     /* block sizes (AttentionInputs::bq/bk, attention.hpp:27-28) */
     double k_percent;   /* router budget, hard_topk (router.hpp:106-125); in (0, 100] */
     int32_t dtype;      /* sla2_dtype of q, k, v, out */

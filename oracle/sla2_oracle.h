@@ -77,7 +77,21 @@ size_t sla2o_topk_budget(double k_percent, size_t tn);
     int sla2o_attention_##S(const T* q, const T* k, const T* v, size_t n, size_t d, size_t bq,   \
                             size_t bk, const T* proj_q, const T* proj_k, const T* rho,           \
                             double k_percent, int quant, int smooth, T* out, uint8_t* mask,      \
-                            T* o_s, T* o_l, T* big_l);
+                            T* o_s, T* o_l, T* big_l);                                   \
+    /* RAGGED EXTENSION: n need not be divisible by bq / bk; the last   \
+     * query / key block is partial. Equal to the functions above when the blocks divide n. */ \
+    int sla2o_mean_pool_ragged_##S(const T* x, size_t rows, size_t cols, size_t block, T* out); \
+    int sla2o_block_scores_ragged_##S(const T* q, const T* k, size_t n, size_t d,               \
+                                      const T* proj_q, const T* proj_k, T tau, size_t bq,       \
+                                      size_t bk, T* pc);                                        \
+    int sla2o_forward_blockwise_ragged_##S(const T* q, const T* k, const T* v, size_t n,        \
+                                           size_t d, size_t bq, size_t bk, const uint8_t* mask, \
+                                           const T* rho, int quant, int smooth, T* out, T* o_s, \
+                                           T* o_l, T* big_l);                                   \
+    int sla2o_attention_ragged_##S(const T* q, const T* k, const T* v, size_t n, size_t d,      \
+                                   size_t bq, size_t bk, const T* proj_q, const T* proj_k,      \
+                                   const T* rho, double k_percent, int quant, int smooth,       \
+                                   T* out, uint8_t* mask, T* o_s, T* o_l, T* big_l);
 
 SLA2O_DECLARE(float, f)
 SLA2O_DECLARE(double, d)

@@ -31,15 +31,25 @@ void FN(sla2o_smooth_k)(const T* k, size_t rows, size_t cols, T* ktilde, T* mean
  * double), rows of a group added in ascending order, then (T)(acc / (ACC)block). */
 int FN(sla2o_mean_pool)(const T* x, size_t rows, size_t cols, size_t block, T* out) {
     if (block == 0 || rows % block != 0) return SLA2O_SHAPE;
-    const size_t out_rows = rows / block;
+    return FN(sla2o_mean_pool_ragged)(x, rows, cols, block, out);
+}
+
+/* RAGGED EXTENSION (not in the reference, which rejects rows % block != 0 at
+ * matrix.hpp:176-179): ceil(rows / block) groups, the last one averaging
+ * only its cnt = rows - g * block rows: (T)(acc / (ACC)cnt). Identical to mean_pool when
+ * block divides rows (same loop, cnt == block). */
+int FN(sla2o_mean_pool_ragged)(const T* x, size_t rows, size_t cols, size_t block, T* out) {
+    if (block == 0) return SLA2O_SHAPE;
+    const size_t out_rows = (rows + block - 1) / block;
     ACC* acc = (ACC*)malloc(sizeof(ACC) * (cols ? cols : 1));
     for (size_t g = 0; g < out_rows; ++g) {
+        const size_t cnt = rows - g * block < block ? rows - g * block : block;
         for (size_t c = 0; c < cols; ++c) acc[c] = (ACC)0;
-        for (size_t r = 0; r < block; ++r) {
+        for (size_t r = 0; r < cnt; ++r) {
             const T* in = x + (g * block + r) * cols;
             for (size_t c = 0; c < cols; ++c) acc[c] += (ACC)in[c];
         }
-        for (size_t c = 0; c < cols; ++c) out[g * cols + c] = (T)(acc[c] / (ACC)block);
+        for (size_t c = 0; c < cols; ++c) out[g * cols + c] = (T)(acc[c] / (ACC)cnt);
     }
     free(acc);
     return SLA2O_OK;
@@ -106,14 +116,23 @@ int FN(sla2o_block_scores)(const T* q, const T* k, size_t n, size_t d, const T* 
                            const T* proj_k, T tau, size_t bq, size_t bk, T* pc) {
     if (!(tau > (T)0)) return SLA2O_NUMERIC;
     if (bq == 0 || bk == 0 || n % bq || n % bk) return SLA2O_SHAPE;
-    const size_t tm = n / bq, tn = n / bk;
+    return FN(sla2o_block_scores_ragged)(q, k, n, d, proj_q, proj_k, tau, bq, bk, pc);
+}
+
+/* RAGGED EXTENSION of block_scores: tm = ceil(n/bq), tn = ceil(n/bk), partial last blocks pooled
+ * over their own rows (sla2o_mean_pool_ragged); everything after the pooling unchanged. */
+int FN(sla2o_block_scores_ragged)(const T* q, const T* k, size_t n, size_t d, const T* proj_q,
+                                  const T* proj_k, T tau, size_t bq, size_t bk, T* pc) {
+    if (!(tau > (T)0)) return SLA2O_NUMERIC;
+    if (bq == 0 || bk == 0 || n == 0) return SLA2O_SHAPE;
+    const size_t tm = (n + bq - 1) / bq, tn = (n + bk - 1) / bk;
     T* qbar = (T*)malloc(sizeof(T) * tm * d);
     T* kbar = (T*)malloc(sizeof(T) * tn * d);
     T* qp = (T*)malloc(sizeof(T) * tm * d);
     T* kp = (T*)malloc(sizeof(T) * tn * d);
     T* sc = (T*)malloc(sizeof(T) * tm * tn);
-    FN(sla2o_mean_pool)(q, n, d, bq, qbar);
-    FN(sla2o_mean_pool)(k, n, d, bk, kbar);
+    FN(sla2o_mean_pool_ragged)(q, n, d, bq, qbar);
+    FN(sla2o_mean_pool_ragged)(k, n, d, bk, kbar);
     FN(sla2o_matmul)(qbar, tm, d, proj_q, d, d, 0, qp);
     FN(sla2o_matmul)(kbar, tn, d, proj_k, d, d, 0, kp);
     FN(sla2o_matmul)(qp, tm, d, kp, tn, d, 1, sc);
@@ -227,8 +246,10 @@ typedef struct {
 
 /* attention.hpp:372-394 block_scores_qk and 396-415 block_product_pv are inlined below. */
 static void FN(oracle_fwd_qblock)(const FN(oracle_fwd_ctx) * c, size_t i) {
-    const size_t d = c->d, bq = c->bq, bk = c->bk, tn = c->tn;
-    const size_t r0 = i * bq;
+    const size_t d = c->d, bk = c->bk, tn = c->tn;
+    const size_t r0 = i * c->bq;
+    /* rows of this query block: bq, or fewer for the ragged tail (n % bq != 0) */
+    const size_t bq = c->n - r0 < c->bq ? c->n - r0 : c->bq;
     const T inv_sqrt_d = (T)1 / SQRT((T)d);
     T* m_run = (T*)malloc(sizeof(T) * bq);
     T* l_run = (T*)calloc(bq, sizeof(T));
@@ -256,34 +277,37 @@ static void FN(oracle_fwd_qblock)(const FN(oracle_fwd_ctx) * c, size_t i) {
             }
         }
         if (w <= (T)0) continue;
+        /* keys of this block: bk, or fewer for the ragged tail; S is bq x kc, kept packed with
+         * row stride kc (the reference's layout when kc == bk) */
+        const size_t kc = c->n - j * bk < bk ? c->n - j * bk : bk;
         /* S = Q_i K~_j^T / sqrt(d) (attention.hpp:372-394) */
         if (c->quant) {
             T sa, sb;
             FN(sla2o_quantize)(c->q + r0 * d, bq * d, qa, &sa);
-            FN(sla2o_quantize)(c->ktilde + j * bk * d, bk * d, qb, &sb);
-            FN(sla2o_quantized_product)(qa, bq, d, sa, qb, bk, d, sb, 1, s);
-            FN(sla2o_scale)(s, bq * bk, inv_sqrt_d, s);
+            FN(sla2o_quantize)(c->ktilde + j * bk * d, kc * d, qb, &sb);
+            FN(sla2o_quantized_product)(qa, bq, d, sa, qb, kc, d, sb, 1, s);
+            FN(sla2o_scale)(s, bq * kc, inv_sqrt_d, s);
         } else {
             for (size_t r = 0; r < bq; ++r) {
                 const T* qrow = c->q + (r0 + r) * d;
-                for (size_t t = 0; t < bk; ++t) {
+                for (size_t t = 0; t < kc; ++t) {
                     const T* krow = c->ktilde + (j * bk + t) * d;
                     T acc = (T)0;
                     for (size_t f = 0; f < d; ++f) acc += qrow[f] * krow[f];
-                    s[r * bk + t] = acc * inv_sqrt_d;
+                    s[r * kc + t] = acc * inv_sqrt_d;
                 }
             }
         }
         /* online softmax (attention.hpp:506-523) */
         for (size_t r = 0; r < bq; ++r) {
-            T mx = s[r * bk];
-            for (size_t t = 1; t < bk; ++t) mx = (mx < s[r * bk + t]) ? s[r * bk + t] : mx;
+            T mx = s[r * kc];
+            for (size_t t = 1; t < kc; ++t) mx = (mx < s[r * kc + t]) ? s[r * kc + t] : mx;
             const T m_new = (m_run[r] < mx) ? mx : m_run[r];
             const T rescale = EXP(m_run[r] - m_new);
             T rs = (T)0;
-            for (size_t t = 0; t < bk; ++t) {
-                p[r * bk + t] = EXP(s[r * bk + t] - m_new);
-                rs += p[r * bk + t];
+            for (size_t t = 0; t < kc; ++t) {
+                p[r * kc + t] = EXP(s[r * kc + t] - m_new);
+                rs += p[r * kc + t];
             }
             l_run[r] = rescale * l_run[r] + w * rs;
             T* orow = o_acc + r * d;
@@ -293,15 +317,15 @@ static void FN(oracle_fwd_qblock)(const FN(oracle_fwd_ctx) * c, size_t i) {
         /* PV (attention.hpp:396-415) */
         if (c->quant) {
             T sp, sv;
-            FN(sla2o_quantize)(p, bq * bk, qpc, &sp);
-            FN(sla2o_quantize)(c->v + j * bk * d, bk * d, qv, &sv);
-            FN(sla2o_quantized_product)(qpc, bq, bk, sp, qv, bk, d, sv, 0, pv);
+            FN(sla2o_quantize)(p, bq * kc, qpc, &sp);
+            FN(sla2o_quantize)(c->v + j * bk * d, kc * d, qv, &sv);
+            FN(sla2o_quantized_product)(qpc, bq, kc, sp, qv, kc, d, sv, 0, pv);
         } else {
             for (size_t r = 0; r < bq * d; ++r) pv[r] = (T)0;
             for (size_t r = 0; r < bq; ++r) {
                 T* orow = pv + r * d;
-                for (size_t t = 0; t < bk; ++t) {
-                    const T prt = p[r * bk + t];
+                for (size_t t = 0; t < kc; ++t) {
+                    const T prt = p[r * kc + t];
                     const T* vrow = c->v + (j * bk + t) * d;
                     for (size_t cc = 0; cc < d; ++cc) orow[cc] += prt * vrow[cc];
                 }
@@ -361,7 +385,18 @@ int FN(sla2o_forward_blockwise)(const T* q, const T* k, const T* v, size_t n, si
                                 int smooth, T* out, T* o_s, T* o_l, T* big_l) {
     /* validation (attention.hpp:427-447, AttentionInputs::validate 36-43) */
     if (bq == 0 || bk == 0 || n % bq || n % bk) return SLA2O_SHAPE;
-    const size_t tm = n / bq, tn = n / bk;
+    return FN(sla2o_forward_blockwise_ragged)(q, k, v, n, d, bq, bk, mask, rho, quant, smooth, out,
+                                              o_s, o_l, big_l);
+}
+
+/* RAGGED EXTENSION of sla2_forward_blockwise: tm = ceil(n/bq), tn = ceil(n/bk); the tail query
+ * block has n - (tm-1) bq rows, the tail key block n - (tn-1) bk keys (h_j, z_j, S, P and PV over
+ * those keys only). Same code path as forward_blockwise, which it equals when the blocks divide n. */
+int FN(sla2o_forward_blockwise_ragged)(const T* q, const T* k, const T* v, size_t n, size_t d,
+                                       size_t bq, size_t bk, const uint8_t* mask, const T* rho,
+                                       int quant, int smooth, T* out, T* o_s, T* o_l, T* big_l) {
+    if (bq == 0 || bk == 0 || n == 0) return SLA2O_SHAPE;
+    const size_t tm = (n + bq - 1) / bq, tn = (n + bk - 1) / bk;
     for (size_t i = 0; i < tm; ++i) {
         int any = 0;
         for (size_t j = 0; j < tn; ++j) any |= (mask[i * tn + j] != 0);
@@ -379,7 +414,8 @@ int FN(sla2o_forward_blockwise)(const T* q, const T* k, const T* v, size_t n, si
     T* h = (T*)calloc(tn * d * d, sizeof(T));
     T* z = (T*)calloc(tn * d, sizeof(T));
     for (size_t j = 0; j < tn; ++j) {
-        for (size_t t = 0; t < bk; ++t) {
+        const size_t kc = n - j * bk < bk ? n - j * bk : bk;
+        for (size_t t = 0; t < kc; ++t) {
             const T* kp = k_phi + (j * bk + t) * d;
             const T* vr = v + (j * bk + t) * d;
             for (size_t f = 0; f < d; ++f) {
@@ -511,6 +547,28 @@ int FN(sla2o_attention)(const T* q, const T* k, const T* v, size_t n, size_t d, 
     if (rc == SLA2O_OK)
         rc = FN(sla2o_forward_blockwise)(q, k, v, n, d, bq, bk, mask, rho, quant, smooth, out, o_s,
                                          o_l, big_l);
+    free(kt); free(mean); free(pc);
+    return rc;
+}
+
+/* RAGGED EXTENSION of the tape.hpp:263-272 composition for n not divisible by the blocks:
+ * smooth_k (colmean over all n rows) -> block_scores_ragged -> hard_topk -> forward_blockwise_ragged. */
+int FN(sla2o_attention_ragged)(const T* q, const T* k, const T* v, size_t n, size_t d, size_t bq,
+                               size_t bk, const T* proj_q, const T* proj_k, const T* rho,
+                               double k_percent, int quant, int smooth, T* out, uint8_t* mask,
+                               T* o_s, T* o_l, T* big_l) {
+    if (bq == 0 || bk == 0 || n == 0) return SLA2O_SHAPE;
+    const size_t tm = (n + bq - 1) / bq, tn = (n + bk - 1) / bk;
+    T* kt = (T*)malloc(sizeof(T) * n * d);
+    T* mean = (T*)malloc(sizeof(T) * d);
+    if (smooth) FN(sla2o_smooth_k)(k, n, d, kt, mean);
+    else memcpy(kt, k, sizeof(T) * n * d);
+    T* pc = (T*)malloc(sizeof(T) * tm * tn);
+    int rc = FN(sla2o_block_scores_ragged)(q, kt, n, d, proj_q, proj_k, (T)0.1, bq, bk, pc);
+    if (rc == SLA2O_OK) rc = FN(sla2o_hard_topk)(pc, tm, tn, k_percent, mask, NULL);
+    if (rc == SLA2O_OK)
+        rc = FN(sla2o_forward_blockwise_ragged)(q, k, v, n, d, bq, bk, mask, rho, quant, smooth, out,
+                                                o_s, o_l, big_l);
     free(kt); free(mean); free(pc);
     return rc;
 }

@@ -169,11 +169,11 @@ class FwdParams:
 
     @property
     def tm(self):
-        return self.N // self.bq
+        return -(-self.N // self.bq)  # ceil: a ragged N has a partial last block (bf16 path)
 
     @property
     def tn(self):
-        return self.N // self.bk
+        return -(-self.N // self.bk)
 
     @property
     def kappa(self):

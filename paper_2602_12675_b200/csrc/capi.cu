@@ -92,15 +92,16 @@ struct MapKey {
     uint64_t rows, cols;
     uint32_t box_x, box_y, elem;
     bool swz;
+    uint64_t heads;  // 0: 2-D map; else 3-D [heads][rows][cols]
     bool operator==(const MapKey& o) const {
         return ptr == o.ptr && rows == o.rows && cols == o.cols && box_x == o.box_x && box_y == o.box_y &&
-               elem == o.elem && swz == o.swz;
+               elem == o.elem && swz == o.swz && heads == o.heads;
     }
 };
 struct MapKeyHash {
     size_t operator()(const MapKey& k) const {
         return std::hash<const void*>()(k.ptr) ^ (k.rows * 1315423911u) ^ (k.cols << 7) ^ (k.box_x << 17) ^
-               (k.box_y << 23) ^ k.elem;
+               (k.box_y << 23) ^ k.elem ^ (k.heads << 29);
     }
 };
 
@@ -110,7 +111,7 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, u
               uint32_t elem, bool swizzle128 = true) {
     static std::mutex mu;
     static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-    MapKey key{ptr, rows, cols, box_x, box_y, elem, swizzle128};
+    MapKey key{ptr, rows, cols, box_x, box_y, elem, swizzle128, 0};
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -138,6 +139,41 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, u
     return true;
 }
 
+// 3-D [heads][rows][cols] tensor (rows = N per head), box (box_x cols, box_y rows, 1 head):
+// a box never crosses a head, so a ragged N (N % box_y != 0) reads zeros past the head's last
+// row and a store drops them.
+bool make_map3(CUtensorMap* out, const void* ptr, uint64_t heads, uint64_t rows, uint64_t cols, uint32_t box_x,
+               uint32_t box_y, uint32_t elem, bool swizzle128 = true) {
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    MapKey key{ptr, rows, cols, box_x, box_y, elem, swizzle128, heads};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *out = it->second;
+            return true;
+        }
+    }
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {cols, rows, heads};
+    cuuint64_t strides[2] = {cols * elem, rows * cols * elem};
+    cuuint32_t box[3] = {box_x, box_y, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = elem == 2   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                   : elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                               : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    CUresult r = fn(out, dt, 3, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, *out);
+    return true;
+}
+
 // ---------------------------------------------------------------- geometry + workspace
 struct Geo {
     int64_t B, H, BH, N, d, bq, bk, tm, tn, kappa;
@@ -154,8 +190,9 @@ Geo geometry(const sla2_fwd_params* p) {
     g.d = p->d;
     g.bq = p->bq;
     g.bk = p->bk;
-    g.tm = p->bq ? p->N / p->bq : 0;
-    g.tn = p->bk ? p->N / p->bk : 0;
+    // ceil: a ragged N (bf16 path) has a partial last query / key block
+    g.tm = p->bq ? (p->N + p->bq - 1) / p->bq : 0;
+    g.tn = p->bk ? (p->N + p->bk - 1) / p->bk : 0;
     g.kappa = sla2_topk_budget(p->k_percent, g.tn);
     g.bf16 = p->dtype == SLA2_BF16;
     g.quant = p->quant == SLA2_QUANT_INT8;
@@ -229,11 +266,15 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     return c.off + 256;
 }
 
-// TMA view of K for the serial column-mean kernel: [B*H*N][d] elements, 32 x 256 boxes.
+// TMA view of K for the serial column-mean kernels, boxes of 128 rows x one 128-byte segment:
+// bf16 3-D [BH][N][d] (colmean_tr_kernel, any N: rows past N read as zeros, which leave the
+// serial sum unchanged), fp32 2-D [B*H*N][d] (colmean_tma_kernel, N % 128 == 0).
 const CUtensorMap* colmean_map(CUtensorMap* m, const void* k, bool bf16, int64_t BH, int64_t N, int64_t d) {
-    const uint32_t cols = bf16 ? 64 : 32;  // one 128-byte segment per row
-    if (N % 128 != 0 || d % cols != 0) return nullptr;
-    return make_map(m, k, (uint64_t)(BH * N), (uint64_t)d, cols, 128, bf16 ? 2 : 4, false) ? m : nullptr;
+    const uint32_t cols = bf16 ? 64 : 32;
+    if (d % cols != 0) return nullptr;
+    if (bf16) return make_map3(m, k, (uint64_t)BH, (uint64_t)N, (uint64_t)d, cols, 128, 2, false) ? m : nullptr;
+    if (N % 128 != 0) return nullptr;
+    return make_map(m, k, (uint64_t)(BH * N), (uint64_t)d, cols, 128, 4, false) ? m : nullptr;
 }
 
 float inv_sqrt(int64_t d) {
@@ -309,8 +350,12 @@ static sla2_status check_common(const sla2_fwd_params* p) {
     if (!p) return fail(SLA2_CONTRACT_ERROR, "params is NULL");
     if (p->B <= 0 || p->H <= 0 || p->N <= 0 || p->d <= 0)
         return fail(SLA2_SHAPE_ERROR, "B, H, N, d must be positive");
-    if (p->bq <= 0 || p->bk <= 0 || p->N % p->bq != 0 || p->N % p->bk != 0)
-        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");  // attention.hpp:39-41
+    if (p->bq <= 0 || p->bk <= 0) return fail(SLA2_SHAPE_ERROR, "block sizes must be positive");
+    if ((p->N % p->bq != 0 || p->N % p->bk != 0) &&
+        !(p->dtype == SLA2_BF16 && p->quant == SLA2_QUANT_NONE && p->d == 128 && p->bq == 128 && p->bk == 64))
+        // the reference's rule (attention.hpp:39-41); the ragged extension (partial last blocks,
+        // SURVEY.md 8f item 2) exists on the bf16 tcgen05 path only
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
     if (!(p->k_percent > 0.0 && p->k_percent <= 100.0))
         return fail(SLA2_SHAPE_ERROR, "hard_topk: k_percent must be in (0, 100]");  // router.hpp:108-110
     if (!(p->tau > 0.0f)) return fail(SLA2_NUMERIC_ERROR, "RouterParams: tau must be positive");  // router.hpp:32
@@ -368,10 +413,12 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     CUtensorMap mq, mk, mv, mphi, mht, mpq, mo;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
     if (g.bf16) {
-        if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
-            !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mphi, w.phik, rows, g.d, 64, 64, 2) ||
+        // per-token tensors as 3-D [BH][N][d] maps (ragged N safe); Htot 2-D
+        const uint64_t BH = (uint64_t)g.BH, N = (uint64_t)g.N;
+        if (!make_map3(&mq, q, BH, N, g.d, 64, 64, 2) || !make_map3(&mk, k, BH, N, g.d, 64, 64, 2) ||
+            !make_map3(&mv, v, BH, N, g.d, 64, 64, 2) || !make_map3(&mphi, w.phik, BH, N, g.d, 64, 64, 2) ||
             !make_map(&mht, w.htot16, (uint64_t)(g.BH * g.d), g.d, 64, 128, 2) ||
-            (w.phiq && !make_map(&mpq, w.phiq, rows, g.d, 64, 64, 2)) || !make_map(&mo, out, rows, g.d, 64, 64, 2))
+            (w.phiq && !make_map3(&mpq, w.phiq, BH, N, g.d, 64, 64, 2)) || !make_map3(&mo, out, BH, N, g.d, 64, 64, 2))
             return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (pointers must be 16-byte aligned)");
         if (w.phiq && !plan.phiq_ready) SLA2_CUDA_TRY(launch_phiq(q, w.phiq, (int64_t)rows, st, &g_launches));
     }
@@ -495,6 +542,14 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             qa.vct = w.vct;
             qa.vs = w.vs;
             SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+            // the INT8 kernel addresses its bf16 tiles with 2-D [B*H*N][d] maps (N divisible)
+            CUtensorMap mq2, mv2, mphi2;
+            if (!make_map(&mq2, q, rows, g.d, 64, 64, 2) || !make_map(&mv2, v, rows, g.d, 64, 64, 2) ||
+                !make_map(&mphi2, w.phik, rows, g.d, 64, 64, 2))
+                return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+            sa.tm_q = &mq2;
+            sa.tm_v = &mv2;
+            sa.tm_phik = &mphi2;
             CUtensorMap mqc, mkc, mvc;
             if (!make_map(&mqc, w.qc, rows, g.d, 128, 128, 1) || !make_map(&mkc, w.kc, rows, g.d, 128, 64, 1) ||
                 !make_map(&mvc, w.vct, rows, g.d, 128, 64, 1))
@@ -707,8 +762,10 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
     CUtensorMap mq, mk, mv;
     const uint64_t rows = (uint64_t)(g.BH * g.N);
     CUtensorMap mo;
-    if (!make_map(&mq, q, rows, g.d, 64, 64, 2) || !make_map(&mk, k, rows, g.d, 64, 64, 2) ||
-        !make_map(&mv, v, rows, g.d, 64, 64, 2) || !make_map(&mo, out, rows, g.d, 64, 64, 2))
+    (void)rows;
+    const uint64_t BH = (uint64_t)g.BH, N = (uint64_t)g.N;
+    if (!make_map3(&mq, q, BH, N, g.d, 64, 64, 2) || !make_map3(&mk, k, BH, N, g.d, 64, 64, 2) ||
+        !make_map3(&mv, v, BH, N, g.d, 64, 64, 2) || !make_map3(&mo, out, BH, N, g.d, 64, 64, 2))
         return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
     SparseLaunch sa{};
     sa.B = g.B;

@@ -107,9 +107,10 @@ __global__ void __launch_bounds__(128) phik_kernel(const InT* __restrict__ k, co
 // 16 lanes per row, 8 features (one 16-byte load / store) per lane.
 __global__ void __launch_bounds__(256) phiq_kernel(const __nv_bfloat16* __restrict__ q,
                                                    __nv_bfloat16* __restrict__ phiq, int64_t rows) {
-    const int64_t row = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
+    const int64_t row0 = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
     const int sub = threadIdx.x & 15;
-    if (row >= rows) return;  // rows is a multiple of 16 (N % 128 == 0): whole half-warps exit
+    const bool live = row0 < rows;  // the shuffles below need every lane of the warp
+    const int64_t row = live ? row0 : rows - 1;
     const uint4 w = *reinterpret_cast<const uint4*>(q + row * 128 + sub * 8);
     const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
     float x[8];
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256) phiq_kernel(const __nv_bfloat16* __restri
     r.y = pack_bf16(x[2] * inv, x[3] * inv);
     r.z = pack_bf16(x[4] * inv, x[5] * inv);
     r.w = pack_bf16(x[6] * inv, x[7] * inv);
-    *reinterpret_cast<uint4*>(phiq + row * 128 + sub * 8) = r;
+    if (live) *reinterpret_cast<uint4*>(phiq + row * 128 + sub * 8) = r;
 }
 
 cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(192, 1)
     const int chunk = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tn = N / BK;
+    const int tn = (N + BK - 1) / BK;
     const int j0 = chunk * per;
     const int nblk = min(per, tn - j0);
     if (threadIdx.x == 0) {
@@ -287,12 +288,12 @@ __global__ void __launch_bounds__(192, 1)
             for (int b = 0; b < nblk; ++b) {
                 const int s = b % NS;
                 if (b >= NS) mbar_wait(&empty[s], ((b / NS) - 1) & 1);
-                const int row = (int)(bh * N + (int64_t)(j0 + b) * BK);
+                const int row = (j0 + b) * BK, hz = (int)bh;  // 3-D maps: rows past N read as zeros
                 mbar_arrive_expect_tx(&full[s], 2 * TILE);
-                tma_load_2d(sK(s), &tmK, 0, row, &full[s]);
-                tma_load_2d(sK(s) + 8192, &tmK, 64, row, &full[s]);
-                tma_load_2d(sV(s), &tmV, 0, row, &full[s]);
-                tma_load_2d(sV(s) + 8192, &tmV, 64, row, &full[s]);
+                tma_load_3d(sK(s), &tmK, 0, row, hz, &full[s]);
+                tma_load_3d(sK(s) + 8192, &tmK, 64, row, hz, &full[s]);
+                tma_load_3d(sV(s), &tmV, 0, row, hz, &full[s]);
+                tma_load_3d(sV(s) + 8192, &tmV, 64, row, hz, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -314,8 +315,8 @@ __global__ void __launch_bounds__(192, 1)
     } else {
         // phi(K~): warp g = warp - 2 owns rows 16g .. 16g + 15; lane l owns features 4l .. 4l + 3
         const int g = warp - 2;
-        float m[4];
-        {
+        float m[4] = {0.f, 0.f, 0.f, 0.f};  // mu == nullptr: phi of the raw K (smooth = 0)
+        if (mu) {
             const float4 t = *reinterpret_cast<const float4*>(mu + bh * D + lane * 4);
             m[0] = t.x;
             m[1] = t.y;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&full[s], (b / NS) & 1);
             const uint32_t kb = smem_u32(sK(s));
             const int64_t grow0 = bh * N + (int64_t)(j0 + b) * BK;
+            const int cnt = min(BK, N - (j0 + b) * BK);  // keys of this block (ragged tail: fewer)
             float z[4] = {0.f, 0.f, 0.f, 0.f};
             constexpr int U = 4;
             for (int r0 = g * 16; r0 < g * 16 + 16; r0 += U) {
@@ -371,10 +373,12 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const float inv = __fdividef(1.0f, sum[u]);
-                    const uint32_t w0 = pack_bf16(xs[u][0] * inv, xs[u][1] * inv);
-                    const uint32_t w1 = pack_bf16(xs[u][2] * inv, xs[u][3] * inv);
+                    uint32_t w0 = pack_bf16(xs[u][0] * inv, xs[u][1] * inv);
+                    uint32_t w1 = pack_bf16(xs[u][2] * inv, xs[u][3] * inv);
+                    if (r0 + u >= cnt) w0 = w1 = 0u;  // past N: no key, phi = 0 (adds nothing to Htot)
                     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr[u]), "r"(w0), "r"(w1) : "memory");
-                    *reinterpret_cast<uint2*>(phik + (grow0 + r0 + u) * D + lane * 4) = make_uint2(w0, w1);
+                    if (r0 + u < cnt)
+                        *reinterpret_cast<uint2*>(phik + (grow0 + r0 + u) * D + lane * 4) = make_uint2(w0, w1);
                     z[0] += __uint_as_float(w0 << 16);
                     z[1] += __uint_as_float(w0 & 0xffff0000u);
                     z[2] += __uint_as_float(w1 << 16);
@@ -582,8 +586,9 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * 4 + warp;
     const int64_t bh = blockIdx.y;
-    const uint32_t blk_bytes = (uint32_t)bk * D * sizeof(T);
-    T* tile = reinterpret_cast<T*>(kps + (size_t)warp * blk_bytes);
+    const int cnt = min(bk, N - j * bk);  // rows of this key block (ragged tail: fewer)
+    const uint32_t blk_bytes = (uint32_t)(cnt > 0 ? cnt : 0) * D * sizeof(T);  // bytes copied
+    T* tile = reinterpret_cast<T*>(kps + (size_t)warp * bk * D * sizeof(T));      // full-block slots
     const int64_t row0 = bh * N + (int64_t)j * bk;
     // the warp's whole key block (bk rows, contiguous in global) in one bulk copy
     if (lane == 0) {
@@ -618,12 +623,14 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
         float xs[U][4], mx[U], sum[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            kp_vec<T>::load(tr + (r0 + u) * D, xs[u]);
+            const bool real = r0 + u < cnt;
+            if (real) kp_vec<T>::load(tr + (r0 + u) * D, xs[u]);
+            else xs[u][0] = xs[u][1] = xs[u][2] = xs[u][3] = 0.0f;
             mx[u] = -INFINITY;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (mu) xs[u][e] = __fsub_rn(xs[u][e], m[e]);
-                if (POOL) pool[e] = __dadd_rn(pool[e], (double)xs[u][e]);  // rows in order (exact pooling)
+                if (POOL && real) pool[e] = __dadd_rn(pool[e], (double)xs[u][e]);  // rows in order (exact pooling)
                 mx[u] = fmaxf(mx[u], xs[u][e]);
             }
         }
@@ -649,6 +656,7 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
             const float inv = __fdividef(1.0f, sum[u]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) xs[u][e] *= inv;
+            if (r0 + u >= cnt) continue;  // ragged tail: no key past N
             kp_vec<T>::store(pr + (int64_t)(r0 + u) * D, xs[u]);  // rounds xs to the stored values
 #pragma unroll
             for (int e = 0; e < 4; ++e) z[e] += xs[u][e];
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
     if (POOL) {
         float kv[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) kv[e] = __double2float_rn(__ddiv_rn(pool[e], (double)bk));
+        for (int e = 0; e < 4; ++e) kv[e] = __double2float_rn(__ddiv_rn(pool[e], (double)cnt));
         *reinterpret_cast<float4*>(kb) = make_float4(kv[0], kv[1], kv[2], kv[3]);
     }
     if (PHI) *reinterpret_cast<float4*>(zb) = make_float4(z[0], z[1], z[2], z[3]);
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(128) kprep_kernel(const T* __restrict__ k, con
 
 template <bool POOL, bool PHI>
 static void kprep_go(const LinearLaunch& a, float* kbar, cudaStream_t st) {
-    const int tn = a.N / a.bk;
+    const int tn = (a.N + a.bk - 1) / a.bk;
     const dim3 g((tn + 3) / 4, (unsigned)a.BH);
     const size_t smem = (size_t)4 * a.bk * 128 * (a.bf16 ? 2 : 4);
     if (a.bf16) {
@@ -699,9 +707,9 @@ cudaError_t launch_kphi(const LinearLaunch& a, cudaStream_t st, int* launches) {
 }
 
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches) {
-    const int tn = a.N / a.bk;
+    const int tn = (a.N + a.bk - 1) / a.bk;
     dim3 g1(tn, (unsigned)a.BH);
-    if (a.bf16 && a.tm_k && !a.phik_ready && a.mu) {
+    if (a.bf16 && a.tm_k && !a.phik_ready) {
         // phi(K~), z_j and the Htot partials in one pass over K and V
         static bool attr_f = false;
         if (!attr_f) {
@@ -735,7 +743,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
     const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
     lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
         a.hpart, a.zblk, a.htot, a.bf16 ? (__nv_bfloat16*)a.htot16 : nullptr, a.ztot, a.nchunk, a.d, tn);
-    *launches += (a.phik_ready || (a.bf16 && a.tm_k && a.mu)) ? 2 : 3;
+    *launches += (a.phik_ready || (a.bf16 && a.tm_k)) ? 2 : 3;
     return cudaGetLastError();
 }
 

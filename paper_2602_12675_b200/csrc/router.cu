@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__
     const int cg = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int warp = threadIdx.x >> 5;
-    const int nchunk = N / ROWS;  // N % 128 == 0 is checked by the launcher
+    const int nchunk = (N + ROWS - 1) / ROWS;  // rows past N (ragged tail) arrive as zeros
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__
                 const int s = c % NST;
                 if (c >= NST) mbar_wait(&empty[s], ((c / NST) - 1) & 1);
                 mbar_arrive_expect_tx(&full[s], TILE);
-                tma_load_2d(ring + s * TILE, &tmK, cg * COLS, (int)(bh * N + (int64_t)c * ROWS), &full[s]);
+                tma_load_3d(ring + s * TILE, &tmK, cg * COLS, c * ROWS, (int)bh, &full[s]);
             }
         }
         return;
@@ -338,29 +338,31 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
     const int g = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int h = (int)(bh % H);
-    // stage the whole [block x d] slab with independent 16-byte loads (one DRAM round trip)
+    const int nblk = (N + block - 1) / block;
+    const int cnt = min(block, N - g * block);  // rows of this block (ragged tail: fewer)
+    // stage the whole [cnt x d] slab with independent 16-byte loads (one DRAM round trip)
     {
         const T* src = x + (bh * N + (int64_t)g * block) * d;
         if (((d * sizeof(T)) & 15) == 0) {
             const uint4* src4 = reinterpret_cast<const uint4*>(src);
             uint4* dst4 = reinterpret_cast<uint4*>(tile);
-            const int n16 = (int)((size_t)block * d * sizeof(T) / 16);
+            const int n16 = (int)((size_t)cnt * d * sizeof(T) / 16);
             for (int e = c; e < n16; e += blockDim.x) dst4[e] = src4[e];
         } else {
-            for (int e = c; e < block * d; e += blockDim.x) tile[e] = src[e];
+            for (int e = c; e < cnt * d; e += blockDim.x) tile[e] = src[e];
         }
     }
     __syncthreads();
     const float m = mu ? mu[bh * d + c] : 0.0f;
     double acc = 0.0;
-    for (int r = 0; r < block; ++r) {
+    for (int r = 0; r < cnt; ++r) {
         float v = to_f32(tile[r * d + c]);
         if (mu) v = __fsub_rn(v, m);
         acc = __dadd_rn(acc, (double)v);
     }
-    sbar[c] = __double2float_rn(__ddiv_rn(acc, (double)block));
+    sbar[c] = __double2float_rn(__ddiv_rn(acc, (double)cnt));
     if (xbar_out) {  // pooled rows only; the projection runs in project_kernel
-        xbar_out[(bh * (N / block) + g) * d + c] = sbar[c];
+        xbar_out[(bh * nblk + g) * d + c] = sbar[c];
         return;
     }
     __syncthreads();
@@ -375,7 +377,7 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
         for (int u = 0; u < 16; ++u) o = __fadd_rn(o, __fmul_rn(sbar[f + u], pv[u]));
     }
     for (; f < d; ++f) o = __fadd_rn(o, __fmul_rn(sbar[f], P[(int64_t)f * d + c]));
-    xp[(bh * (N / block) + g) * d + c] = o;
+    xp[(bh * nblk + g) * d + c] = o;
 }
 
 // xp[g][c] = sum_f xbar[g][f] * P[f][c] (matrix.hpp:121-132: i-k-j order, one serial chain
@@ -876,7 +878,7 @@ template <typename T>
 static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, int N, int d, cudaStream_t st,
                       int* launches) {
     constexpr int COLS = 128 / sizeof(T);
-    if (sizeof(T) == 2 && tmk && N % cmt::ROWS == 0 && d % cmt::COLS == 0) {
+    if (sizeof(T) == 2 && tmk && d % cmt::COLS == 0) {
         const int smem = (cmt::NST + cmt::NTS) * cmt::TILE;
         static bool attr_t = false;
         if (!attr_t) {
@@ -910,11 +912,11 @@ static bool launch_pool_project(const T* x, const float* mu, const float* proj, 
     const size_t smem = ((d * sizeof(float) + 15) & ~size_t(15)) + (size_t)block * d * sizeof(T);
     if (smem > 48 * 1024) cudaFuncSetAttribute(pool_project_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const bool split = scratch && (d % 16 == 0) && ((size_t)d * d + 32 * d) * 4 <= 200 * 1024;
-    pool_project_kernel<T><<<dim3(N / block, BH), d, smem, st>>>(x, mu, proj, xp, N, d, H, block,
+    pool_project_kernel<T><<<dim3((N + block - 1) / block, BH), d, smem, st>>>(x, mu, proj, xp, N, d, H, block,
                                                                   split ? scratch : nullptr);
     ++*launches;
     if (split) {
-        const int nrows = N / block;
+        const int nrows = (N + block - 1) / block;
         const size_t ps = ((size_t)d * d + 32 * d) * 4;
         cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
         project_kernel<<<dim3((nrows + 31) / 32, BH), 256, ps, st>>>(scratch, proj, xp, nrows, d, H, want_t ? 1 : 0);
@@ -969,7 +971,7 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
 template <typename T>
 static cudaError_t router_back_t(const RouterLaunch& a, cudaStream_t st, int* launches) {
     const int BH = (int)(a.B * a.H);
-    const int tm = a.N / a.bq, tn = a.N / a.bk;
+    const int tm = (a.N + a.bq - 1) / a.bq, tn = (a.N + a.bk - 1) / a.bk;
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
     const size_t rsm = router_rows_smem(tn, a.d);

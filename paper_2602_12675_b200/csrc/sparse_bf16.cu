@@ -83,6 +83,7 @@ struct SparseBf16Params {
     float* o_l;
     float* big_l;
     int N, H, tm, tn;
+    int last_valid;  // keys in the last key block (BK unless N % BK != 0)
     float scale_log2;
     float inv_sqrt_d;
     int dense;
@@ -223,12 +224,12 @@ __global__ void __launch_bounds__(256, 1)
             tma_prefetch_desc(&tmQ);
             tma_prefetch_desc(&tmK);
             const uint64_t pol_keep = policy_evict_last();
-            const int qrow = (int)(bh * p.N + (int64_t)i * BQ);
+            const int qrow = i * BQ, hz = (int)bh;  // 3-D maps: (column, row in head, head)
             mbar_arrive_expect_tx(&bar_q, Q_BYTES);
-            tma_load_2d(sQ, &tmQ, 0, qrow, &bar_q);
-            tma_load_2d(sQ + 8192, &tmQ, 0, qrow + 64, &bar_q);
-            tma_load_2d(sQ + 16384, &tmQ, 64, qrow, &bar_q);
-            tma_load_2d(sQ + 24576, &tmQ, 64, qrow + 64, &bar_q);
+            tma_load_3d(sQ, &tmQ, 0, qrow, hz, &bar_q);
+            tma_load_3d(sQ + 8192, &tmQ, 0, qrow + 64, hz, &bar_q);
+            tma_load_3d(sQ + 16384, &tmQ, 64, qrow, hz, &bar_q);
+            tma_load_3d(sQ + 24576, &tmQ, 64, qrow + 64, hz, &bar_q);
             for (int n = 0; n < npair; ++n) {
                 const int s = n % NKP;
                 if (n >= NKP) mbar_wait(&bar_k_empty[s], ((n / NKP) - 1) & 1);
@@ -237,10 +238,10 @@ __global__ void __launch_bounds__(256, 1)
                 if (n == npair - 1) SLA2_TR(55);
                 mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
                 for (int b = 0; b < cnt; ++b) {
-                    const int krow = (int)(bh * p.N + (int64_t)kblock(2 * n + b) * BK);
+                    const int krow = kblock(2 * n + b) * BK;
                     // rows b*64.. of each 128-row k-atom: [cols 0-63] then [cols 64-127]
-                    tma_load_2d_hint(sKp(s) + b * 8192, &tmK, 0, krow, &bar_k_full[s], pol_keep);
-                    tma_load_2d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, &bar_k_full[s], pol_keep);
+                    tma_load_3d_hint(sKp(s) + b * 8192, &tmK, 0, krow, hz, &bar_k_full[s], pol_keep);
+                    tma_load_3d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, hz, &bar_k_full[s], pol_keep);
                 }
             }
             if (linear) {
@@ -248,10 +249,10 @@ __global__ void __launch_bounds__(256, 1)
                 tma_prefetch_desc(&tmPq);
                 mbar_wait(&bar_qk_done, 0);
                 mbar_arrive_expect_tx(&bar_pq, Q_BYTES);
-                tma_load_2d(sQ, &tmPq, 0, qrow, &bar_pq);
-                tma_load_2d(sQ + 8192, &tmPq, 0, qrow + 64, &bar_pq);
-                tma_load_2d(sQ + 16384, &tmPq, 64, qrow, &bar_pq);
-                tma_load_2d(sQ + 24576, &tmPq, 64, qrow + 64, &bar_pq);
+                tma_load_3d(sQ, &tmPq, 0, qrow, hz, &bar_pq);
+                tma_load_3d(sQ + 8192, &tmPq, 0, qrow + 64, hz, &bar_pq);
+                tma_load_3d(sQ + 16384, &tmPq, 64, qrow, hz, &bar_pq);
+                tma_load_3d(sQ + 24576, &tmPq, 64, qrow + 64, hz, &bar_pq);
             }
         }
     } else if (warp == 2) {
@@ -269,14 +270,14 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < nb; ++j) {
                 const int s = j % NSV;
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
-                const int krow = (int)(bh * p.N + (int64_t)kblock(j) * BK);
+                const int krow = kblock(j) * BK, hz = (int)bh;
                 if (j < 16) SLA2_TR(64 + j);
                 mbar_arrive_expect_tx(&bar_v_full[s], tx);
-                tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol_keep);
-                tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol_keep);
+                tma_load_3d_hint(sV(s), &tmV, 0, krow, hz, &bar_v_full[s], pol_keep);
+                tma_load_3d_hint(sV(s) + 8192, &tmV, 64, krow, hz, &bar_v_full[s], pol_keep);
                 if (ldphi) {
-                    tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol_keep);
-                    tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol_keep);
+                    tma_load_3d_hint(sPh(s), &tmPhi, 0, krow, hz, &bar_v_full[s], pol_keep);
+                    tma_load_3d_hint(sPh(s) + 8192, &tmPhi, 64, krow, hz, &bar_v_full[s], pol_keep);
                 }
             }
             if (linear) {
@@ -461,6 +462,18 @@ __global__ void __launch_bounds__(256, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&bar_s_free);  // QK(n+1) may overwrite S now
+            if (p.last_valid < BK) {
+                // ragged N: keys past N in the partial last key block (TMA zero-filled) get -inf
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    if (blk == 1 && !two) break;
+                    if (kblock(2 * n + blk) == p.tn - 1) {
+#pragma unroll
+                        for (int t = 0; t < 64; ++t)
+                            if (t >= p.last_valid) sr[blk * 64 + t] = __float_as_uint(-INFINITY);
+                    }
+                }
+            }
 #ifdef SLA2_EXP_NOSOFTMAX
             // experiment: MMA / TMA pipeline alone (P is garbage)
             if (n >= 2) mbar_wait(&bar_pv_done[b], ((n - 2) >> 1) & 1);
@@ -592,8 +605,9 @@ __global__ void __launch_bounds__(256, 1)
         const float inv_den = 1.0f / den;
         const float beta = 1.0f - alpha;
         const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
+        const bool row_ok = i * BQ + r < p.N;  // ragged tail: rows past N are not stored
         const uint32_t ob = smem_u32(sQ);  // every MMA reading sQ (Q K^T, phi(Q) Hc) is complete
-        const bool want_saved = p.o_s != nullptr;
+        const bool want_saved = p.o_s != nullptr && row_ok;
 #pragma unroll
         for (int c0 = 0; c0 < 128; c0 += 64) {
             uint32_t o[64], ln[64];  // 64 columns of O and of phi(Q) Hc: four loads, one wait
@@ -625,15 +639,15 @@ __global__ void __launch_bounds__(256, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (r == 0) {
-            const int orow0 = (int)(bh * p.N + (int64_t)i * BQ);
-            tma_store_2d(&tmO, 0, orow0, sQ);
-            tma_store_2d(&tmO, 0, orow0 + 64, sQ + 8192);
-            tma_store_2d(&tmO, 64, orow0, sQ + 16384);
-            tma_store_2d(&tmO, 64, orow0 + 64, sQ + 24576);
+            const int orow0 = i * BQ, hz = (int)bh;  // rows past N (ragged tail) are dropped
+            tma_store_3d(&tmO, 0, orow0, hz, sQ);
+            tma_store_3d(&tmO, 0, orow0 + 64, hz, sQ + 8192);
+            tma_store_3d(&tmO, 64, orow0, hz, sQ + 16384);
+            tma_store_3d(&tmO, 64, orow0 + 64, hz, sQ + 24576);
             tma_store_commit();
         }
         if (r == 0) SLA2_TR(53);
-        if (p.big_l) {
+        if (p.big_l && row_ok) {
             // L with raw K scores, shifted to the smoothed-K scores the reference uses:
             // q_r . K~_t = q_r . K_t - q_r . mu
             float shift = 0.0f;
@@ -678,6 +692,7 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
     p.H = (int)a.H;
     p.tm = a.tm;
     p.tn = a.tn;
+    p.last_valid = a.N - (a.tn - 1) * sp::BK;
     p.inv_sqrt_d = a.inv_sqrt_d;
     p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
     p.dense = a.dense;

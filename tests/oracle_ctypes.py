@@ -70,6 +70,12 @@ class Oracle:
         self._sig("topk_budget", [C.c_double, _sz], _sz)
         if prefix == "sla2o_":
             self._sig("set_threads", [C.c_int], None)
+            for s, fp, ft in (("f", _f32p, C.c_float), ("d", _f64p, C.c_double)):
+                ofp = _Opt(fp)
+                # ragged extension (the C port only; the reference rejects n % block != 0)
+                self._sig(f"attention_ragged_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, fp, fp, fp, C.c_double,
+                                                    C.c_int, C.c_int, fp, _Opt(_u8p), ofp, ofp, ofp], C.c_int)
+                self._sig(f"block_scores_ragged_{s}", [fp, fp, _sz, _sz, fp, fp, ft, _sz, _sz, fp], C.c_int)
 
     def _sig(self, name, argtypes, restype=C.c_int):
         fn = getattr(self.lib, self.prefix + name)
@@ -167,6 +173,25 @@ class Oracle:
         big_l = np.empty(n, dt)
         mask = np.empty((n // bq, n // bk), np.uint8)
         rc = getattr(self, "_attention_" + self._sfx(dt))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v), n, d, bq, bk,
+            np.ascontiguousarray(proj_q, dtype=dt), np.ascontiguousarray(proj_k, dtype=dt),
+            np.ascontiguousarray(rho, dtype=dt), k_percent, int(quant), int(smooth), out, mask,
+            o_s, o_l, big_l)
+        _check(rc)
+        return out, mask, o_s, o_l, big_l
+
+
+    def attention_ragged(self, q, k, v, bq, bk, proj_q, proj_k, rho, k_percent, quant=False, smooth=True):
+        """Ragged extension of attention(): n need not be divisible by bq / bk (C port only)."""
+        n, d = q.shape
+        dt = q.dtype
+        tm, tn = -(-n // bq), -(-n // bk)
+        out = np.empty((n, d), dt)
+        o_s = np.empty((n, d), dt)
+        o_l = np.empty((n, d), dt)
+        big_l = np.empty(n, dt)
+        mask = np.empty((tm, tn), np.uint8)
+        rc = getattr(self, "_attention_ragged_" + self._sfx(dt))(
             np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v), n, d, bq, bk,
             np.ascontiguousarray(proj_q, dtype=dt), np.ascontiguousarray(proj_k, dtype=dt),
             np.ascontiguousarray(rho, dtype=dt), k_percent, int(quant), int(smooth), out, mask,

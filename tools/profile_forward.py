@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {"cfg1": (1, 2, 4096), "cfg2": (1, 12, 32768), "cfg3": (1, 12, 75600), "cfg4": (1, 40, 75600)}
+CONFIGS = {"cfg1": (1, 2, 4096), "cfg2": (1, 12, 32760), "cfg2pad": (1, 12, 32768), "cfg3": (1, 12, 75600), "cfg4": (1, 40, 75600)}
 
 
 def main():
@@ -33,7 +33,7 @@ def main():
     eye = torch.eye(d, device=dev)[None]
     pq = (eye + 0.05 * torch.randn((H, d, d), generator=g, device=dev)).contiguous()
     pk = (eye + 0.05 * torch.randn((H, d, d), generator=g, device=dev)).contiguous()
-    rho = torch.zeros((H, N // 128), device=dev)
+    rho = torch.zeros((H, -(-N // 128)), device=dev)
     for _ in range(a.iters):
         sla2.forward(q, k, v, pq, pk, rho, k_percent=a.k_percent, quant=a.quant)
     torch.cuda.synchronize()
