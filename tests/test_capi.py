@@ -78,3 +78,10 @@ def test_no_cpu_fallback():
     rc = sla2.lib().sla2_forward(C.byref(p), None, None, None, None, None, None, None, None, None, None, None, 0, None)
     assert rc == 4  # SLA2_CUDA_ERROR
     assert b"no CUDA device" in sla2.lib().sla2_last_error() or b"sm_100a" in sla2.lib().sla2_last_error()
+
+
+def test_ragged_n_accepted_on_bf16_path():
+    """bf16, non-QAT: N need not divide into blocks (ragged extension, tests/test_ragged.py)."""
+    p = sla2.FwdParams(1, 2, 32760, 128)
+    assert (p.tm, p.tn) == (256, 512)
+    assert sla2.workspace_bytes(p) > 0
