@@ -43,7 +43,8 @@ def test_default_params_are_the_papers():
 
 
 @pytest.mark.parametrize("kw,err", [
-    (dict(N=1000), sla2.ShapeError),                      # attention.hpp:39-41
+    (dict(N=1000, quant=True), sla2.ShapeError),          # attention.hpp:39-41 (QAT keeps the rule)
+    (dict(N=1000, bf16=False, d=64, bq=64, bk=64), sla2.ShapeError),  # and so does the fp32 path
     (dict(k_percent=0.0), sla2.ShapeError),               # router.hpp:108-110
     (dict(k_percent=101.0), sla2.ShapeError),
     (dict(tau=0.0), sla2.NumericError),                   # router.hpp:32
