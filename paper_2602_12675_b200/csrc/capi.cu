@@ -241,7 +241,7 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.mu = c.take<float>(g.BH * g.d);
     t.mu_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
     t.qp = c.take<float>(g.BH * g.tm * g.d);
-    t.kp = c.take<float>(g.BH * g.tn * g.d);
+    t.kp = c.take<float>(g.BH * ((g.tn + 3) & ~int64_t(3)) * g.d);  // transposed rows padded to 4 keys
     t.qbar = c.take<float>(g.BH * g.tm * g.d);
     t.kbar = c.take<float>(g.BH * g.tn * g.d);
     t.idx = c.take<int32_t>(g.BH * g.tm * std::max<int64_t>(g.kappa, g.tn));

@@ -426,10 +426,12 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
             }
         }
         if (xp_t) {
+            // transposed rows padded to a multiple of 4 keys (aligned float4 rows for any tn)
+            const int ldt = (nrows + 3) & ~3;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                float* dst = xp + (bh * d + cg * 4 + b) * (int64_t)nrows + r0 + rg * 4;
-                if (rg * 4 + 4 <= nr && (nrows & 3) == 0) {
+                float* dst = xp + (bh * d + cg * 4 + b) * (int64_t)ldt + r0 + rg * 4;
+                if (rg * 4 + 4 <= nr) {
                     *reinterpret_cast<float4*>(dst) = make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
                 } else {
 #pragma unroll
@@ -576,42 +578,45 @@ __global__ void router_scores_topk_kernel(const float* __restrict__ qp, const fl
              idx_out + (bh * tm + i) * (int64_t)kappa, sel, warp_cnt);
 }
 
-// Warp-local top-k for small kappa (<= 64) and tn <= 32 * TKMAX: each lane holds the keys of
-// columns lane, lane+32, ... in registers; kappa rounds of a warp-wide minimum over
-// (desc_key, column) pick exactly the stable-sort prefix (value desc, ties to the lower column).
+// Warp-local top-k, one warp per row, tn <= 32 * TKMAX keys (lane l holds j = l + 32u), any
+// kappa <= tn: a radix select on the 32-bit descending keys finds T, the kappa-th best value
+// (32 rounds of one compare per key and a warp add), then every key better than T is kept and
+// the ties at T in ascending column order -- exactly std::stable_sort with pc(i,a) > pc(i,b)
+// (router.hpp:117-122). About 2 * 32 * TKMAX instructions per row, against kappa rescans of
+// TKMAX 64-bit keys for a kappa-round argmax.
 template <int TKMAX>  // keys per lane: tn <= 32 * TKMAX
-__device__ void warp_topk_small(const float* __restrict__ vals, int tn, int kappa, uint8_t* __restrict__ mask_row,
+__device__ void warp_topk_small(float* __restrict__ vals, int tn, int kappa, uint8_t* __restrict__ mask_row,
                                 int32_t* __restrict__ idx_row, uint8_t* sel) {
     const int lane = threadIdx.x & 31;
-    const int per = (tn + 31) >> 5;
-    unsigned long long key[TKMAX];
-#pragma unroll
-    for (int u = 0; u < TKMAX; ++u) {
-        const int j = lane + 32 * u;
-        key[u] = (u < per && j < tn) ? (((unsigned long long)desc_key(vals[j]) << 32) | (unsigned)j) : ~0ull;
-    }
-    for (int j = lane; j < tn; j += 32) sel[j] = 0;
-    unsigned long long best = ~0ull;
-#pragma unroll
-    for (int u = 0; u < TKMAX; ++u) best = key[u] < best ? key[u] : best;
+    // the row's keys replace its (already stored) probabilities in shared memory: no per-lane
+    // key array, so a 2048-key row does not cost the kernel 64 registers (occupancy)
+    uint32_t* hk = reinterpret_cast<uint32_t*>(vals);  // desc_key: smaller is better
+    for (int j = lane; j < tn; j += 32) hk[j] = desc_key(vals[j]);
     __syncwarp();
-    for (int r = 0; r < kappa; ++r) {
-        unsigned long long w = best;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long t = __shfl_xor_sync(0xffffffffu, w, o);
-            w = t < w ? t : w;
-        }
-        const int jw = (int)(w & 0xffffffffu);
-        if ((jw & 31) == lane) {  // owner removes it and rescans its registers
-            sel[jw] = 1;
-            best = ~0ull;
-#pragma unroll
-            for (int u = 0; u < TKMAX; ++u) {
-                if (key[u] == w) key[u] = ~0ull;
-                best = key[u] < best ? key[u] : best;
-            }
-        }
+    auto count_below = [&](uint32_t t) {
+        int c = 0;
+#pragma unroll 4
+        for (int j = lane; j < tn; j += 32) c += hk[j] < t ? 1 : 0;
+        return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    };
+    // invariant: #(keys < prefix) < kappa
+    uint32_t prefix = 0;
+    for (int b = 31; b >= 0; --b) {
+        const uint32_t cand = prefix | (1u << b);
+        if (count_below(cand) < kappa) prefix = cand;
+    }
+    const int ties = kappa - count_below(prefix);  // keys equal to T = prefix still to keep
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int taken = 0;
+    for (int j0 = 0; j0 < tn; j0 += 32) {  // ascending columns: ties are kept lowest column first
+        const int j = j0 + lane;
+        const bool valid = j < tn;
+        const uint32_t kj = valid ? hk[j] : 0xffffffffu;
+        const bool eq = valid && kj == prefix;
+        const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+        const bool take = valid && (kj < prefix || (eq && taken + __popc(eqm & lt_mask) < ties));
+        taken += __popc(eqm);
+        if (valid) sel[j] = take ? 1 : 0;
     }
     __syncwarp();
     int base = 0;
@@ -674,7 +679,7 @@ __device__ void warp_topk_row(const float* __restrict__ vals, int tn, int kappa,
 // Dynamic smem: 8*tn floats + 8*(npow2*8 + tn) bytes + 8*d floats.
 constexpr int RROWS = 8;
 template <int TK>  // 0: bitonic top-k; otherwise register top-k with TK keys per lane
-__global__ void __launch_bounds__(256) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
+__global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
                                                           int kp_t, float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
                                                           float* __restrict__ pc_out, uint8_t* __restrict__ mask_out,
                                                           int32_t* __restrict__ idx_out) {
@@ -682,7 +687,8 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
     float* vals = reinterpret_cast<float*>(smem);       // [8][tn]
     float* sq = vals + RROWS * tn;                       // [8][d]
     uint8_t* keyb = reinterpret_cast<uint8_t*>(sq + RROWS * d);
-    const size_t key_stride = ((size_t)npow2 * 8 + tn + 15) & ~size_t(15);
+    // per-row top-k scratch: 64-bit sort keys for the bitonic path, selection flags otherwise
+    const size_t key_stride = TK > 0 ? (((size_t)tn + 15) & ~size_t(15)) : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
     const int i0 = blockIdx.x * RROWS;
     const int64_t bh = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -692,8 +698,10 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
         sq[e] = (r < nrows) ? qp[(bh * tm + i0 + r) * (int64_t)d + (e % d)] : 0.0f;
     }
     __syncthreads();
-    const float* kpb = kp + bh * (int64_t)tn * d;
+    const float* kpb = kp + bh * (int64_t)tn * d;  // row-major [tn][d]
     if (kp_t) {
+        const int tnp = (tn + 3) & ~3;  // transposed key rows are padded to whole float4s
+        const float* kpt = kp + bh * (int64_t)tnp * d;
         // same 4 x 4 register tile over the transposed keys [d][tn]: for each feature c the
         // lanes read 4 consecutive keys each (one coalesced 512-B row per warp); each chain
         // still accumulates over c ascending with separate mul and add
@@ -706,8 +714,8 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
                 for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
             // pointer-stepped (d and tn are run-time: recomputing 64-bit addresses per step
             // cost more instructions than the FP work, ncu source page)
-            const float4* kq = reinterpret_cast<const float4*>(kpb + jg * 4);
-            const size_t kstep = (size_t)tn / 4;  // one feature row of keys, in float4
+            const float4* kq = reinterpret_cast<const float4*>(kpt + jg * 4);
+            const size_t kstep = (size_t)tnp / 4;  // one feature row of keys, in float4
             const float* sqr = sq + rg * 4 * d;
 #pragma unroll 2
             for (int c = 0; c < d; c += 4) {
@@ -732,7 +740,8 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
+                for (int b = 0; b < 4; ++b)
+                    if (jg * 4 + b < tn) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
         }
     } else if ((tn & 3) == 0 && (d & 3) == 0) {
         // register tile: 4 rows x 4 columns per thread, 16 independent serial chains; each
@@ -836,10 +845,10 @@ __global__ void __launch_bounds__(256) router_rows_kernel(const float* __restric
     else warp_topk_row(v, tn, kappa, keys, npow2, mrow, irow);
 }
 
-size_t router_rows_smem(int tn, int d) {
+size_t router_rows_smem(int tn, int d, bool radix) {
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
-    const size_t key_stride = ((size_t)npow2 * 8 + tn + 15) & ~size_t(15);
+    const size_t key_stride = radix ? (((size_t)tn + 15) & ~size_t(15)) : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
     return (size_t)RROWS * tn * 4 + (size_t)RROWS * d * 4 + RROWS * key_stride + 16;
 }
 
@@ -974,8 +983,10 @@ static cudaError_t router_back_t(const RouterLaunch& a, cudaStream_t st, int* la
     const int tm = (a.N + a.bq - 1) / a.bq, tn = (a.N + a.bk - 1) / a.bk;
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
-    const size_t rsm = router_rows_smem(tn, a.d);
-    const bool tile_ok = rsm <= 220 * 1024 && (tn & 3) == 0 && (a.d & 3) == 0;
+    // register radix top-k for tn <= 2048 (any kappa), bitonic in shared memory beyond
+    const int tk = tn <= 32 * 16 ? 16 : (tn <= 32 * 64 ? 64 : 0);
+    const size_t rsm = router_rows_smem(tn, a.d, tk > 0);
+    const bool tile_ok = rsm <= 220 * 1024 && (a.d & 3) == 0;  // any tn: transposed rows are padded
     bool kp_t;
     if (a.kbar_ready) {
         // pooled keys already in kbar (launch_kprep, d = 128): project only
@@ -996,8 +1007,8 @@ static cudaError_t router_back_t(const RouterLaunch& a, cudaStream_t st, int* la
             kern<<<grid, 256, rsm, st>>>(a.qp, a.kp, kp_t ? 1 : 0, a.inv_sqrt_d, tm, tn, a.d, a.kappa, npow2,
                                          a.pc_out, a.mask_out, a.idx_out);
         };
-        if (a.kappa <= 64 && tn <= 32 * 16) go(router_rows_kernel<16>);
-        else if (a.kappa <= 64 && tn <= 32 * 64) go(router_rows_kernel<64>);
+        if (tk == 16) go(router_rows_kernel<16>);
+        else if (tk == 64) go(router_rows_kernel<64>);
         else go(router_rows_kernel<0>);
     } else {
         const size_t smem = npow2 * 8 + tn * 4 + a.d * 4 + tn + 16;

@@ -443,6 +443,8 @@ __global__ void __launch_bounds__(256, 1)
         const int r = threadIdx.x - 128;  // query row within the block
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         const float rho_i = linear ? p.rho[(int64_t)h * p.tm + i] : 0.0f;  // loaded now, used after the loop
+        // ragged N: does this row keep the partial last key block? (one load, before the loop)
+        const bool tail_kept = p.last_valid < BK && kblock(nb - 1) == p.tn - 1;
         float m2 = -INFINITY, l = 0.0f;
         for (int n = 0; n < npair; ++n) {
             const int b = n & 1;
@@ -452,6 +454,14 @@ __global__ void __launch_bounds__(256, 1)
             if (r == 0 && n < 16) SLA2_TR(2 + n);
             tc_fence_after();
             const uint32_t sbase = tmem + lane_base + TM_S;
+            if (tail_kept && n == npair - 1) {
+                // ragged N: keys past N in the partial last key block (zero-filled K) get -inf,
+                // written into S in TMEM before the load (no extra registers in the softmax).
+                // Kept blocks ascend, so that block is the row's last one (nb - 1).
+                const uint32_t col0 = (uint32_t)(((nb - 1) - 2 * n) * 64);
+                for (int t = p.last_valid; t < BK; ++t) tmem_st1(sbase + col0 + t, __float_as_uint(-INFINITY));
+                tmem_st_wait();
+            }
             uint32_t sr[128];
             tmem_ld32(sbase, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
             tmem_ld32(sbase + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
@@ -462,27 +472,6 @@ __global__ void __launch_bounds__(256, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&bar_s_free);  // QK(n+1) may overwrite S now
-            if (p.last_valid < BK) {
-                // ragged N: keys past N in the partial last key block (TMA zero-filled) get -inf
-#pragma unroll
-                for (int blk = 0; blk < 2; ++blk) {
-                    if (blk == 1 && !two) break;
-                    if (kblock(2 * n + blk) == p.tn - 1) {
-#pragma unroll
-                        for (int t = 0; t < 64; ++t)
-                            if (t >= p.last_valid) sr[blk * 64 + t] = __float_as_uint(-INFINITY);
-                    }
-                }
-            }
-#ifdef SLA2_EXP_NOSOFTMAX
-            // experiment: MMA / TMA pipeline alone (P is garbage)
-            if (n >= 2) mbar_wait(&bar_pv_done[b], ((n - 2) >> 1) & 1);
-            m2 = 0.0f;
-            l = 1.0f;
-            tc_fence_before();
-            mbar_arrive(&bar_p_full[b]);
-            continue;
-#endif
             // row max as four independent FMNMX3 chains (one 64-long chain was ~0.13 us a pair)
             float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
