@@ -135,14 +135,14 @@ __global__ void __launch_bounds__(256, 1)
     using namespace sp;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_pq, bar_den, bar_zc, bar_ht, bar_k_full[NKP],
+    __shared__ uint64_t bar_q, bar_qk_done, bar_mma_done, bar_pq, bar_zc, bar_ht, bar_k_full[NKP],
         bar_k_empty[NKP],
         bar_v_full[NSV],
         bar_v_empty[NSV], bar_s_full, bar_s_free, bar_p_full[2], bar_pv_done[2], bar_lin_ready, bar_lin_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[D];
     __shared__ float sDen[BQ];
-    __shared__ int den_ctr;
+    __shared__ float sInvL[BQ];  // 1 / l per row, for the 8-warp epilogue
 
     const int i = blockIdx.x;       // query block
     const int64_t bh = blockIdx.y;  // (b, h)
@@ -160,9 +160,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(&bar_qk_done, 1);
         mbar_init(&bar_mma_done, 1);
         mbar_init(&bar_pq, 1);
-        mbar_init(&bar_den, 96);
         mbar_init(&bar_zc, 1);
-        den_ctr = 0;
         mbar_init(&bar_ht, 1);
         for (int s = 0; s < NKP; ++s) {
             mbar_init(&bar_k_full[s], 1);
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         mbar_init(&bar_s_full, 1);
         mbar_init(&bar_s_free, 128);
-        mbar_init(&bar_lin_ready, 128);
+        mbar_init(&bar_lin_ready, 256);
         mbar_init(&bar_lin_done, 1);
         fence_barrier_init();
     }
@@ -198,25 +196,6 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sHt = sV(nb % NSV);
     uint8_t* sHc = sV((nb + 1) % NSV);
     auto kblock = [&](int j) { return dense ? j : idx[j]; };
-    // phi(Q) . Zc, shared by warps 0, 2 and 3 once their own work is issued: phi(Q) replaces
-    // Q in sQ (TMA, bar_pq) after the last Q K^T; warps claim 32-row chunks. Every thread of
-    // the three warps arrives on bar_den once.
-    auto den_share = [&]() {
-        if (!linear) return;
-        __syncwarp();
-        mbar_wait(&bar_zc, 0);
-        mbar_wait(&bar_pq, 0);
-        __syncwarp();
-        const uint32_t qb = smem_u32(sQ);
-        for (;;) {
-            int c = 0;
-            if (lane == 0) c = atomicAdd(&den_ctr, 32);
-            c = __shfl_sync(0xffffffffu, c, 0);
-            if (c >= BQ) break;
-            den_row(qb, c + lane, sZc, sDen);
-        }
-        mbar_arrive(&bar_den);
-    };
 
     if (warp == 0) {
         // ===================== TMA producer: Q, K pair ring =====================
@@ -386,19 +365,6 @@ __global__ void __launch_bounds__(256, 1)
             if (lane == 0 && n < 16) SLA2_TR(112 + n);
         }
         umma_commit_w(&bar_mma_done);  // every QK / PV / HS of the loop
-        if (linear) {
-            // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
-            mbar_wait(&bar_lin_ready, 0);
-            mbar_wait(&bar_pq, 0);
-            tc_fence_after();
-            const uint64_t dH = sdesc_sw128(warp_uniform(smem_u32(sHc)), 16384, 1024);
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
-                umma_bf16_ss_w(tm + TM_L, dQ + off, dH + ((ks * 2048) >> 4), ID_PV, ks > 0);
-            }
-            umma_commit_w(&bar_lin_done);
-        }
     } else if (warp == 3) {
         // ===================== Zc, then phi(Q) in place over sQ and phi(Q) . Zc =====================
         if (linear) {
@@ -541,104 +507,17 @@ __global__ void __launch_bounds__(256, 1)
             mbar_arrive(&bar_p_full[b]);
             if (r == 0 && n < 16) SLA2_TR(18 + n);
         }
-        // all MMAs of the main loop complete (the last HS may come after the last PV)
-        mbar_wait(&bar_mma_done, 0);
-        __syncwarp();
-        tc_fence_after();
-        if (r == 0) SLA2_TR(50);
-
-        float alpha = 1.0f;
-        float den = 1.0f;
-        if (linear) {
-            // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
-            const float x = rho_i;
-            float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
-            a = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
-            alpha = a;
-            // Hc = Htot - Hsel, row f = r, bf16 into the MN-major B tile [c_atom][f][64]
-            mbar_wait(&bar_ht, 0);
-            __syncwarp();
-            const uint32_t hb = smem_u32(sHc), htb = smem_u32(sHt);
-            fence_proxy_async_smem();
-            uint32_t hs[128];  // the whole Hsel row: four loads, one wait
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(tmem + lane_base + TM_H + c0, *reinterpret_cast<uint32_t(*)[32]>(&hs[c0]));
-            tmem_ld_wait();
-#pragma unroll
-            for (int ch = 0; ch < 16; ++ch) {
-                const int c = ch * 8;
-                const uint32_t off = (c >> 6) * 16384 + sw128_off(r, c & 63);
-                uint32_t t[4], o4[4];
-                ld_shared_v4(htb + off, t[0], t[1], t[2], t[3]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t[e]));
-                    o4[e] = pack_bf16(tf.x - __uint_as_float(hs[c + 2 * e]), tf.y - __uint_as_float(hs[c + 2 * e + 1]));
-                }
-                st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
-            }
-            fence_proxy_async_smem();
-            tc_fence_before();
-            mbar_arrive(&bar_lin_ready);
-            if (r == 0) SLA2_TR(51);
-            mbar_wait(&bar_den, 0);
-            den = sDen[r];
-            mbar_wait(&bar_lin_done, 0);
-            if (r == 0) SLA2_TR(52);
-            __syncwarp();
-            tc_fence_after();
+        // row statistics for the 8-warp epilogue (published through bar_lin_ready)
+        sInvL[r] = 1.0f / l;
+        if (linear) {  // den = phi(Q)_r . Zc, from the TMA-loaded phi(Q) tile
+            mbar_wait(&bar_zc, 0);
+            mbar_wait(&bar_pq, 0);
+            den_row(smem_u32(sQ), r, sZc, sDen);
         }
-
-        // output: out = alpha * O / l + (1 - alpha) * num / den
-        const float inv_l = 1.0f / l;
-        const float inv_den = 1.0f / den;
-        const float beta = 1.0f - alpha;
-        const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
-        const bool row_ok = i * BQ + r < p.N;  // ragged tail: rows past N are not stored
-        const uint32_t ob = smem_u32(sQ);  // every MMA reading sQ (Q K^T, phi(Q) Hc) is complete
-        const bool want_saved = p.o_s != nullptr && row_ok;
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 64) {
-            uint32_t o[64], ln[64];  // 64 columns of O and of phi(Q) Hc: four loads, one wait
-            tmem_ld32(tmem + lane_base + TM_O + c0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-            tmem_ld32(tmem + lane_base + TM_O + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-            if (linear) {
-                tmem_ld32(tmem + lane_base + TM_L + c0, *reinterpret_cast<uint32_t(*)[32]>(&ln[0]));
-                tmem_ld32(tmem + lane_base + TM_L + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ln[32]));
-            }
-            tmem_ld_wait();
-            float res[64];
-#pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const float os = __uint_as_float(o[c]) * inv_l;
-                const float ol = linear ? __uint_as_float(ln[c]) * inv_den : 0.0f;
-                res[c] = linear ? alpha * os + beta * ol : os;
-                if (want_saved) {
-                    p.o_s[grow * D + c0 + c] = os;
-                    p.o_l[grow * D + c0 + c] = ol;
-                }
-            }
-            // bf16 row into the (now free) Q tile, SW128 layout: one TMA store writes the block
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-                st_shared_v4(ob + (c0 >> 6) * 16384 + sw128_off(r, ch * 8), pack_bf16(res[ch * 8 + 0], res[ch * 8 + 1]),
-                             pack_bf16(res[ch * 8 + 2], res[ch * 8 + 3]), pack_bf16(res[ch * 8 + 4], res[ch * 8 + 5]),
-                             pack_bf16(res[ch * 8 + 6], res[ch * 8 + 7]));
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (r == 0) {
-            const int orow0 = i * BQ, hz = (int)bh;  // rows past N (ragged tail) are dropped
-            tma_store_3d(&tmO, 0, orow0, hz, sQ);
-            tma_store_3d(&tmO, 0, orow0 + 64, hz, sQ + 8192);
-            tma_store_3d(&tmO, 64, orow0, hz, sQ + 16384);
-            tma_store_3d(&tmO, 64, orow0 + 64, hz, sQ + 24576);
-            tma_store_commit();
-        }
-        if (r == 0) SLA2_TR(53);
-        if (p.big_l && row_ok) {
+        if (p.big_l && i * BQ + r < p.N) {
             // L with raw K scores, shifted to the smoothed-K scores the reference uses:
             // q_r . K~_t = q_r . K_t - q_r . mu
+            const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
             float shift = 0.0f;
             if (p.mu) {
                 const float* mu = p.mu + bh * D;
@@ -648,13 +527,126 @@ __global__ void __launch_bounds__(256, 1)
             }
             p.big_l[grow] = m2 / 1.4426950408889634f + logf(l) - shift;
         }
-        if (r == 0) tma_store_wait_read();  // sQ must stay valid until the store has read it
+    }
+
+    // ===================== epilogue, all eight warps =====================
+    // Warp w serves rows 32 (w % 4) + lane (its TMEM lane quarter) and column half
+    // ch = w < 4 ? 1 : 0 of Hc and of the output, so each thread moves 64 columns, not 128.
+    {
+        __syncwarp();
+        const int q4 = warp & 3, r = q4 * 32 + lane;
+        const int c0 = warp < 4 ? 64 : 0;
+        const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+        mbar_wait(&bar_mma_done, 0);  // every QK / PV / HS of the loop is complete
+        __syncwarp();
+        tc_fence_after();
+        if (threadIdx.x == 128) SLA2_TR(50);
+        float alpha = 1.0f;
+        if (linear) {
+            // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
+            const float x = p.rho[(int64_t)h * p.tm + i];
+            float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
+            a = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
+            alpha = a;
+            // Hc = Htot - Hsel: row f = r, columns c0 .. c0 + 63, bf16 into the MN-major B tile
+            mbar_wait(&bar_ht, 0);
+            __syncwarp();
+            const uint32_t hb = smem_u32(sHc), htb = smem_u32(sHt);
+            uint32_t hs[64];
+            tmem_ld32(tmem + lane_base + TM_H + c0, *reinterpret_cast<uint32_t(*)[32]>(&hs[0]));
+            tmem_ld32(tmem + lane_base + TM_H + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&hs[32]));
+            tmem_ld_wait();
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const uint32_t off = (c0 >> 6) * 16384 + sw128_off(r, ch * 8);
+                uint32_t t[4], o4[4];
+                ld_shared_v4(htb + off, t[0], t[1], t[2], t[3]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t[e]));
+                    o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
+                                      tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
+                }
+                st_shared_v4(hb + off, o4[0], o4[1], o4[2], o4[3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+        }
+        mbar_arrive(&bar_lin_ready);  // also publishes sInvL (written by the softmax warps)
+        mbar_wait(&bar_lin_ready, 0);
+        if (threadIdx.x == 128) SLA2_TR(51);
+        if (linear && warp == 1) {
+            // O_l numerator = phi(Q) (Htot - Hsel): A = phi(Q) (K-major, in sQ), B = Hc (MN-major)
+            mbar_wait(&bar_pq, 0);
+            tc_fence_after();
+            constexpr uint32_t ID_LIN = idesc_bf16(128, 128, false, true);
+            const uint32_t tm = warp_uniform(tmem);
+            const uint64_t dQl = sdesc_sw128(warp_uniform(smem_u32(sQ)), 16, 1024);
+            const uint64_t dH = sdesc_sw128(warp_uniform(smem_u32(sHc)), 16384, 1024);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+                umma_bf16_ss_w(tm + TM_L, dQl + off, dH + ((ks * 2048) >> 4), ID_LIN, ks > 0);
+            }
+            umma_commit_w(&bar_lin_done);
+        }
+        float inv_den = 0.0f;
+        if (linear) {
+            inv_den = 1.0f / sDen[r];  // written before bar_lin_ready by the softmax warps
+            mbar_wait(&bar_lin_done, 0);
+            __syncwarp();
+            tc_fence_after();
+        }
+        if (threadIdx.x == 128) SLA2_TR(52);
+        // out = alpha * O / l + (1 - alpha) * num / den, columns c0 .. c0 + 63 of row r
+        const float inv_l = sInvL[r];
+        const float beta = 1.0f - alpha;
+        const int64_t grow = bh * p.N + (int64_t)i * BQ + r;
+        const bool want_saved = p.o_s != nullptr && i * BQ + r < p.N;  // ragged tail: not stored
+        const uint32_t ob = smem_u32(sQ);  // every MMA reading sQ (Q K^T, phi(Q) Hc) is complete
+        uint32_t o[64], ln[64];
+        tmem_ld32(tmem + lane_base + TM_O + c0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+        tmem_ld32(tmem + lane_base + TM_O + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+        if (linear) {
+            tmem_ld32(tmem + lane_base + TM_L + c0, *reinterpret_cast<uint32_t(*)[32]>(&ln[0]));
+            tmem_ld32(tmem + lane_base + TM_L + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ln[32]));
+        }
+        tmem_ld_wait();
+        float res[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+            const float os = __uint_as_float(o[c]) * inv_l;
+            const float ol = linear ? __uint_as_float(ln[c]) * inv_den : 0.0f;
+            res[c] = linear ? alpha * os + beta * ol : os;
+            if (want_saved) {
+                p.o_s[grow * D + c0 + c] = os;
+                p.o_l[grow * D + c0 + c] = ol;
+            }
+        }
+        // bf16 half-row into the (now free) Q tile, SW128 layout: one TMA store writes the block
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch)
+            st_shared_v4(ob + (c0 >> 6) * 16384 + sw128_off(r, ch * 8), pack_bf16(res[ch * 8 + 0], res[ch * 8 + 1]),
+                         pack_bf16(res[ch * 8 + 2], res[ch * 8 + 3]), pack_bf16(res[ch * 8 + 4], res[ch * 8 + 5]),
+                         pack_bf16(res[ch * 8 + 6], res[ch * 8 + 7]));
+        fence_proxy_async_smem();
         tc_fence_before();
     }
-    // one call site, so the denominator code exists once (the softmax loop keeps the I-cache)
-    if (warp == 0 || warp == 2 || warp == 3) den_share();
     __syncthreads();
-    if (warp == 2) tmem_free(tmem, 512);
+    if (threadIdx.x == 0) {
+        const int orow0 = i * BQ, hz = (int)bh;  // rows past N (ragged tail) are dropped
+        tma_store_3d(&tmO, 0, orow0, hz, sQ);
+        tma_store_3d(&tmO, 0, orow0 + 64, hz, sQ + 8192);
+        tma_store_3d(&tmO, 64, orow0, hz, sQ + 16384);
+        tma_store_3d(&tmO, 64, orow0 + 64, hz, sQ + 24576);
+        tma_store_commit();
+        SLA2_TR(53);
+        tma_store_wait_read();  // sQ must stay valid until the store has read it
+    }
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_free(tmem, 512);
+    }
 }
 
 #ifdef SLA2_TRACE
