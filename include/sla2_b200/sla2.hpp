@@ -29,6 +29,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <type_traits>
 #include <limits>
 #include <stdexcept>
 #include <string>
@@ -428,5 +430,80 @@ inline Matrix<float> sla2_attention(const Matrix<float>& q, const Matrix<float>&
     }
     return b200::download_as(dout, n, d, p);
 }
+
+// ------------------------------------------------------------------ RTEN1 files (tensor_io.hpp:12-115)
+// magic "RTEN1\0" | u32le rank | u32le dims[rank] | u8 dtype (0 = f32, 1 = f64) | raw LE data.
+// The golden-exchange format of the reference's harness; same names, same errors.
+namespace rten {
+template <class T>
+constexpr std::uint8_t dtype_code() {
+    static_assert(std::is_same<T, float>::value || std::is_same<T, double>::value, "RTEN1 supports f32 and f64 only");
+    return std::is_same<T, float>::value ? 0 : 1;
+}
+namespace io {
+inline void put_u32(std::ostream& os, std::uint32_t v) {
+    const unsigned char b[4] = {(unsigned char)v, (unsigned char)(v >> 8), (unsigned char)(v >> 16),
+                                (unsigned char)(v >> 24)};
+    os.write(reinterpret_cast<const char*>(b), 4);
+}
+inline std::uint32_t get_u32(std::istream& is) {
+    unsigned char b[4] = {0, 0, 0, 0};
+    is.read(reinterpret_cast<char*>(b), 4);
+    return (std::uint32_t)b[0] | ((std::uint32_t)b[1] << 8) | ((std::uint32_t)b[2] << 16) | ((std::uint32_t)b[3] << 24);
+}
+template <class T>
+void write(const std::string& path, const std::vector<std::uint32_t>& dims, const std::vector<T>& data) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw contract_error("RTEN1: cannot open for write: " + path);
+    os.write("RTEN1\0", 6);
+    put_u32(os, (std::uint32_t)dims.size());
+    for (std::uint32_t d : dims) put_u32(os, d);
+    const std::uint8_t code = dtype_code<T>();
+    os.write(reinterpret_cast<const char*>(&code), 1);
+    os.write(reinterpret_cast<const char*>(data.data()), (std::streamsize)(data.size() * sizeof(T)));
+}
+template <class T>
+std::vector<T> read(const std::string& path, std::vector<std::uint32_t>& dims) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw contract_error("RTEN1: cannot open: " + path);
+    char magic[6];
+    is.read(magic, 6);
+    if (!is || std::memcmp(magic, "RTEN1\0", 6) != 0) throw contract_error("RTEN1: bad magic in " + path);
+    dims.assign(get_u32(is), 0);
+    std::size_t count = 1;
+    for (auto& d : dims) count *= (d = get_u32(is));
+    std::uint8_t code = 0xff;
+    is.read(reinterpret_cast<char*>(&code), 1);
+    if (code != dtype_code<T>()) throw contract_error("RTEN1: dtype mismatch in " + path);
+    std::vector<T> data(count);
+    is.read(reinterpret_cast<char*>(data.data()), (std::streamsize)(count * sizeof(T)));
+    if (!is) throw contract_error("RTEN1: truncated file " + path);
+    return data;
+}
+}  // namespace io
+
+template <class T>
+void save(const std::string& path, const Matrix<T>& m) {
+    io::write(path, {(std::uint32_t)m.rows(), (std::uint32_t)m.cols()}, m.data());
+}
+template <class T>
+void save(const std::string& path, const Vector<T>& v) {
+    io::write(path, {(std::uint32_t)v.size()}, v.data());
+}
+template <class T>
+Matrix<T> load_matrix(const std::string& path) {
+    std::vector<std::uint32_t> dims;
+    std::vector<T> data = io::read<T>(path, dims);
+    if (dims.size() != 2) throw contract_error("RTEN1: expected rank 2 in " + path);
+    return Matrix<T>(dims[0], dims[1], std::move(data));
+}
+template <class T>
+Vector<T> load_vector(const std::string& path) {
+    std::vector<std::uint32_t> dims;
+    std::vector<T> data = io::read<T>(path, dims);
+    if (dims.size() != 1) throw contract_error("RTEN1: expected rank 1 in " + path);
+    return Vector<T>(std::move(data));
+}
+}  // namespace rten
 
 }  // namespace sla2

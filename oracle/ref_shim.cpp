@@ -14,6 +14,7 @@
 #include "sla2/attention.hpp"
 #include "sla2/quant.hpp"
 #include "sla2/router.hpp"
+#include "sla2/tensor_io.hpp"
 #include "test_util.hpp"
 
 using namespace sla2;
@@ -204,6 +205,33 @@ extern "C" {
 
 SLA2R_INST(float, f)
 SLA2R_INST(double, d)
+
+// RTEN1 through the reference's own sla2::rten (tensor_io.hpp): rank-2 save / load (rank 1 when
+// rows == 0), so the exchange format is checked against the reference's writer and reader.
+#define SLA2R_RTEN(T, S)                                                                          \
+    int sla2r_rten_save_##S(const char* path, std::size_t rows, std::size_t cols, const T* data) { \
+        try {                                                                                     \
+            if (rows == 0) rten::save(path, Vector<T>(std::vector<T>(data, data + cols)));        \
+            else rten::save(path, wrap(data, rows, cols));                                        \
+            return 0;                                                                             \
+        } catch (const std::exception& e) { return classify(e); }                                 \
+    }                                                                                             \
+    int sla2r_rten_load_##S(const char* path, std::size_t rows, std::size_t cols, T* out) {      \
+        try {                                                                                     \
+            if (rows == 0) {                                                                      \
+                auto v = rten::load_vector<T>(path);                                              \
+                if (v.size() != cols) return 1;                                                   \
+                std::memcpy(out, v.data().data(), sizeof(T) * cols);                              \
+            } else {                                                                              \
+                auto m = rten::load_matrix<T>(path);                                              \
+                if (m.rows() != rows || m.cols() != cols) return 1;                               \
+                copy_out(m, out);                                                                 \
+            }                                                                                     \
+            return 0;                                                                             \
+        } catch (const std::exception& e) { return classify(e); }                                 \
+    }
+SLA2R_RTEN(float, f)
+SLA2R_RTEN(double, d)
 
 std::size_t sla2r_topk_budget(double kp, std::size_t tn) { return topk_budget(kp, tn); }
 std::size_t sla2r_max_worker_threads(void) { return max_worker_threads(); }

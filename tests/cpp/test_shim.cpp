@@ -170,7 +170,35 @@ static void attention_tests() {
     }
 }
 
+// RTEN1 (tensor_io.hpp): round trip and the reference's error messages
+static void rten_tests() {
+    const std::string f = "/tmp/sla2_shim_rten_test.rten";
+    Matrix<float> m = gaussian(5, 7, 11);
+    rten::save(f, m);
+    Matrix<float> back = rten::load_matrix<float>(f);
+    EXPECT(back.rows() == 5 && back.cols() == 7 && back.data() == m.data());
+    bool threw = false;
+    try {
+        (void)rten::load_matrix<double>(f);
+    } catch (const contract_error& e) {
+        threw = std::string(e.what()).find("dtype mismatch") != std::string::npos;
+    }
+    EXPECT(threw);
+    Vector<double> v(std::vector<double>{1.0, -2.5, 3.25});
+    rten::save(f, v);
+    EXPECT(rten::load_vector<double>(f).data() == v.data());
+    threw = false;
+    try {
+        (void)rten::load_matrix<double>(f);
+    } catch (const contract_error& e) {
+        threw = std::string(e.what()).find("expected rank 2") != std::string::npos;
+    }
+    EXPECT(threw);
+    std::remove(f.c_str());
+}
+
 int main() {
+    rten_tests();
     hard_topk_kats();
     block_scores_tests();
     smooth_k_tests();

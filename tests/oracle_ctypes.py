@@ -68,6 +68,10 @@ class Oracle:
             self._sig(f"gaussian_matrix_{s}", [fp, _sz, C.c_uint64, C.c_double], None)
             self._sig(f"random_matrix_{s}", [fp, _sz, C.c_uint64, C.c_double, C.c_double], None)
         self._sig("topk_budget", [C.c_double, _sz], _sz)
+        if prefix == "sla2r_":
+            for s, fp in (("f", _f32p), ("d", _f64p)):
+                self._sig(f"rten_save_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
+                self._sig(f"rten_load_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
         if prefix == "sla2o_":
             self._sig("set_threads", [C.c_int], None)
             for s, fp, ft in (("f", _f32p, C.c_float), ("d", _f64p, C.c_double)):
@@ -198,6 +202,19 @@ class Oracle:
             o_s, o_l, big_l)
         _check(rc)
         return out, mask, o_s, o_l, big_l
+
+
+    # --- RTEN1 through the reference's sla2::rten (tensor_io.hpp), reference library only ---
+    def rten_save(self, path, a):
+        a = np.ascontiguousarray(a)
+        rows, cols = (a.shape if a.ndim == 2 else (0, a.shape[0]))
+        _check(getattr(self, "_rten_save_" + self._sfx(a.dtype))(str(path).encode(), rows, cols, a))
+
+    def rten_load(self, path, shape, dtype=np.float32):
+        out = np.empty(shape, dtype)
+        rows, cols = (shape if len(shape) == 2 else (0, shape[0]))
+        _check(getattr(self, "_rten_load_" + self._sfx(dtype))(str(path).encode(), rows, cols, out))
+        return out
 
 
 class OracleError(Exception):
