@@ -175,6 +175,9 @@ bool make_map3(CUtensorMap* out, const void* ptr, uint64_t heads, uint64_t rows,
 }
 
 // ---------------------------------------------------------------- geometry + workspace
+#ifndef SLA2_HT_PER
+#define SLA2_HT_PER 22
+#endif
 struct Geo {
     int64_t B, H, BH, N, d, bq, bk, tm, tn, kappa;
     bool bf16, quant;
@@ -196,9 +199,15 @@ Geo geometry(const sla2_fwd_params* p) {
     g.kappa = sla2_topk_budget(p->k_percent, g.tn);
     g.bf16 = p->dtype == SLA2_BF16;
     g.quant = p->quant == SLA2_QUANT_INT8;
-    const int per = g.bf16 ? 16 : 0;
-    if (g.bf16) g.nchunk = (int)((g.tn + per - 1) / per);
-    else g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
+    if (g.bf16) {
+        // Htot partial chunks of 22 key blocks (kphi_htot_kernel, 2 CTAs per SM): at cfg2, 12 heads
+        // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
+        // the output) is bit-identical however many heads share a call.
+        constexpr int64_t per = SLA2_HT_PER;
+        g.nchunk = (int)((g.tn + per - 1) / per);
+    } else {
+        g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
+    }
     return g;
 }
 
@@ -217,6 +226,8 @@ struct Carver {
 struct Workspace {
     float* mu;
     double* mu_part;
+    float* mu_lin;        // the linear branch's mean (parallel, tolerance-level), bf16 path
+    double* mu_lin_part;
     float* qp;
     float* kp;
     float* qbar;
@@ -240,6 +251,8 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     Workspace t{};
     t.mu = c.take<float>(g.BH * g.d);
     t.mu_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
+    t.mu_lin = c.take<float>(g.BH * g.d);
+    t.mu_lin_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
     t.qp = c.take<float>(g.BH * g.tm * g.d);
     t.kp = c.take<float>(g.BH * ((g.tn + 3) & ~int64_t(3)) * g.d);  // transposed rows padded to 4 keys
     t.qbar = c.take<float>(g.BH * g.tm * g.d);
@@ -398,6 +411,7 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
+    cudaEvent_t early = nullptr;  // fork the linear precompute here, with its own parallel mean
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
     float* kbar = nullptr;
@@ -442,7 +456,14 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.tm_v = &mv;
     la.tm_k = (g.bf16 && g.d == 128 && g.bk == 64) ? &mk : nullptr;
     cudaEvent_t dep = plan.dep;
-    if (plan.kprep) {
+    if (plan.early) {
+        // phi(K~) only feeds the linear branch (tolerance 1e-2): it smooths with a parallel fp64
+        // mean (a few ulps from the serial one) and starts with the call, beside the serial
+        // column mean, instead of after it. The router keeps the exact mean (bit-exact mask).
+        la.mu = w.mu_lin;
+        la.phik_ready = false;
+        dep = plan.early;
+    } else if (plan.kprep) {
         thread_local cudaEvent_t ev_k = nullptr;
         if (!ev_k) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming));
         // fork at mu: phi(K~), z_j and Htot on the linear stream, beside the router's pooled
@@ -455,16 +476,27 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         thread_local cudaStream_t lin = nullptr;
         thread_local cudaEvent_t lin_done = nullptr;
         if (!lin) {
-            SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&lin, cudaStreamNonBlocking));
+            // lowest priority: the block scheduler serves the router (the critical path) first;
+            // the linear precompute has slack
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            SLA2_CUDA_TRY(cudaStreamCreateWithPriority(&lin, cudaStreamNonBlocking, lo));
             SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
         }
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
+        if (plan.early)
+            SLA2_CUDA_TRY(launch_colmean_fast(k, g.bf16, w.mu_lin_part, w.mu_lin, (int)g.BH, (int)g.N, (int)g.d, lin,
+                                              &g_launches));
         if (plan.kprep && la.phik_ready) SLA2_CUDA_TRY(launch_kphi(la, lin, &g_launches));
+#ifndef SLA2_EXP_NOLIN  // experiment only: router timeline without the concurrent linear precompute
         SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
+#endif
         mark(8, lin);
         SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
         if (plan.kprep) {
-            SLA2_CUDA_TRY(launch_kpool(la, plan.kbar, st, &g_launches));
+            LinearLaunch lk = la;  // the router's pooled keys: always the exact serial mean
+            lk.mu = p->smooth ? w.mu : nullptr;
+            SLA2_CUDA_TRY(launch_kpool(lk, plan.kbar, st, &g_launches));
             mark(6, st);
         }
         if (plan.between) {
@@ -655,8 +687,19 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);
         ra.kbar_ready = true;
         ra.phiq_out = w.phiq;  // phi(Q) on the query side, beside the serial column mean
-        SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         LinPlan plan;
+#ifdef SLA2_EARLY_LIN
+        // Experiment (measured slower, 0.649-0.708 vs 0.632 ms at cfg2): start the linear
+        // precompute with the call, on its own parallel mean. Its CTAs then hold the SMs the
+        // serial column mean and the router need, and the critical path grows.
+        thread_local cudaEvent_t ev_start = nullptr;
+        if (g.bf16 && p->smooth) {
+            if (!ev_start) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+            SLA2_CUDA_TRY(cudaEventRecord(ev_start, st));
+            plan.early = ev_start;
+        }
+#endif
+        SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;
         plan.phiq_ready = w.phiq != nullptr;
         plan.kbar = w.kbar;

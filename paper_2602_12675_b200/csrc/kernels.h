@@ -40,6 +40,9 @@ cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches)
 // pooling/projection; back = key-side pooling (unless kbar_ready)/projection + scores/top-k.
 cudaError_t launch_router_front(const RouterLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_router_back(const RouterLaunch& a, cudaStream_t st, int* launches);
+// parallel fp64 column mean (not the reference's serial order): the linear branch's mu
+cudaError_t launch_colmean_fast(const void* k, bool bf16, double* part, float* mu, int BH, int N, int d,
+                                cudaStream_t st, int* launches);
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
                            cudaStream_t st, int* launches);
 cudaError_t launch_topk_only(const float* pc, int BH, int tm, int tn, int kappa, uint8_t* mask, int32_t* idx,

@@ -1031,6 +1031,20 @@ cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches)
     return e != cudaSuccess ? e : launch_router_back(a, st, launches);
 }
 
+cudaError_t launch_colmean_fast(const void* k, bool bf16, double* part, float* mu, int BH, int N, int d,
+                                cudaStream_t st, int* launches) {
+    // parallel column mean (fp64 partial sums, one rounding): within a few ulps of the serial
+    // mean, for the linear branch only (tolerance-level); the router keeps the exact serial mean
+    const int rows_per = 256, nch = (N + rows_per - 1) / rows_per;
+    if (bf16)
+        colmean_partial_kernel<__nv_bfloat16><<<dim3(nch, BH), d, 0, st>>>((const __nv_bfloat16*)k, part, N, d, rows_per);
+    else
+        colmean_partial_kernel<float><<<dim3(nch, BH), d, 0, st>>>((const float*)k, part, N, d, rows_per);
+    colmean_finish_kernel<<<BH, d, 0, st>>>(part, mu, nch, N, d);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
                            cudaStream_t st, int* launches) {
     if (bf16) colmean_t<__nv_bfloat16>(k, tmk, mu, BH, N, d, st, launches);
