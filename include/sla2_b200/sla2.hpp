@@ -393,6 +393,60 @@ inline std::pair<Matrix<float>, SLA2ForwardSaved<float>> sla2_forward_blockwise(
     return {b200::download_as(dout, n, d, p), std::move(saved)};
 }
 
+// ------------------------------------------------------------------ backward (attention.hpp:562-809)
+template <class T>
+struct SLA2Gradients {
+    Matrix<T> dq, dk, dv;
+    Vector<T> drho;
+    Matrix<T> dproj_q, dproj_k;  // stage-1 soft routing only: not on this path (left empty)
+};
+
+// sla2_backward on the hard-routing path (the stage-2 / QAT fine-tuning backward): full
+// precision on the device from the forward's saved O_s, O_l, L and the mask. d, bq, bk <= 64.
+inline SLA2Gradients<float> sla2_backward(const SLA2ForwardSaved<float>& saved, const AttentionInputs<float>& inputs,
+                                          const MixRatio<float>& alpha, const Matrix<float>& d_out) {
+    inputs.validate();
+    const std::size_t n = inputs.seq_len(), d = inputs.head_dim(), tm = inputs.tm(), tn = inputs.tn();
+    if (saved.o_s.rows() != n || saved.o_s.cols() != d || saved.big_l.size() != n)
+        throw contract_error("sla2_backward: saved state missing or inconsistent");  // attention.hpp:620-622
+    if (!d_out.same_shape(saved.o_s)) throw shape_error("sla2_backward: d_out shape mismatch");
+    if (!saved.hard())
+        throw contract_error("sla2_backward: SoftMask routing (stage-1 training) is not on the B200 path");
+    if (alpha.rho.size() != tm) throw shape_error("sla2_backward: rho length != tm");
+    const BlockMask& mask = std::get<BlockMask>(saved.routing);
+    sla2_fwd_params p = b200::params(n, d, inputs.bq, inputs.bk, 100.0, false, saved.smoothed);
+    p.dtype = SLA2_F32;  // the backward is full precision
+    const size_t ws = sla2_backward_workspace_size(&p);
+    if (ws == 0) b200::check(sla2_backward(&p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                           nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr));
+    const size_t nd = n * d * 4;
+    b200::DeviceBuffer dq(nd), dk(nd), dv(nd), ddo(nd), dos(nd), dol(nd), dl(n * 4), drho(tm * 4), dmask(tm * tn);
+    b200::DeviceBuffer gq(nd), gk(nd), gv(nd), grho(tm * 4), dws(ws);
+    dq.upload(inputs.q.data().data(), nd);
+    dk.upload(inputs.k.data().data(), nd);
+    dv.upload(inputs.v.data().data(), nd);
+    ddo.upload(d_out.data().data(), nd);
+    dos.upload(saved.o_s.data().data(), nd);
+    dol.upload(saved.o_l.data().data(), nd);
+    dl.upload(saved.big_l.data().data(), n * 4);
+    drho.upload(alpha.rho.data().data(), tm * 4);
+    dmask.upload(mask.bits.data(), tm * tn);
+    b200::check(sla2_backward(&p, dq.p, dk.p, dv.p, drho.as<float>(), dmask.as<uint8_t>(), dos.as<float>(),
+                              dol.as<float>(), dl.as<float>(), ddo.p, gq.p, gk.p, gv.p, grho.as<float>(), dws.p, ws,
+                              nullptr));
+    b200::cuda_check(cudaDeviceSynchronize(), "sla2_backward");
+    SLA2Gradients<float> g;
+    g.dq = Matrix<float>(n, d);
+    g.dk = Matrix<float>(n, d);
+    g.dv = Matrix<float>(n, d);
+    g.drho = Vector<float>(tm);
+    gq.download(g.dq.data().data(), nd);
+    gk.download(g.dk.data().data(), nd);
+    gv.download(g.dv.data().data(), nd);
+    grho.download(g.drho.data().data(), tm * 4);
+    return g;
+}
+
 // Tape::sla2_attention's forward composition (tape.hpp:263-272) on the device:
 // smooth_k -> block_scores(q, K~) -> hard_topk -> sla2_forward_blockwise.
 inline Matrix<float> sla2_attention(const Matrix<float>& q, const Matrix<float>& k, const Matrix<float>& v,

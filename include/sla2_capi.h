@@ -142,6 +142,22 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * SLA2 backward with hard routing (sla2_backward, attention.hpp:610-809; the stage-2 / QAT
+ * fine-tuning path). Full precision whatever the forward was (the QAT contract):
+ * fp32 q, k, v, d_out [B,H,N,d]; the routing mask [B,H,tm,tn] (u8, every row keeps a block);
+ * rho [H,tm]; the forward's saved o_s, o_l [B,H,N,d] and big_l [B,H,N] (sla2_forward with
+ * `saved`). Writes dq, dk, dv [B,H,N,d] and drho [B,H,tm] (per (b,h); sum over b for the
+ * shared per-head logits). params: dtype SLA2_F32, d <= 64, bq <= 64, bk <= 64, N divisible,
+ * tm <= 1024; smooth as in the forward. SoftMask routing (stage 1) is not on this path.
+ * The workspace is sla2_backward_workspace_size(p) bytes.
+ */
+size_t sla2_backward_workspace_size(const sla2_fwd_params* p);
+sla2_status sla2_backward(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
+                          const uint8_t* mask, const float* o_s, const float* o_l, const float* big_l,
+                          const void* d_out, void* dq, void* dk, void* dv, float* drho, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/*
  * Host-buffer forward: the reference's call shape (inputs and outputs in host memory).
  * Copies q/k/v/proj/rho host->device, runs sla2_forward on an internal stream with an
  * internally cached workspace, copies out (and the optional mask) back, synchronizes.

@@ -152,6 +152,28 @@ int attention_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,
     } catch (const std::exception& e) { return classify(e); }
 }
 
+template <class T>
+int backward_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, std::size_t bq, std::size_t bk,
+              const std::uint8_t* mask, const T* rho, int smooth, const T* d_out, T* dq, T* dk, T* dv, T* drho,
+              T* o_s, T* o_l, T* big_l) {
+    try {
+        AttentionInputs<T> in{wrap(q, n, d), wrap(k, n, d), wrap(v, n, d), bq, bk};
+        MixRatio<T> mix{Vector<T>(std::vector<T>(rho, rho + n / bq))};
+        Routing<T> routing{wrap_mask(mask, n / bq, n / bk)};
+        auto fwd = sla2_forward_blockwise(in, routing, mix, nullptr, smooth != 0);
+        const SLA2ForwardSaved<T>& saved = fwd.second;
+        SLA2Gradients<T> g = sla2_backward(saved, in, mix, wrap(d_out, n, d));
+        copy_out(g.dq, dq);
+        copy_out(g.dk, dk);
+        copy_out(g.dv, dv);
+        std::memcpy(drho, g.drho.data().data(), sizeof(T) * (n / bq));
+        copy_out(saved.o_s, o_s);
+        copy_out(saved.o_l, o_l);
+        if (big_l) std::memcpy(big_l, saved.big_l.data().data(), sizeof(T) * n);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
 }  // namespace
 
 extern "C" {
@@ -205,6 +227,18 @@ extern "C" {
 
 SLA2R_INST(float, f)
 SLA2R_INST(double, d)
+
+// attention.hpp:610-809 on the reference's own forward state (sla2_forward_blockwise, hard mask)
+#define SLA2R_BWD(T, S)                                                                           \
+    int sla2r_backward_##S(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,     \
+                           std::size_t bq, std::size_t bk, const std::uint8_t* mask, const T* rho, \
+                           int smooth, const T* d_out, T* dq, T* dk, T* dv, T* drho, T* o_s,      \
+                           T* o_l, T* big_l) {                                                   \
+        return backward_<T>(q, k, v, n, d, bq, bk, mask, rho, smooth, d_out, dq, dk, dv, drho, o_s, \
+                            o_l, big_l);                                                          \
+    }
+SLA2R_BWD(float, f)
+SLA2R_BWD(double, d)
 
 // RTEN1 through the reference's own sla2::rten (tensor_io.hpp): rank-2 save / load (rank 1 when
 // rows == 0), so the exchange format is checked against the reference's writer and reader.

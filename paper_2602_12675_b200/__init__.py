@@ -96,6 +96,8 @@ def lib():
         "sla2_sparse_fwd": ([P, vp, vp, vp, vp, vp, vp, C.POINTER(_Saved), vp, sz, vp], C.c_int),
         "sla2_dense_fwd": ([P, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_forward_host": ([P, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "sla2_backward_workspace_size": ([P], sz),
+        "sla2_backward": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_last_error": ([], C.c_char_p),
         "sla2_last_launch_count": ([], C.c_int32),
         "sla2_version": ([], C.c_char_p),
@@ -357,6 +359,31 @@ def sla2_forward_blockwise(q, k, v, mask, rho, *, bq=128, bk=64, quant=False, sm
                                  _ptr(mask.contiguous().to(torch.uint8)), _ptr(out),
                                  C.byref(sv) if sv is not None else None, _ptr(ws), ws.numel(), _stream(dev)))
     return (out, svs) if saved else out
+
+
+def sla2_backward(q, k, v, d_out, rho, mask, saved, *, bq=64, bk=64, smooth=True):
+    """attention.hpp:610-809 with hard routing (the stage-2 / QAT fine-tuning backward), on the
+    device: fp32 q, k, v, d_out [B,H,N,d]; mask [B,H,tm,tn] u8 (the forward's routing); rho
+    [H,tm]; `saved` = the dict forward(..., saved=True) returns (o_s, o_l, big_l). Returns
+    {"dq", "dk", "dv", "drho" [B,H,tm]}. Full precision whatever the forward was."""
+    import torch
+    _check_like(q, k, v, d_out)
+    if q.dtype != torch.float32:
+        raise ContractError("sla2_backward: fp32 tensors (the backward is full precision)")
+    p = _params_from(q, bq, bk, 100.0, False, smooth, True)
+    cp = p.c()
+    n = int(lib().sla2_backward_workspace_size(C.byref(cp)))
+    if n == 0:
+        _raise(lib().sla2_backward(C.byref(cp), *([None] * 14), 0, None))  # raises the validation error
+    dev = q.device
+    ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    drho = torch.empty((p.B, p.H, p.tm), dtype=torch.float32, device=dev)
+    rc = lib().sla2_backward(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()), _ptr(mask.contiguous()),
+                             _ptr(saved["o_s"]), _ptr(saved["o_l"]), _ptr(saved["big_l"]), _ptr(d_out), _ptr(dq),
+                             _ptr(dk), _ptr(dv), _ptr(drho), _ptr(ws), n, _stream(dev))
+    _raise(rc)
+    return {"dq": dq, "dk": dk, "dv": dv, "drho": drho}
 
 
 def sla2_attention(q, k, v, rho, proj_q, proj_k, bq=128, bk=64, k_percent=3.0, quant=False, smooth=True):

@@ -833,6 +833,89 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
     return SLA2_OK;
 }
 
+// ---------------------------------------------------------------- backward (attention.hpp:610-809)
+static sla2_status check_backward(const sla2_fwd_params* p) {
+    sla2_status s = check_common(p);
+    if (s != SLA2_OK) return s;
+    if (p->dtype != SLA2_F32)
+        return fail(SLA2_CONTRACT_ERROR, "sla2_backward: fp32 tensors (the backward is full precision, SPEC.md:358)");
+    if (p->N % p->bq != 0 || p->N % p->bk != 0)
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");  // attention.hpp:39-41
+    if (p->d > 64 || p->bq > 64 || p->bk > 64 || p->N / p->bq > 1024)
+        return fail(SLA2_CONTRACT_ERROR, "sla2_backward: d, bq, bk <= 64 and tm <= 1024 on this path");
+    return SLA2_OK;
+}
+
+static size_t carve_backward(const Geo& g, void* base, BackwardLaunch* a) {
+    Carver c{reinterpret_cast<uint8_t*>(base)};
+    BackwardLaunch t{};
+    t.mu = c.take<float>(g.BH * g.d);
+    t.phik = c.take<float>(g.BH * g.N * g.d);
+    t.h = c.take<float>(g.BH * g.tn * g.d * g.d);
+    t.z = c.take<float>(g.BH * g.tn * g.d);
+    t.htot = c.take<float>(g.BH * g.d * g.d);
+    t.ztot = c.take<float>(g.BH * g.d);
+    t.dh = c.take<float>(g.BH * g.tm * g.d * g.d);
+    t.dz = c.take<float>(g.BH * g.tm * g.d);
+    t.dsr = c.take<float>(g.BH * g.N);
+    if (a) {
+        a->mu = t.mu; a->phik = t.phik; a->h = t.h; a->z = t.z; a->htot = t.htot; a->ztot = t.ztot;
+        a->dh = t.dh; a->dz = t.dz; a->dsr = t.dsr;
+    }
+    return c.off + 256;
+}
+
+size_t sla2_backward_workspace_size(const sla2_fwd_params* p) {
+    if (check_backward(p) != SLA2_OK) return 0;
+    return carve_backward(geometry(p), nullptr, nullptr);
+}
+
+sla2_status sla2_backward(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
+                          const uint8_t* mask, const float* o_s, const float* o_l, const float* big_l,
+                          const void* d_out, void* dq, void* dk, void* dv, float* drho, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = check_backward(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!q || !k || !v || !rho || !mask || !o_s || !o_l || !big_l || !d_out || !dq || !dk || !dv || !drho)
+        return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    if (!workspace || workspace_bytes < carve_backward(g, nullptr, nullptr))
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_backward_workspace_size)");
+    cudaStream_t st = (cudaStream_t)stream;
+    // every row keeps a block (the forward's own precondition, attention.hpp:442-447)
+    CUtensorMap unused;
+    (void)unused;
+    BackwardLaunch a{};
+    carve_backward(g, workspace, &a);
+    a.BH = g.BH;
+    a.H = g.H;
+    a.N = (int)g.N;
+    a.d = (int)g.d;
+    a.bq = (int)g.bq;
+    a.bk = (int)g.bk;
+    a.tm = (int)g.tm;
+    a.tn = (int)g.tn;
+    a.smooth = p->smooth;
+    a.inv_sqrt_d = inv_sqrt(g.d);
+    a.q = (const float*)q;
+    a.k = (const float*)k;
+    a.v = (const float*)v;
+    a.d_out = (const float*)d_out;
+    a.o_s = o_s;
+    a.o_l = o_l;
+    a.big_l = big_l;
+    a.rho = rho;
+    a.mask = mask;
+    a.dq = (float*)dq;
+    a.dk = (float*)dk;
+    a.dv = (float*)dv;
+    a.drho = drho;
+    SLA2_CUDA_TRY(launch_backward(a, st, &g_launches));
+    return SLA2_OK;
+}
+
 sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
                               const float* proj_q, const float* proj_k, const float* rho, void* out,
                               uint8_t* mask_out) {

@@ -149,4 +149,18 @@ struct SparseI8Launch {
 };
 cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* launches);
 
+// ---- backward (backward.cu): sla2_backward, hard routing, fp32, d / bq / bk <= 64
+struct BackwardLaunch {
+    int64_t BH, H;
+    int N, d, bq, bk, tm, tn;
+    int smooth;
+    float inv_sqrt_d;
+    const float *q, *k, *v, *d_out, *o_s, *o_l, *big_l, *rho;
+    const uint8_t* mask;  // [BH][tm][tn]
+    float *dq, *dk, *dv, *drho;
+    // workspace
+    float *mu, *phik, *h, *z, *htot, *ztot, *dh, *dz, *dsr;
+};
+cudaError_t launch_backward(const BackwardLaunch& a, cudaStream_t st, int* launches);
+
 }  // namespace sla2dev

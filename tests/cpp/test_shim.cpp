@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cmath>
 // test_shim.cpp -- the reference's own forward-path tests (proj/tests/test_router.cpp,
 // test_quant.cpp, test_attention.cpp), re-expressed against the drop-in header
 // include/sla2_b200/sla2.hpp, with the CPU oracle (oracle/liboracle.so, TEST INFRASTRUCTURE)
@@ -197,8 +199,50 @@ static void rten_tests() {
     std::remove(f.c_str());
 }
 
+// sla2_backward (attention.hpp:610-809) through the header: on a full mask alpha is forced to 1,
+// so dV = P^T dO with P the row softmax of Q K~^T / sqrt(d) (host restatement, double).
+static void backward_tests() {
+    const std::size_t n = 128, d = 16, b = 32;
+    Matrix<float> q = gaussian(n, d, 21), k = gaussian(n, d, 22), v = gaussian(n, d, 23), dout = gaussian(n, d, 24);
+    AttentionInputs<float> in{q, k, v, b, b};
+    MixRatio<float> mix{Vector<float>(n / b, 0.3f)};
+    BlockMask full = BlockMask::zeros(n / b, n / b);
+    for (auto& x : full.bits) x = 1;
+    full.keep_per_row = n / b;
+    b200::precision() = b200::Precision::fp32;
+    auto fwd = sla2_forward_blockwise(in, Routing<float>{full}, mix);
+    SLA2Gradients<float> g = sla2_backward(fwd.second, in, mix, dout);
+    std::vector<double> mu(d, 0.0);
+    for (std::size_t r = 0; r < n; ++r)
+        for (std::size_t c = 0; c < d; ++c) mu[c] += k(r, c) / (double)n;
+    double worst = 0.0, scale = 0.0;
+    std::vector<double> p(n);
+    std::vector<double> dv(n * d, 0.0);
+    for (std::size_t r = 0; r < n; ++r) {
+        double mx = -1e300, s = 0.0;
+        for (std::size_t t = 0; t < n; ++t) {
+            double acc = 0.0;
+            for (std::size_t f = 0; f < d; ++f) acc += (double)q(r, f) * ((double)k(t, f) - mu[f]);
+            p[t] = acc / std::sqrt((double)d);
+            mx = std::max(mx, p[t]);
+        }
+        for (std::size_t t = 0; t < n; ++t) s += (p[t] = std::exp(p[t] - mx));
+        for (std::size_t t = 0; t < n; ++t)
+            for (std::size_t c = 0; c < d; ++c) dv[t * d + c] += p[t] / s * dout(r, c);
+    }
+    for (std::size_t e = 0; e < n * d; ++e) {
+        worst = std::max(worst, std::abs(dv[e] - (double)g.dv.data()[e]));
+        scale = std::max(scale, std::abs(dv[e]));
+    }
+    EXPECT(worst <= 1e-4 * scale);
+    bool all_zero = true;
+    for (std::size_t i = 0; i < n / b; ++i) all_zero &= g.drho[i] == 0.0f;
+    EXPECT(all_zero);  // full rows: alpha forced to 1, no rho gradient (attention.hpp:648-651)
+}
+
 int main() {
     rten_tests();
+    backward_tests();
     hard_topk_kats();
     block_scores_tests();
     smooth_k_tests();

@@ -70,6 +70,8 @@ class Oracle:
         self._sig("topk_budget", [C.c_double, _sz], _sz)
         if prefix == "sla2r_":
             for s, fp in (("f", _f32p), ("d", _f64p)):
+                self._sig(f"backward_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, _u8p, fp, C.c_int, fp, fp, fp, fp, fp,
+                                            fp, fp, fp], C.c_int)
                 self._sig(f"rten_save_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
                 self._sig(f"rten_load_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
         if prefix == "sla2o_":
@@ -203,6 +205,20 @@ class Oracle:
         _check(rc)
         return out, mask, o_s, o_l, big_l
 
+
+    def backward(self, q, k, v, bq, bk, mask, rho, d_out, smooth=True):
+        """sla2_backward (attention.hpp:610-809) on the reference's own forward state, hard mask
+        (reference library only). Returns dq, dk, dv, drho, o_s, o_l, big_l."""
+        n, d = q.shape
+        dt = q.dtype
+        outs = [np.empty((n, d), dt) for _ in range(3)] + [np.empty(n // bq, dt)] + \
+            [np.empty((n, d), dt) for _ in range(2)] + [np.empty(n, dt)]
+        rc = getattr(self, "_backward_" + self._sfx(dt))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v), n, d, bq, bk,
+            np.ascontiguousarray(mask, dtype=np.uint8), np.ascontiguousarray(rho, dtype=dt), int(smooth),
+            np.ascontiguousarray(d_out, dtype=dt), *outs)
+        _check(rc)
+        return tuple(outs)
 
     # --- RTEN1 through the reference's sla2::rten (tensor_io.hpp), reference library only ---
     def rten_save(self, path, a):
