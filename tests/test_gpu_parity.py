@@ -114,6 +114,22 @@ def test_forward_host_matches_device(cuda, quant):
     assert rel_err(out_h.float().numpy()[1, 2], r)[0] <= BF16_TOL
 
 
+def test_captured_forward_matches_eager(cuda):
+    """CapturedForward (the forward as one CUDA graph) replays to exactly the eager result,
+    and picks up new inputs written into the captured tensors."""
+    torch = _torch()
+    B, H, N, d = 1, 2, 4096, 128
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 23)
+    dev = [to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)] + [to_dev(x, torch.float32, cuda) for x in (pq, pk, rho)]
+    eager = sla2.forward(*dev, k_percent=3.0).clone()
+    g = sla2.CapturedForward(*dev, k_percent=3.0)
+    assert torch.equal(g(), eager)
+    q2, k2, v2 = make_inputs(B, H, N, d, 24)[:3]
+    for t, x in zip(dev[:3], (q2, k2, v2)):
+        t.copy_(to_dev(x, torch.bfloat16, cuda))
+    assert torch.equal(g(), sla2.forward(*dev, k_percent=3.0))
+
+
 # ----------------------------------------------------------------------------- INT8 QAT forward
 @pytest.mark.parametrize("N,H,k_percent,seed", [(4096, 2, 3.0, 51), (8192, 1, 10.0, 52), (2048, 1, 100.0, 53)])
 def test_forward_qat_vs_oracle(cuda, N, H, k_percent, seed):
