@@ -163,7 +163,17 @@ __global__ void __launch_bounds__(256, 1)
     const bool full_row = dense || (nb == p.tn);
     const bool linear = !full_row;
 
+    uint8_t* sQ = smem + OFF_Q;
+    auto sKp = [&](int s) { return smem + OFF_K + s * KP_BYTES; };
+    auto sV = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES; };
+    auto sPh = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES + TILE_BYTES; };
+    auto kblock = [&](int j) { return dense ? j : idx[j]; };
+    const uint32_t v_tx = dense ? TILE_BYTES : 2 * TILE_BYTES;  // V (+ phi(K~)) per stage
+    constexpr int NV0 = 2;  // V stages thread 0 fills before the CTA-wide barrier
+
     if (threadIdx.x == 0) {
+        // the kept-block indices of the first pair: their global loads overlap the barrier setup
+        int jk[2] = {kblock(0), nb > 1 ? kblock(1) : 0};
         mbar_init(&bar_q, 1);
         mbar_init(&bar_qt, 128);  // Q copied into TMEM by the softmax warps
         mbar_init(&bar_qk_done, 1);
@@ -188,6 +198,30 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(&bar_lin_ready, 256);
         mbar_init(&bar_lin_done, 1);
         fence_barrier_init();
+        // Q, the first K pair and the first V / phi(K~) stages go out before the TMEM allocation
+        // and the CTA barrier (they need only the initialized mbarriers): ~0.5 us off the prologue
+        const int qrow = i * BQ, hz = (int)bh;
+        const uint64_t pol_keep = policy_evict_last();
+        mbar_arrive_expect_tx(&bar_q, Q_BYTES);
+        tma_load_3d(sQ, &tmQ, 0, qrow, hz, &bar_q);
+        tma_load_3d(sQ + 8192, &tmQ, 0, qrow + 64, hz, &bar_q);
+        tma_load_3d(sQ + 16384, &tmQ, 64, qrow, hz, &bar_q);
+        tma_load_3d(sQ + 24576, &tmQ, 64, qrow + 64, hz, &bar_q);
+        const int cnt0 = min(2, nb);
+        mbar_arrive_expect_tx(&bar_k_full[0], cnt0 * TILE_BYTES);
+        for (int b = 0; b < cnt0; ++b) {
+            tma_load_3d_hint(sKp(0) + b * 8192, &tmK, 0, jk[b] * BK, hz, &bar_k_full[0], pol_keep);
+            tma_load_3d_hint(sKp(0) + 16384 + b * 8192, &tmK, 64, jk[b] * BK, hz, &bar_k_full[0], pol_keep);
+        }
+        for (int j = 0; j < NV0 && j < nb; ++j) {
+            mbar_arrive_expect_tx(&bar_v_full[j], v_tx);
+            tma_load_3d_hint(sV(j), &tmV, 0, jk[j] * BK, hz, &bar_v_full[j], pol_keep);
+            tma_load_3d_hint(sV(j) + 8192, &tmV, 64, jk[j] * BK, hz, &bar_v_full[j], pol_keep);
+            if (!dense) {
+                tma_load_3d_hint(sPh(j), &tmPhi, 0, jk[j] * BK, hz, &bar_v_full[j], pol_keep);
+                tma_load_3d_hint(sPh(j) + 8192, &tmPhi, 64, jk[j] * BK, hz, &bar_v_full[j], pol_keep);
+            }
+        }
     }
     if (warp == 2) tmem_alloc(&tmem_base_sh, 512);
     tc_fence_before();
@@ -196,15 +230,10 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tmem = tmem_base_sh;
     if (threadIdx.x == 0) SLA2_TR(0);
 
-    uint8_t* sQ = smem + OFF_Q;
-    auto sKp = [&](int s) { return smem + OFF_K + s * KP_BYTES; };
-    auto sV = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES; };
-    auto sPh = [&](int s) { return smem + OFF_V + s * 2 * TILE_BYTES + TILE_BYTES; };
     // epilogue buffers in V stages: Htot goes where block nb would have gone (loaded by the V
     // producer once that stage drains), Hc into the next one (free once every PV is done)
     uint8_t* sHt = sV(nb % NSV);
     uint8_t* sHc = sV((nb + 1) % NSV);
-    auto kblock = [&](int j) { return dense ? j : idx[j]; };
 
     if (warp == 0) {
         // ===================== TMA producer: Q, K pair ring =====================
@@ -213,12 +242,8 @@ __global__ void __launch_bounds__(256, 1)
             tma_prefetch_desc(&tmK);
             const uint64_t pol_keep = policy_evict_last();
             const int qrow = i * BQ, hz = (int)bh;  // 3-D maps: (column, row in head, head)
-            mbar_arrive_expect_tx(&bar_q, Q_BYTES);
-            tma_load_3d(sQ, &tmQ, 0, qrow, hz, &bar_q);
-            tma_load_3d(sQ + 8192, &tmQ, 0, qrow + 64, hz, &bar_q);
-            tma_load_3d(sQ + 16384, &tmQ, 64, qrow, hz, &bar_q);
-            tma_load_3d(sQ + 24576, &tmQ, 64, qrow + 64, hz, &bar_q);
-            for (int n = 0; n < npair; ++n) {
+            // Q and pair 0 were issued by this thread before the CTA barrier
+            for (int n = 1; n < npair; ++n) {
                 const int s = n % NKP;
                 if (n >= NKP) mbar_wait(&bar_k_empty[s], ((n / NKP) - 1) & 1);
                 const int cnt = min(2, nb - 2 * n);
@@ -259,7 +284,9 @@ __global__ void __launch_bounds__(256, 1)
             const bool ldphi = !dense;
 #endif
             const uint32_t tx = ldphi ? 2 * TILE_BYTES : TILE_BYTES;
-            for (int j = 0; j < nb; ++j) {
+            // stages 0 .. NV0-1 were issued by thread 0 before the CTA barrier (with phi(K~) unless
+            // dense; the SLA2_EXP_NOPHIK experiment loads V only from stage NV0 on)
+            for (int j = NV0; j < nb; ++j) {
                 const int s = j % NSV;
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
                 const int krow = kblock(j) * BK, hz = (int)bh;
