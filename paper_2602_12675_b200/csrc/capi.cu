@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -940,8 +941,15 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
     // one cached device arena and three streams per thread
     thread_local void* arena = nullptr;
     thread_local size_t arena_bytes = 0;
-    thread_local cudaStream_t st = nullptr, up = nullptr, down = nullptr;
-    thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    thread_local cudaStream_t st = nullptr, up = nullptr, up2 = nullptr, down = nullptr;
+    thread_local cudaEvent_t ev_in = nullptr, ev_in2 = nullptr, ev_out = nullptr;
+    // one upload stream: a second one (a head's V beside its K and Q, SLA2_H2D_STREAMS=2)
+    // measured slower, 7.08 vs 6.70 ms at cfg2 -- the copies already run at the link's rate
+    // (~45 GB/s pinned H2D on the box; tools/e2e_ab.py)
+    static const int n_up = [] {
+        const char* e = std::getenv("SLA2_H2D_STREAMS");
+        return (e && std::atoi(e) == 2) ? 2 : 1;
+    }();
     const size_t need = 4 * tensor + 2 * projb + rhob + maskb + wsb + 10 * 256;
     if (need > arena_bytes) {
         if (arena) cudaFree(arena);
@@ -953,8 +961,10 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
     if (!st) {
         SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&up2, cudaStreamNonBlocking));
         SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
         SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_in2, cudaEventDisableTiming));
         SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
     }
     Carver c{reinterpret_cast<uint8_t*>(arena)};
@@ -977,11 +987,16 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
         const size_t o = (size_t)bh * head;
         const int64_t h = bh % g.H;
         // K first: the column mean, the head's latency-bound first stage, needs only K
+        cudaStream_t upv = n_up == 2 ? up2 : up;
         SLA2_CUDA_TRY(cudaMemcpyAsync(dk + o, hk + o, head, cudaMemcpyHostToDevice, up));
         SLA2_CUDA_TRY(cudaMemcpyAsync(dq + o, hq + o, head, cudaMemcpyHostToDevice, up));
-        SLA2_CUDA_TRY(cudaMemcpyAsync(dv + o, hv + o, head, cudaMemcpyHostToDevice, up));
+        SLA2_CUDA_TRY(cudaMemcpyAsync(dv + o, hv + o, head, cudaMemcpyHostToDevice, upv));
         SLA2_CUDA_TRY(cudaEventRecord(ev_in, up));
         SLA2_CUDA_TRY(cudaStreamWaitEvent(st, ev_in, 0));
+        if (n_up == 2) {
+            SLA2_CUDA_TRY(cudaEventRecord(ev_in2, upv));
+            SLA2_CUDA_TRY(cudaStreamWaitEvent(st, ev_in2, 0));
+        }
         uint8_t* hm = mask_out ? dmask + (size_t)bh * head_mask : nullptr;
         s = sla2_forward(&hp, dq + o, dk + o, dv + o, dpq + h * g.d * g.d, dpk + h * g.d * g.d, drho + h * g.tm,
                          dout + o, hm, nullptr, nullptr, dws, wsb, st);
