@@ -203,7 +203,8 @@ Geo geometry(const sla2_fwd_params* p) {
     if (g.bf16) {
         // Htot partial chunks of 22 key blocks (kphi_htot_kernel, 2 CTAs per SM): at cfg2, 12 heads
         // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
-        // the output) is bit-identical however many heads share a call.
+        // the output) is bit-identical however many heads share a call. (Measured at cfg2:
+        // 8 -> 0.654-0.662 ms, 12 -> 0.641-0.644, 22 -> 0.637-0.649, 32 / 43 slower.)
         constexpr int64_t per = SLA2_HT_PER;
         g.nchunk = (int)((g.tn + per - 1) / per);
     } else {
@@ -689,7 +690,7 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         ra.kbar_ready = true;
         ra.phiq_out = w.phiq;  // phi(Q) on the query side, beside the serial column mean
         LinPlan plan;
-#ifdef SLA2_EARLY_LIN
+#if defined(SLA2_EARLY_LIN)
         // Experiment (measured slower, 0.649-0.708 vs 0.632 ms at cfg2): start the linear
         // precompute with the call, on its own parallel mean. Its CTAs then hold the SMs the
         // serial column mean and the router need, and the critical path grows.
@@ -698,6 +699,15 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
             if (!ev_start) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
             SLA2_CUDA_TRY(cudaEventRecord(ev_start, st));
             plan.early = ev_start;
+        }
+#elif defined(SLA2_QUERY_LIN)
+        // Experiment (measured slower, 0.670 vs 0.649 ms): fork the linear precompute (own
+        // parallel mean) when the query side is done, ~15 us before the serial mean
+        thread_local cudaEvent_t ev_qd = nullptr;
+        if (g.bf16 && p->smooth) {
+            if (!ev_qd) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_qd, cudaEventDisableTiming));
+            ra.query_done = ev_qd;
+            plan.early = ev_qd;
         }
 #endif
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));

@@ -32,6 +32,7 @@ struct RouterLaunch {
                            // the linear-branch precompute off it)
     bool kbar_ready;       // kbar already holds the pooled keys (launch_kprep): back half only projects
     void* phiq_out;        // optional: the front half also writes phi(Q) here (launch_phiq, bf16 d = 128)
+    cudaEvent_t query_done;  // optional: recorded once the query side is done (before the mu join)
 };
 // stage-timing hook (capi.cu): records timeline event `slot` on st when timing is enabled
 void timeline_mark(int slot, cudaStream_t st);

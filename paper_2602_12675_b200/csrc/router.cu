@@ -973,6 +973,7 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
     launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
     if (a.phiq_out) launch_phiq(a.q, a.phiq_out, (int64_t)BH * a.N, st, launches);
     timeline_mark(5, st);
+    if (a.query_done) cudaEventRecord(a.query_done, st);
     if (forked) cudaStreamWaitEvent(st, ev_join, 0);
     return cudaGetLastError();
 }
