@@ -158,6 +158,29 @@ sla2_status sla2_backward(const sla2_fwd_params* p, const void* q, const void* k
                           size_t workspace_bytes, void* stream);
 
 /*
+ * Stage-1 soft routing (the router-training path, training.hpp:186-201).
+ *
+ * sla2_soft_topk replaces soft_topk (router.hpp:126-190): per row of pc [B,H,tm,tn] fp32, the
+ * shift lambda_i found by bisection (<= 200 halvings, |row sum - kappa| <= 1e-6, in double) with
+ * values_ij = clamp(sigma(pc_ij / tau + lambda_i), DBL_MIN, 1 - eps/2) cast to fp32; kappa =
+ * sla2_topk_budget(p->k_percent, tn), tau = p->tau. Writes values [B,H,tm,tn] and lambdas
+ * [B,H,tm]. A row that does not converge returns SLA2_NUMERIC_ERROR like the reference's throw
+ * (the check is one device->host read: this call synchronizes `stream`).
+ *
+ * sla2_forward_soft replaces sla2_forward_blockwise with Routing = SoftMask (attention.hpp:
+ * 484-558): every key block j of query block i feeds the sparse branch with weight w_ij =
+ * values_ij and the linear branch with 1 - w_ij; there are no full rows, so out = alpha O_s +
+ * (1 - alpha) O_l. fp32 q, k, v, out [B,H,N,d], values [B,H,tm,tn], rho [H,tm]; saved as in
+ * sla2_forward. params: dtype SLA2_F32, no quant, d, bq, bk <= 64, N divisible; smooth as in
+ * the reference. Workspace: sla2_forward_soft_workspace_size(p) bytes.
+ */
+sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* values, float* lambdas, void* stream);
+size_t sla2_forward_soft_workspace_size(const sla2_fwd_params* p);
+sla2_status sla2_forward_soft(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
+                              const float* values, void* out, const sla2_fwd_saved* saved, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/*
  * Host-buffer forward: the reference's call shape (inputs and outputs in host memory).
  * Copies q/k/v/proj/rho host->device, runs sla2_forward on an internal stream with an
  * internally cached workspace, copies out (and the optional mask) back, synchronizes.

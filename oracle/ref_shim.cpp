@@ -174,6 +174,39 @@ int backward_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, 
     } catch (const std::exception& e) { return classify(e); }
 }
 
+// soft_topk (router.hpp:126-190): values and lambdas of one [tm, tn] score matrix
+template <class T>
+int soft_topk_(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau, T* values, T* lambdas) {
+    try {
+        SoftMask<T> sm = soft_topk(wrap(pc, tm, tn), kp, tau);
+        copy_out(sm.values, values);
+        std::memcpy(lambdas, sm.lambdas.data().data(), sizeof(T) * tm);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
+// sla2_forward_blockwise with Routing = SoftMask (attention.hpp:484-558), caller-given values
+template <class T>
+int forward_soft_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, std::size_t bq,
+                  std::size_t bk, const T* values, const T* rho, int smooth, T* out, T* o_s, T* o_l,
+                  T* big_l) {
+    try {
+        AttentionInputs<T> in{wrap(q, n, d), wrap(k, n, d), wrap(v, n, d), bq, bk};
+        MixRatio<T> mix{Vector<T>(std::vector<T>(rho, rho + n / bq))};
+        SoftMask<T> sm;
+        sm.tm = n / bq;
+        sm.tn = n / bk;
+        sm.values = wrap(values, sm.tm, sm.tn);
+        sm.lambdas = Vector<T>(sm.tm);
+        auto [o, saved] = sla2_forward_blockwise(in, Routing<T>{sm}, mix, nullptr, smooth != 0);
+        copy_out(o, out);
+        copy_out(saved.o_s, o_s);
+        copy_out(saved.o_l, o_l);
+        if (big_l) std::memcpy(big_l, saved.big_l.data().data(), sizeof(T) * n);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
 }  // namespace
 
 extern "C" {
@@ -266,6 +299,19 @@ SLA2R_BWD(double, d)
     }
 SLA2R_RTEN(float, f)
 SLA2R_RTEN(double, d)
+
+#define SLA2R_SOFT(T, S)                                                                          \
+    int sla2r_soft_topk_##S(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau, T* values, \
+                            T* lambdas) {                                                         \
+        return soft_topk_<T>(pc, tm, tn, kp, tau, values, lambdas);                               \
+    }                                                                                             \
+    int sla2r_forward_soft_##S(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,  \
+                               std::size_t bq, std::size_t bk, const T* values, const T* rho,     \
+                               int smooth, T* out, T* o_s, T* o_l, T* big_l) {                    \
+        return forward_soft_<T>(q, k, v, n, d, bq, bk, values, rho, smooth, out, o_s, o_l, big_l); \
+    }
+SLA2R_SOFT(float, f)
+SLA2R_SOFT(double, d)
 
 std::size_t sla2r_topk_budget(double kp, std::size_t tn) { return topk_budget(kp, tn); }
 std::size_t sla2r_max_worker_threads(void) { return max_worker_threads(); }

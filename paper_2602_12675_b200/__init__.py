@@ -97,6 +97,9 @@ def lib():
         "sla2_dense_fwd": ([P, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_forward_host": ([P, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "sla2_backward_workspace_size": ([P], sz),
+        "sla2_soft_topk": ([P, vp, vp, vp, vp], C.c_int),
+        "sla2_forward_soft_workspace_size": ([P], sz),
+        "sla2_forward_soft": ([P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_backward": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_last_error": ([], C.c_char_p),
         "sla2_last_launch_count": ([], C.c_int32),
@@ -409,6 +412,55 @@ def sla2_backward(q, k, v, d_out, rho, mask, saved, *, bq=64, bk=64, smooth=True
                              _ptr(dk), _ptr(dv), _ptr(drho), _ptr(ws), n, _stream(dev))
     _raise(rc)
     return {"dq": dq, "dk": dk, "dv": dv, "drho": drho}
+
+
+def soft_topk(pc, k_percent=3.0, tau=0.1):
+    """soft_topk (router.hpp:126-190) on device: pc [B,H,tm,tn] fp32 -> (values [B,H,tm,tn],
+    lambdas [B,H,tm]); per row the bisected shift lambda with sum_j sigma(pc/tau + lambda) = kappa.
+    Raises NumericError on a row whose bisection does not converge, like the reference."""
+    import torch
+    if pc.dim() != 4 or pc.dtype != torch.float32 or not pc.is_contiguous():
+        raise ContractError("soft_topk: contiguous fp32 scores [B, H, tm, tn]")
+    B, H, tm, tn = pc.shape
+    # only the score geometry is read: N = tm * tn with bq = tn, bk = tm gives tm x tn blocks
+    p = FwdParams(B, H, tm * tn, 1, tn, tm, k_percent, False, False, False, True, tau)
+    cp = p.c()
+    values = torch.empty_like(pc)
+    lambdas = torch.empty((B, H, tm), dtype=torch.float32, device=pc.device)
+    _raise(lib().sla2_soft_topk(C.byref(cp), _ptr(pc), _ptr(values), _ptr(lambdas), _stream(pc.device)))
+    return values, lambdas
+
+
+def forward_soft(q, k, v, rho, values, *, bq=64, bk=64, smooth=True, saved=False):
+    """sla2_forward_blockwise with Routing = SoftMask (attention.hpp:484-558), the stage-1
+    training forward: fp32 q, k, v [B,H,N,d] (d, bq, bk <= 64), rho [H,tm], values [B,H,tm,tn]
+    (soft_topk's). Returns out, or (out, {"o_s", "o_l", "big_l"}) with saved=True."""
+    import torch
+    _check_like(q, k, v)
+    if q.dtype != torch.float32:
+        raise ContractError("sla2_forward_soft: fp32 tensors (the stage-1 training path)")
+    p = _params_from(q, bq, bk, 100.0, False, smooth, True)
+    cp = p.c()
+    n = int(lib().sla2_forward_soft_workspace_size(C.byref(cp)))
+    if n == 0:
+        _raise(lib().sla2_forward_soft(C.byref(cp), *([None] * 8), 0, None))  # raises the validation error
+    dev = q.device
+    if tuple(values.shape) != (p.B, p.H, p.tm, p.tn) or values.dtype != torch.float32:
+        raise ShapeError("sla2_forward_blockwise: soft mask geometry mismatch")  # attention.hpp:438-440
+    if tuple(rho.shape) != (p.H, p.tm):
+        raise ShapeError("sla2_forward_blockwise: rho length != tm")  # attention.hpp:434
+    ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = torch.empty_like(q)
+    sv = None
+    keep = {}
+    if saved:
+        keep = {"o_s": torch.empty_like(q), "o_l": torch.empty_like(q),
+                "big_l": torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=dev)}
+        sv = _Saved(keep["o_s"].data_ptr(), keep["o_l"].data_ptr(), keep["big_l"].data_ptr())
+    _raise(lib().sla2_forward_soft(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()),
+                                   _ptr(values.contiguous()), _ptr(out), C.byref(sv) if sv is not None else None,
+                                   _ptr(ws), n, _stream(dev)))
+    return (out, keep) if saved else out
 
 
 def sla2_attention(q, k, v, rho, proj_q, proj_k, bq=128, bk=64, k_percent=3.0, quant=False, smooth=True):

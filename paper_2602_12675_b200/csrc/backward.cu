@@ -400,6 +400,14 @@ __global__ void bwd_smooth_kernel(float* __restrict__ dk, int N, int d) {
     for (int64_t e = threadIdx.x; e < (int64_t)N * d; e += blockDim.x) dk[bh * N * d + e] -= smean[e % d];
 }
 
+cudaError_t launch_keyblock_linear(const float* k, const float* v, const float* mu, float* phik, float* h, float* z,
+                                   int64_t BH, int N, int d, int bk, cudaStream_t st, int* launches) {
+    if (d > bw::MAXD || bk > bw::MAXB) return cudaErrorInvalidValue;
+    bwd_keyblock_kernel<<<dim3(N / bk, (unsigned)BH), 256, 0, st>>>(k, v, mu, phik, h, z, N, d, bk);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 size_t bwd_sparse_smem() {
     const int ld = bw::MAXD + 1, pl = bw::MAXB + 1;
     return sizeof(float) * (5 * bw::MAXB * ld + 2 * bw::MAXB * pl);

@@ -927,6 +927,104 @@ sla2_status sla2_backward(const sla2_fwd_params* p, const void* q, const void* k
     return SLA2_OK;
 }
 
+// ---------------------------------------------------------------- stage-1 soft routing
+// soft_topk (router.hpp:126-190) and sla2_forward_blockwise with a SoftMask (attention.hpp:484-558)
+static sla2_status check_soft(const sla2_fwd_params* p, const char* who) {
+    sla2_status s = check_common(p);
+    if (s != SLA2_OK) return s;
+    if (p->dtype != SLA2_F32 || p->quant != SLA2_QUANT_NONE)
+        return fail(SLA2_CONTRACT_ERROR, std::string(who) + ": fp32 without quantization (the stage-1 training path)");
+    if (p->N % p->bq != 0 || p->N % p->bk != 0)
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");  // attention.hpp:39-41
+    if (p->d > 64 || p->bq > 64 || p->bk > 64)
+        return fail(SLA2_CONTRACT_ERROR, std::string(who) + ": d, bq, bk <= 64 on this path");
+    return SLA2_OK;
+}
+
+sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* values, float* lambdas, void* stream) {
+    g_launches = 0;
+    sla2_status s = check_common(p);  // only the score geometry tm x tn matters here
+    if (s != SLA2_OK) return s;
+    if (p->N % p->bq != 0 || p->N % p->bk != 0)
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!pc || !values || !lambdas) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    thread_local int* dfail = nullptr;
+    if (!dfail) SLA2_CUDA_TRY(cudaMalloc(&dfail, sizeof(int)));
+    SLA2_CUDA_TRY(cudaMemsetAsync(dfail, 0, sizeof(int), st));
+    const double kappa = (double)sla2_topk_budget(p->k_percent, g.tn);
+    SLA2_CUDA_TRY(launch_soft_topk(pc, (int)(g.BH * g.tm), (int)g.tn, kappa, (double)p->tau, values, lambdas, dfail,
+                                   st, &g_launches));
+    int hfail = 0;  // the reference throws on a row that does not converge: one D2H read
+    SLA2_CUDA_TRY(cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SLA2_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hfail) return fail(SLA2_NUMERIC_ERROR, "soft_topk: bisection did not converge");
+    return SLA2_OK;
+}
+
+static size_t carve_soft(const Geo& g, void* base, SoftLaunch* a, float** mu, float** phik) {
+    Carver c{reinterpret_cast<uint8_t*>(base)};
+    float* m = c.take<float>(g.BH * g.d);
+    float* pk = c.take<float>(g.BH * g.N * g.d);
+    float* h = c.take<float>(g.BH * g.tn * g.d * g.d);
+    float* z = c.take<float>(g.BH * g.tn * g.d);
+    if (a) {
+        *mu = m;
+        *phik = pk;
+        a->h = h;
+        a->z = z;
+    }
+    return c.off + 256;
+}
+
+size_t sla2_forward_soft_workspace_size(const sla2_fwd_params* p) {
+    if (check_soft(p, "sla2_forward_soft") != SLA2_OK) return 0;
+    return carve_soft(geometry(p), nullptr, nullptr, nullptr, nullptr);
+}
+
+sla2_status sla2_forward_soft(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
+                              const float* values, void* out, const sla2_fwd_saved* saved, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = check_soft(p, "sla2_forward_soft");
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!q || !k || !v || !rho || !values || !out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    if (!workspace || workspace_bytes < carve_soft(g, nullptr, nullptr, nullptr, nullptr))
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_forward_soft_workspace_size)");
+    cudaStream_t st = (cudaStream_t)stream;
+    SoftLaunch a{};
+    float *mu = nullptr, *phik = nullptr;
+    carve_soft(g, workspace, &a, &mu, &phik);
+    if (p->smooth) SLA2_CUDA_TRY(launch_colmean(k, nullptr, false, mu, (int)g.BH, (int)g.N, (int)g.d, st, &g_launches));
+    a.BH = g.BH;
+    a.H = g.H;
+    a.N = (int)g.N;
+    a.d = (int)g.d;
+    a.bq = (int)g.bq;
+    a.bk = (int)g.bk;
+    a.tm = (int)g.tm;
+    a.tn = (int)g.tn;
+    a.inv_sqrt_d = inv_sqrt(g.d);
+    a.q = (const float*)q;
+    a.k = (const float*)k;
+    a.v = (const float*)v;
+    a.mu = p->smooth ? mu : nullptr;
+    a.values = values;
+    a.rho = rho;
+    a.out = (float*)out;
+    a.o_s = saved ? saved->o_s : nullptr;
+    a.o_l = saved ? saved->o_l : nullptr;
+    a.big_l = saved ? saved->big_l : nullptr;
+    SLA2_CUDA_TRY(launch_keyblock_linear(a.k, a.v, a.mu, phik, const_cast<float*>(a.h), const_cast<float*>(a.z), g.BH,
+                                         a.N, a.d, a.bk, st, &g_launches));
+    SLA2_CUDA_TRY(launch_soft_forward(a, st, &g_launches));
+    return SLA2_OK;
+}
+
 sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const void* k, const void* v,
                               const float* proj_q, const float* proj_k, const float* rho, void* out,
                               uint8_t* mask_out) {

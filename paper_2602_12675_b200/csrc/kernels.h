@@ -163,5 +163,20 @@ struct BackwardLaunch {
     float *mu, *phik, *h, *z, *htot, *ztot, *dh, *dz, *dsr;
 };
 cudaError_t launch_backward(const BackwardLaunch& a, cudaStream_t st, int* launches);
+// phi(K~_j) rows, h_j = phi(K~_j)^T V_j, z_j = colsum phi(K~_j) per key block (mu nullable)
+cudaError_t launch_keyblock_linear(const float* k, const float* v, const float* mu, float* phik, float* h, float* z,
+                                   int64_t BH, int N, int d, int bk, cudaStream_t st, int* launches);
+
+// ---- stage-1 soft routing (soft.cu): soft_topk + the SoftMask forward, fp32, d / bq / bk <= 64
+cudaError_t launch_soft_topk(const float* pc, int rows, int tn, double kappa, double tau, float* values,
+                             float* lambdas, int* fail, cudaStream_t st, int* launches);
+struct SoftLaunch {
+    int64_t BH, H;
+    int N, d, bq, bk, tm, tn;
+    float inv_sqrt_d;
+    const float *q, *k, *v, *mu, *values, *rho, *h, *z;  // mu nullable (smooth off)
+    float *out, *o_s, *o_l, *big_l;                      // o_s / o_l / big_l nullable
+};
+cudaError_t launch_soft_forward(const SoftLaunch& a, cudaStream_t st, int* launches);
 
 }  // namespace sla2dev

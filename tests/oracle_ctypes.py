@@ -72,6 +72,10 @@ class Oracle:
             for s, fp in (("f", _f32p), ("d", _f64p)):
                 self._sig(f"backward_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, _u8p, fp, C.c_int, fp, fp, fp, fp, fp,
                                             fp, fp, fp], C.c_int)
+                self._sig(f"soft_topk_{s}", [fp, _sz, _sz, C.c_double, C.c_float if s == "f" else C.c_double,
+                                             fp, fp], C.c_int)
+                self._sig(f"forward_soft_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, fp, fp, C.c_int, fp, fp, fp, fp],
+                          C.c_int)
                 self._sig(f"rten_save_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
                 self._sig(f"rten_load_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
         if prefix == "sla2o_":
@@ -218,6 +222,26 @@ class Oracle:
             np.ascontiguousarray(mask, dtype=np.uint8), np.ascontiguousarray(rho, dtype=dt), int(smooth),
             np.ascontiguousarray(d_out, dtype=dt), *outs)
         _check(rc)
+        return tuple(outs)
+
+    def soft_topk(self, pc, k_percent, tau):
+        """soft_topk (router.hpp:126-190), reference library only. Returns (values, lambdas)."""
+        tm, tn = pc.shape
+        values = np.empty((tm, tn), pc.dtype)
+        lambdas = np.empty(tm, pc.dtype)
+        _check(getattr(self, "_soft_topk_" + self._sfx(pc.dtype))(np.ascontiguousarray(pc), tm, tn, k_percent, tau,
+                                                                  values, lambdas))
+        return values, lambdas
+
+    def forward_soft(self, q, k, v, bq, bk, values, rho, smooth=True):
+        """sla2_forward_blockwise with a SoftMask (attention.hpp:484-558), reference library only.
+        Returns out, o_s, o_l, big_l."""
+        n, d = q.shape
+        dt = q.dtype
+        outs = [np.empty((n, d), dt) for _ in range(3)] + [np.empty(n, dt)]
+        _check(getattr(self, "_forward_soft_" + self._sfx(dt))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v), n, d, bq, bk,
+            np.ascontiguousarray(values, dtype=dt), np.ascontiguousarray(rho, dtype=dt), int(smooth), *outs))
         return tuple(outs)
 
     # --- RTEN1 through the reference's sla2::rten (tensor_io.hpp), reference library only ---

@@ -242,7 +242,7 @@ def test_deterministic(cuda):
 def _goldens():
     import os
     g = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-    return sorted(os.path.join(g, f) for f in os.listdir(g) if f.endswith(".npz") and not f.startswith("backward_"))
+    return sorted(os.path.join(g, f) for f in os.listdir(g) if f.endswith(".npz") and not f.startswith(("backward_", "soft_")))
 
 
 @pytest.mark.parametrize("path", _goldens(), ids=lambda p: p.rsplit("/", 1)[-1])

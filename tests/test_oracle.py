@@ -224,7 +224,7 @@ def test_port_bitexact_vs_reference_bf16_inputs_wan_block_shape():
 def _golden_files():
     if not os.path.isdir(GOLDEN):
         return []
-    return sorted(f for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("backward_"))
+    return sorted(f for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith(("backward_", "soft_")))
 
 
 @pytest.mark.parametrize("name", _golden_files())
