@@ -179,7 +179,8 @@ struct BlockMask {
     static BlockMask zeros(std::size_t tm, std::size_t tn) { return BlockMask{tm, tn, std::vector<std::uint8_t>(tm * tn, 0), 0}; }
 };
 
-// Stage-1 soft routing exists only so Routing<T> has the reference's shape; not on this path.
+// Stage-1 soft routing (router.hpp:74-82): soft_topk and the SoftMask forward run on the device
+// (sla2_soft_topk / sla2_forward_soft, fp32); the soft backward is not on this path.
 template <class T>
 struct SoftMask {
     std::size_t tm = 0, tn = 0;
@@ -344,18 +345,80 @@ inline BlockMask hard_topk(const Matrix<float>& pc, double k_percent) {
     return mask;
 }
 
-// attention.hpp:423-560 with hard routing.
+// soft_topk (router.hpp:126-190) on the device: bisection in double per row, fp32 values.
+inline SoftMask<float> soft_topk(const Matrix<float>& pc, double k_percent, float tau) {
+    if (!(tau > 0.0f)) throw numeric_error("soft_topk: tau must be positive");
+    const std::size_t tm = pc.rows(), tn = pc.cols();
+    sla2_fwd_params p;
+    sla2_default_params(&p, 1, 1, (int64_t)(tm * tn), 1);  // only the tm x tn geometry is read
+    p.bq = (int64_t)tn;
+    p.bk = (int64_t)tm;
+    p.k_percent = k_percent;
+    p.dtype = SLA2_F32;
+    p.tau = tau;
+    SoftMask<float> out;
+    out.tm = tm;
+    out.tn = tn;
+    out.tau = tau;
+    out.budget = topk_budget(k_percent, tn);
+    out.values = Matrix<float>(tm, tn);
+    out.lambdas = Vector<float>(tm);
+    b200::DeviceBuffer dpc(pc.size() * 4), dv(pc.size() * 4), dl(tm * 4);
+    dpc.upload(pc.data().data(), pc.size() * 4);
+    b200::check(sla2_soft_topk(&p, dpc.as<float>(), dv.as<float>(), dl.as<float>(), nullptr));
+    dv.download(out.values.data().data(), pc.size() * 4);
+    dl.download(out.lambdas.data().data(), tm * 4);
+    return out;
+}
+
+// attention.hpp:423-560 (hard routing on the tcgen05 / fp32 kernels; SoftMask on the fp32
+// stage-1 kernels).
 inline std::pair<Matrix<float>, SLA2ForwardSaved<float>> sla2_forward_blockwise(const AttentionInputs<float>& inputs,
                                                                                 const Routing<float>& routing,
                                                                                 const MixRatio<float>& alpha,
                                                                                 const QuantConfig* quant = nullptr,
                                                                                 bool smooth = true) {
     inputs.validate();
-    if (!std::holds_alternative<BlockMask>(routing))
-        throw contract_error("sla2_forward_blockwise: SoftMask routing (stage-1 training) is not on the B200 path");
-    const BlockMask& mask = std::get<BlockMask>(routing);
     const std::size_t n = inputs.seq_len(), d = inputs.head_dim(), tm = inputs.tm(), tn = inputs.tn();
     if (alpha.rho.size() != tm) throw shape_error("sla2_forward_blockwise: rho length != tm");
+    if (!std::holds_alternative<BlockMask>(routing)) {
+        // SoftMask (attention.hpp:484-558): the fp32 stage-1 kernels, whatever precision() says
+        const SoftMask<float>& soft = std::get<SoftMask<float>>(routing);
+        if (soft.tm != tm || soft.tn != tn) throw shape_error("sla2_forward_blockwise: soft mask geometry mismatch");
+        if (quant != nullptr) throw contract_error("sla2_forward_blockwise: SoftMask routing is full precision");
+        sla2_fwd_params p = b200::params(n, d, inputs.bq, inputs.bk, 100.0, false, smooth);
+        p.dtype = SLA2_F32;
+        const size_t ws = sla2_forward_soft_workspace_size(&p);
+        if (ws == 0)
+            b200::check(sla2_forward_soft(&p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                          nullptr));
+        b200::DeviceBuffer dq(n * d * 4), dk(n * d * 4), dv(n * d * 4), dout(n * d * 4), drho(tm * 4),
+            dw(tm * tn * 4), dos(n * d * 4), dol(n * d * 4), dl(n * 4), dws(ws);
+        dq.upload(inputs.q.data().data(), n * d * 4);
+        dk.upload(inputs.k.data().data(), n * d * 4);
+        dv.upload(inputs.v.data().data(), n * d * 4);
+        drho.upload(alpha.rho.data().data(), tm * 4);
+        dw.upload(soft.values.data().data(), tm * tn * 4);
+        sla2_fwd_saved sv{dos.as<float>(), dol.as<float>(), dl.as<float>()};
+        b200::check(sla2_forward_soft(&p, dq.p, dk.p, dv.p, drho.as<float>(), dw.as<float>(), dout.p, &sv, dws.p, ws,
+                                      nullptr));
+        b200::cuda_check(cudaDeviceSynchronize(), "sla2_forward_blockwise");
+        SLA2ForwardSaved<float> saved;
+        saved.routing = routing;
+        saved.smoothed = smooth;
+        saved.bq = inputs.bq;
+        saved.bk = inputs.bk;
+        saved.o_s = Matrix<float>(n, d);
+        saved.o_l = Matrix<float>(n, d);
+        saved.big_l = Vector<float>(n);
+        Matrix<float> out(n, d);
+        dout.download(out.data().data(), n * d * 4);
+        dos.download(saved.o_s.data().data(), n * d * 4);
+        dol.download(saved.o_l.data().data(), n * d * 4);
+        dl.download(saved.big_l.data().data(), n * 4);
+        return {std::move(out), std::move(saved)};
+    }
+    const BlockMask& mask = std::get<BlockMask>(routing);
     if (mask.tm != tm || mask.tn != tn) throw shape_error("sla2_forward_blockwise: mask geometry mismatch");
     for (std::size_t i = 0; i < tm; ++i) {
         bool any = false;

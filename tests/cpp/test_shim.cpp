@@ -121,12 +121,12 @@ static void blockwise_tests() {
             EXPECT(max_abs_diff(out, ref) <= 1e-4f);
         }
     }
-    // empty row -> shape_error; soft routing -> contract_error
+    // empty row -> shape_error; a SoftMask of the wrong geometry -> shape_error (attention.hpp:438-440)
     AttentionInputs<float> in{gaussian(16, 4, 362), gaussian(16, 4, 363), gaussian(16, 4, 364), 4, 4};
     BlockMask mask = BlockMask::zeros(4, 4);
     mask.at(0, 0) = mask.at(1, 1) = mask.at(2, 2) = 1;
     EXPECT(throws<shape_error>([&] { sla2_forward_blockwise(in, Routing<float>{mask}, MixRatio<float>::zeros(4)); }));
-    EXPECT(throws<contract_error>(
+    EXPECT(throws<shape_error>(
         [&] { sla2_forward_blockwise(in, Routing<float>{SoftMask<float>{}}, MixRatio<float>::zeros(4)); }));
     // full mask: alpha forced to 1 -> O_s
     auto [o, s] = sla2_forward_blockwise(in, Routing<float>{BlockMask::ones(4, 4)}, MixRatio<float>::constant(4, -5.f));
@@ -240,6 +240,85 @@ static void backward_tests() {
     EXPECT(all_zero);  // full rows: alpha forced to 1, no rho gradient (attention.hpp:648-651)
 }
 
+// stage-1 soft routing: test_router.cpp:118-165 (soft_topk) and test_attention.cpp:282-292
+// (SoftRoutingMatchesNaive) on the device path; the naive side is a host restatement in double.
+static void soft_tests() {
+    {
+        Matrix<float> pc(1, 4, std::vector<float>{0.7f, 0.7f, 0.7f, 0.7f});
+        SoftMask<float> sm = soft_topk(pc, 50.0, 0.1f);  // kappa = 2
+        for (std::size_t j = 0; j < 4; ++j) EXPECT(std::fabs(sm.values(0, j) - 0.5f) <= 1e-6f);
+        EXPECT(sm.budget == 2);
+    }
+    {
+        Matrix<float> pc = uniform(6, 12, 122);
+        SoftMask<float> sm = soft_topk(pc, 25.0, 0.1f);  // kappa = 3
+        for (std::size_t i = 0; i < 6; ++i) {
+            double s = 0;
+            for (std::size_t j = 0; j < 12; ++j) s += sm.values(i, j);
+            EXPECT(std::fabs(s - 3.0) <= 1e-5);
+        }
+        EXPECT(throws<numeric_error>([&] { soft_topk(pc, 25.0, 0.0f); }));
+    }
+    const std::size_t n = 32, d = 8, bq = 4, bk = 4, tm = n / bq, tn = n / bk;
+    AttentionInputs<float> in{gaussian(n, d, 359), gaussian(n, d, 360), gaussian(n, d, 361), bq, bk};
+    auto [kt, mu] = smooth_k(in.k);
+    SoftMask<float> soft = soft_topk(block_scores(in.q, kt, RouterParams<float>::identity(d), bq, bk), 25.0, 0.1f);
+    MixRatio<float> mix = MixRatio<float>::constant(tm, 0.3f);
+    auto [out, saved] = sla2_forward_blockwise(in, Routing<float>{soft}, mix);
+    // naive: sparse = softmax weighted by w over all keys; linear = phi(Q) phi(K~)^T weighted by 1 - w
+    std::vector<double> ktd(n * d), pk(n * d);
+    for (std::size_t c = 0; c < d; ++c) {
+        float acc = 0.0f;
+        for (std::size_t r = 0; r < n; ++r) acc += in.k(r, c);
+        const float m = acc / (float)n;
+        for (std::size_t r = 0; r < n; ++r) ktd[r * d + c] = (double)(in.k(r, c) - m);
+    }
+    auto softmax_row = [&](const double* x, double* y) {
+        double mx = x[0], s = 0;
+        for (std::size_t f = 1; f < d; ++f) mx = std::max(mx, x[f]);
+        for (std::size_t f = 0; f < d; ++f) s += (y[f] = std::exp(x[f] - mx));
+        for (std::size_t f = 0; f < d; ++f) y[f] /= s;
+    };
+    for (std::size_t r = 0; r < n; ++r) softmax_row(&ktd[r * d], &pk[r * d]);
+    double worst = 0;
+    for (std::size_t r = 0; r < n; ++r) {
+        std::vector<double> qr(d), pq(d), os(d, 0), ol(d, 0);
+        for (std::size_t f = 0; f < d; ++f) qr[f] = in.q(r, f);
+        softmax_row(qr.data(), pq.data());
+        std::vector<double> s(n);
+        double mx = -1e300;
+        for (std::size_t t = 0; t < n; ++t) {
+            double a = 0;
+            for (std::size_t f = 0; f < d; ++f) a += qr[f] * ktd[t * d + f];
+            s[t] = a / std::sqrt((double)d);
+            mx = std::max(mx, s[t]);
+        }
+        double zs = 0, zl = 0;
+        for (std::size_t t = 0; t < n; ++t) {
+            const double w = soft.values(r / bq, t / bk);
+            const double es = w * std::exp(s[t] - mx);
+            double al = 0;
+            for (std::size_t f = 0; f < d; ++f) al += pq[f] * pk[t * d + f];
+            al *= 1.0 - w;
+            zs += es;
+            zl += al;
+            for (std::size_t c = 0; c < d; ++c) {
+                os[c] += es * in.v(t, c);
+                ol[c] += al * in.v(t, c);
+            }
+        }
+        const double a = 1.0 / (1.0 + std::exp(-0.3));
+        for (std::size_t c = 0; c < d; ++c)
+            worst = std::max(worst, std::fabs(out(r, c) - (a * os[c] / zs + (1 - a) * ol[c] / zl)));
+    }
+    EXPECT(worst <= 1e-5);
+    EXPECT(saved.o_s.rows() == n && !saved.hard());
+    EXPECT(throws<contract_error>([&] {
+        QuantConfig qc;
+        sla2_forward_blockwise(in, Routing<float>{soft}, mix, &qc);
+    }));
+}
+
 int main() {
     rten_tests();
     backward_tests();
@@ -248,6 +327,7 @@ int main() {
     smooth_k_tests();
     blockwise_tests();
     attention_tests();
+    soft_tests();
     std::printf("shim tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
