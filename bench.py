@@ -231,6 +231,8 @@ def main():
     out = torch.empty_like(q)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     kw = dict(k_percent=c["k_percent"], bq=c["bq"], bk=c["bk"], quant=c["quant"], out=out)
+    if os.environ.get("SLA2_BENCH_INEXACT_MU"):  # experiment only: tree-reduced mean (mask may differ)
+        kw["exact_mu"] = False
 
     def eager_step():
         sla2.forward(q, k, v, pq, pk, rho, **kw)

@@ -413,6 +413,7 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
+    bool phiq_on_lin = false;  // phi(Q) on the linear stream (it has slack) instead of the query side
     cudaEvent_t early = nullptr;  // fork the linear precompute here, with its own parallel mean
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
@@ -486,6 +487,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
         }
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
+        if (plan.phiq_on_lin && w.phiq) SLA2_CUDA_TRY(launch_phiq(q, w.phiq, (int64_t)rows, lin, &g_launches));
         if (plan.early)
             SLA2_CUDA_TRY(launch_colmean_fast(k, g.bf16, w.mu_lin_part, w.mu_lin, (int)g.BH, (int)g.N, (int)g.d, lin,
                                               &g_launches));
@@ -688,8 +690,17 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         CUtensorMap mcol;
         fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);
         ra.kbar_ready = true;
-        ra.phiq_out = w.phiq;  // phi(Q) on the query side, beside the serial column mean
+        static const bool phiq_lin = std::getenv("SLA2_PHIQ_LIN") != nullptr;  // experiment
+        ra.phiq_out = phiq_lin ? nullptr : w.phiq;  // phi(Q) on the query side, beside the serial column mean
         LinPlan plan;
+        plan.phiq_on_lin = phiq_lin;
+        static const bool early_env = std::getenv("SLA2_EARLY_LIN_ENV") != nullptr;  // experiment
+        if (early_env && g.bf16 && p->smooth) {
+            thread_local cudaEvent_t ev_start2 = nullptr;
+            if (!ev_start2) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_start2, cudaEventDisableTiming));
+            SLA2_CUDA_TRY(cudaEventRecord(ev_start2, st));
+            plan.early = ev_start2;
+        }
 #if defined(SLA2_EARLY_LIN)
         // Experiment (measured slower, 0.649-0.708 vs 0.632 ms at cfg2): start the linear
         // precompute with the call, on its own parallel mean. Its CTAs then hold the SMs the
@@ -712,7 +723,8 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
 #endif
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;
-        plan.phiq_ready = w.phiq != nullptr;
+        plan.phiq_ready = w.phiq != nullptr && !phiq_lin;
+        if (phiq_lin) plan.phiq_ready = true;  // launched on the linear stream instead
         plan.kbar = w.kbar;
         plan.between = [&]() -> sla2_status {
             SLA2_CUDA_TRY(launch_router_back(ra, st, &g_launches));

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "expf_glibc.cuh"
 #include "kernels.h"
@@ -344,10 +345,8 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
     {
         const T* src = x + (bh * N + (int64_t)g * block) * d;
         if (((d * sizeof(T)) & 15) == 0) {
-            const uint4* src4 = reinterpret_cast<const uint4*>(src);
-            uint4* dst4 = reinterpret_cast<uint4*>(tile);
             const int n16 = (int)((size_t)cnt * d * sizeof(T) / 16);
-            for (int e = c; e < n16; e += blockDim.x) dst4[e] = src4[e];
+            stage_copy<16>(reinterpret_cast<uint4*>(tile), reinterpret_cast<const uint4*>(src), n16, c, blockDim.x);
         } else {
             for (int e = c; e < cnt * d; e += blockDim.x) tile[e] = src[e];
         }
@@ -381,74 +380,106 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
 }
 
 // xp[g][c] = sum_f xbar[g][f] * P[f][c] (matrix.hpp:121-132: i-k-j order, one serial chain
-// per output, f ascending from 0, separate mul and add), for a tile of 32 pooled rows per CTA.
-// P (d x d) and the xbar tile live in shared memory; each thread owns a 4 x 4 register tile
-// of outputs (16 independent chains). grid (ceil(nrows/32), BH), block 256. Requires d % 16 == 0.
-// With xp_t the output is written transposed, [BH][d][nrows] (the router's key side: lanes
-// of router_rows_kernel then read consecutive keys of one feature, coalesced).
-__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ xbar, const float* __restrict__ proj,
+// per output, f ascending from 0, separate mul and add), for a tile of 32 pooled rows x cw
+// output columns per CTA (cw = 64, or d, or 16: a divisor of d): P[:, tile] and the xbar rows live in shared memory;
+// each of the 2 cw threads owns a 4 x 4 register tile of outputs (16 independent chains) and
+// steps f by 4 with vector loads. grid (ceil(nrows/32), d/cw, BH), block 2 cw. Requires
+// d % 16 == 0. The column split keeps ~4 CTAs per SM (the kernel is latency-bound at low
+// occupancy). With xp_t the output is written transposed, [BH][d][nrows]
+// (the router's key side: lanes of router_rows_kernel then read consecutive keys of one
+// feature, coalesced).
+__global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ xbar, const float* __restrict__ proj,
                                                       float* __restrict__ xp, int nrows, int d, int H, int xp_t) {
     extern __shared__ __align__(16) float psh[];
-    float* sP = psh;           // [d][d]
-    float* sX = psh + d * d;   // [32][d]
-    const int64_t bh = blockIdx.y;
+    const int cw = blockDim.x / 2;
+    float* sP = psh;            // [d][cw]
+    float* sX = psh + d * cw;   // [32][d]
+    const int64_t bh = blockIdx.z;
     const int h = (int)(bh % H);
     const int r0 = blockIdx.x * 32;
+    const int c0 = blockIdx.y * cw;
     const int tid = threadIdx.x;
     const int nr = min(32, nrows - r0);
     {
-        const float4* P4 = reinterpret_cast<const float4*>(proj + (int64_t)h * d * d);
-        float4* s4 = reinterpret_cast<float4*>(sP);
-        for (int e = tid; e < d * d / 4; e += 256) s4[e] = P4[e];
-        const float4* X4 = reinterpret_cast<const float4*>(xbar + (bh * nrows + r0) * (int64_t)d);
+        // all of this CTA's loads in flight at once (a load / store loop would make one DRAM
+        // round trip per iteration)
+        const float* Pb = proj + (int64_t)h * d * d + c0;
+        const int cw4 = cw / 4, np = d * cw4, nx = nr * d / 4;
+        for (int base = tid; base < np; base += 16 * blockDim.x) {
+            float4 t[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int e = base + u * blockDim.x;
+                if (e < np) t[u] = *reinterpret_cast<const float4*>(Pb + (int64_t)(e / cw4) * d + (e % cw4) * 4);
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int e = base + u * blockDim.x;
+                if (e < np) reinterpret_cast<float4*>(sP)[e] = t[u];
+            }
+        }
         float4* x4 = reinterpret_cast<float4*>(sX);
-        for (int e = tid; e < 32 * d / 4; e += 256) x4[e] = (e < nr * d / 4) ? X4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+        stage_copy<8>(x4, reinterpret_cast<const float4*>(xbar + (bh * nrows + r0) * (int64_t)d), nx, tid, blockDim.x);
+        for (int e = nx + tid; e < 32 * d / 4; e += blockDim.x) x4[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
-    // d / 4 column groups x 8 row groups of 4 rows; 256 threads cover them in d/128 passes
-    const int ncg = d / 4;
-    for (int t = tid; t < ncg * 8; t += 256) {
-        const int cg = t % ncg, rg = t / ncg;
-        float acc[4][4];
+    const int ncg = cw / 4;
+    const int cg = tid % ncg, rg = tid / ncg;  // 8 row groups of 4 rows
+    float acc[4][4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
-        for (int f = 0; f < d; ++f) {
-            const float4 pv = *reinterpret_cast<const float4*>(sP + f * d + cg * 4);
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+    for (int f = 0; f < d; f += 4) {
+        float4 pv[4], xv[4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const float xv = sX[(rg * 4 + a) * d + f];
-                acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(xv, pv.x));
-                acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(xv, pv.y));
-                acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(xv, pv.z));
-                acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(xv, pv.w));
-            }
-        }
-        if (xp_t) {
-            // transposed rows padded to a multiple of 4 keys (aligned float4 rows for any tn)
-            const int ldt = (nrows + 3) & ~3;
+        for (int u = 0; u < 4; ++u) pv[u] = *reinterpret_cast<const float4*>(sP + (f + u) * cw + cg * 4);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                float* dst = xp + (bh * d + cg * 4 + b) * (int64_t)ldt + r0 + rg * 4;
-                if (rg * 4 + 4 <= nr) {
-                    *reinterpret_cast<float4*>(dst) = make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
-                } else {
+        for (int a = 0; a < 4; ++a) xv[a] = *reinterpret_cast<const float4*>(sX + (rg * 4 + a) * d + f);
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
-                        if (rg * 4 + a < nr) dst[a] = acc[a][b];
-                }
-            }
-        } else {
+        for (int u = 0; u < 4; ++u) {
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                const int r = rg * 4 + a;
-                if (r < nr)
-                    *reinterpret_cast<float4*>(xp + (bh * nrows + r0 + r) * (int64_t)d + cg * 4) =
-                        make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+                const float x = u == 0 ? xv[a].x : u == 1 ? xv[a].y : u == 2 ? xv[a].z : xv[a].w;
+                acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(x, pv[u].x));
+                acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(x, pv[u].y));
+                acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(x, pv[u].z));
+                acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(x, pv[u].w));
             }
         }
     }
+    const int col = c0 + cg * 4;
+    if (xp_t) {
+        // transposed rows padded to a multiple of 4 keys (aligned float4 rows for any tn)
+        const int ldt = (nrows + 3) & ~3;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            float* dst = xp + (bh * d + col + b) * (int64_t)ldt + r0 + rg * 4;
+            if (rg * 4 + 4 <= nr) {
+                *reinterpret_cast<float4*>(dst) = make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
+            } else {
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                    if (rg * 4 + a < nr) dst[a] = acc[a][b];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = rg * 4 + a;
+            if (r < nr)
+                *reinterpret_cast<float4*>(xp + (bh * nrows + r0 + r) * (int64_t)d + col) =
+                    make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+        }
+    }
+}
+
+static void launch_project(const float* xbar, const float* proj, float* xp, int nrows, int d, int H, int BH, int xp_t,
+                           cudaStream_t st) {
+    const int cw = d % 64 == 0 ? 64 : (d <= 64 ? d : 16);  // a divisor of d (d % 16 == 0)
+    const size_t ps = ((size_t)d * cw + 32 * (size_t)d) * 4;
+    if (ps > 48 * 1024) cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+    project_kernel<<<dim3((nrows + 31) / 32, d / cw, BH), 2 * cw, ps, st>>>(xbar, proj, xp, nrows, d, H, xp_t);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -693,9 +724,10 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
     const int64_t bh = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nrows = min(RROWS, tm - i0);
-    for (int e = tid; e < RROWS * d; e += 256) {
-        const int r = e / d;
-        sq[e] = (r < nrows) ? qp[(bh * tm + i0 + r) * (int64_t)d + (e % d)] : 0.0f;
+    {  // the CTA's query rows (contiguous): all loads in flight at once
+        const int nq = nrows * d;
+        stage_copy<8>(sq, qp + (bh * tm + i0) * (int64_t)d, nq, tid, 256);
+        for (int e = nq + tid; e < RROWS * d; e += 256) sq[e] = 0.0f;
     }
     __syncthreads();
     const float* kpb = kp + bh * (int64_t)tn * d;  // row-major [tn][d]
@@ -888,7 +920,12 @@ static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, 
                       int* launches) {
     constexpr int COLS = 128 / sizeof(T);
     if (sizeof(T) == 2 && tmk && d % cmt::COLS == 0) {
-        const int smem = (cmt::NST + cmt::NTS) * cmt::TILE;
+        // SLA2_CM_SMEM (experiment): pad the dynamic shared memory so no other CTA shares the SM
+        static const int smem = [] {
+            const char* e = std::getenv("SLA2_CM_SMEM");
+            const int base = (cmt::NST + cmt::NTS) * cmt::TILE;
+            return e ? (std::atoi(e) > base ? std::atoi(e) : base) : base;
+        }();
         static bool attr_t = false;
         if (!attr_t) {
             cudaFuncSetAttribute(colmean_tr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -926,9 +963,7 @@ static bool launch_pool_project(const T* x, const float* mu, const float* proj, 
     ++*launches;
     if (split) {
         const int nrows = (N + block - 1) / block;
-        const size_t ps = ((size_t)d * d + 32 * d) * 4;
-        cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
-        project_kernel<<<dim3((nrows + 31) / 32, BH), 256, ps, st>>>(scratch, proj, xp, nrows, d, H, want_t ? 1 : 0);
+        launch_project(scratch, proj, xp, nrows, d, H, BH, want_t ? 1 : 0, st);
         ++*launches;
         return want_t;
     }
@@ -962,12 +997,18 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
             if (a.mu_ready) cudaEventRecord(a.mu_ready, side);
             forked = true;
         } else {
+            // tree-reduced mean, also beside the query side
+            cudaEventRecord(ev_fork, st);
+            cudaStreamWaitEvent(side, ev_fork, 0);
             const int rows_per = 256;
             const int nch = (a.N + rows_per - 1) / rows_per;
-            colmean_partial_kernel<T><<<dim3(nch, BH), a.d, 0, st>>>((const T*)a.k, a.mu_part, a.N, a.d, rows_per);
-            colmean_finish_kernel<<<BH, a.d, 0, st>>>(a.mu_part, a.mu_out, nch, a.N, a.d);
+            colmean_partial_kernel<T><<<dim3(nch, BH), a.d, 0, side>>>((const T*)a.k, a.mu_part, a.N, a.d, rows_per);
+            colmean_finish_kernel<<<BH, a.d, 0, side>>>(a.mu_part, a.mu_out, nch, a.N, a.d);
             *launches += 2;
-            if (a.mu_ready) cudaEventRecord(a.mu_ready, st);
+            cudaEventRecord(ev_join, side);
+            timeline_mark(4, side);
+            if (a.mu_ready) cudaEventRecord(a.mu_ready, side);
+            forked = true;
         }
     }
     launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
@@ -991,10 +1032,7 @@ static cudaError_t router_back_t(const RouterLaunch& a, cudaStream_t st, int* la
     bool kp_t;
     if (a.kbar_ready) {
         // pooled keys already in kbar (launch_kprep, d = 128): project only
-        const size_t ps = ((size_t)a.d * a.d + 32 * a.d) * 4;
-        cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
-        project_kernel<<<dim3((tn + 31) / 32, BH), 256, ps, st>>>(a.kbar, a.proj_k, a.kp, tn, a.d, a.H,
-                                                                  tile_ok ? 1 : 0);
+        launch_project(a.kbar, a.proj_k, a.kp, tn, a.d, a.H, BH, tile_ok ? 1 : 0, st);
         ++*launches;
         kp_t = tile_ok;
     } else {

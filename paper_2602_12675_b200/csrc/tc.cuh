@@ -12,6 +12,25 @@ namespace sla2dev {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Global -> shared copy of n elements (e.g. float4 / uint4) by nt threads with U loads in
+// flight per thread: a plain `dst[e] = src[e]` loop compiles to load, store, branch -- one DRAM
+// round trip at a time per thread.
+template <int U, typename V>
+__device__ __forceinline__ void stage_copy(V* __restrict__ dst, const V* __restrict__ src, int n, int tid, int nt) {
+    for (int base = tid; base < n; base += U * nt) {
+        V t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * nt;
+            if (e < n) t[u] = src[e];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * nt;
+            if (e < n) dst[e] = t[u];
+        }
+    }
+}
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ bool elect_one() {
