@@ -661,6 +661,107 @@ __device__ void warp_topk_small(float* __restrict__ vals, int tn, int kappa, uin
     }
 }
 
+// Top-k by candidate bound (same result as warp_topk_small, ~4-7x fewer instructions):
+//  1. each lane keeps its M smallest keys (32 M >= kappa); B = the kappa-th smallest of those
+//     32 M values (radix select over them). At least kappa keys are <= B, so the kept set is
+//     inside C = {j : key_j <= B} (ties at B included).
+//  2. C is compacted in column order into `cand` as (key << 32 | column); if |C| > 64 the row
+//     falls back to the full radix select.
+//  3. a candidate is kept iff fewer than kappa candidates precede it in (key, column) order --
+//     std::stable_sort's order (router.hpp:117-121).
+template <int M>
+__device__ void warp_topk_cand(float* __restrict__ vals, int tn, int kappa, uint8_t* __restrict__ mask_row,
+                               int32_t* __restrict__ idx_row, uint8_t* sel, unsigned long long* cand) {
+    const int lane = threadIdx.x & 31;
+    uint32_t* hk = reinterpret_cast<uint32_t*>(vals);
+    uint32_t lm[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) lm[t] = 0xffffffffu;
+    for (int j = lane; j < tn; j += 32) {
+        uint32_t k = desc_key(vals[j]);
+        hk[j] = k;
+#pragma unroll
+        for (int t = 0; t < M; ++t) {  // insert into the lane's sorted M smallest
+            const uint32_t lo = min(lm[t], k);
+            k = max(lm[t], k);
+            lm[t] = lo;
+        }
+    }
+    __syncwarp();
+    // B: kappa-th smallest of the 32 M lane minima (radix select; sentinels count as keys, so B
+    // can only move up, never below the true kappa-th key)
+    uint32_t prefix = 0;
+    for (int b = 31; b >= 0; --b) {
+        const uint32_t c = prefix | (1u << b);
+        int n = 0;
+#pragma unroll
+        for (int t = 0; t < M; ++t) n += lm[t] < c ? 1 : 0;
+        if ((int)__reduce_add_sync(0xffffffffu, (unsigned)n) < kappa) prefix = c;
+    }
+    const uint32_t B = prefix;
+    // compact C in column order
+    int base = 0;
+    bool overflow = false;
+    for (int j0 = 0; j0 < tn; j0 += 32) {
+        const int j = j0 + lane;
+        const uint32_t k = j < tn ? hk[j] : 0xffffffffu;
+        const bool in = j < tn && k <= B;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const int pos = base + __popc(bal & ((1u << lane) - 1u));
+        if (in && pos < 64) cand[pos] = ((unsigned long long)k << 32) | (unsigned)j;
+        base += __popc(bal);
+    }
+    overflow = base > 64;
+    if (overflow) {  // uncommon: many keys tie near B; the exact radix select over the row
+        __syncwarp();
+        // warp_topk_small recomputes the keys from vals: restore the probabilities' order
+        // encoding is monotone, so select on the keys already in hk
+        uint32_t pfx = 0;
+        auto count_below = [&](uint32_t t) {
+            int c = 0;
+            for (int j = lane; j < tn; j += 32) c += hk[j] < t ? 1 : 0;
+            return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+        };
+        for (int b = 31; b >= 0; --b) {
+            const uint32_t c = pfx | (1u << b);
+            if (count_below(c) < kappa) pfx = c;
+        }
+        const int ties = kappa - count_below(pfx);
+        const unsigned lt = (1u << lane) - 1u;
+        int taken = 0;
+        for (int j0 = 0; j0 < tn; j0 += 32) {
+            const int j = j0 + lane;
+            const bool valid = j < tn;
+            const uint32_t kj = valid ? hk[j] : 0xffffffffu;
+            const bool eq = valid && kj == pfx;
+            const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+            const bool take = valid && (kj < pfx || (eq && taken + __popc(eqm & lt) < ties));
+            taken += __popc(eqm);
+            if (valid) sel[j] = take ? 1 : 0;
+        }
+    } else {
+        for (int j = lane; j < tn; j += 32) sel[j] = 0;
+        __syncwarp();
+        // rank each candidate (lanes own candidates lane, lane + 32)
+        for (int c = lane; c < base; c += 32) {
+            const unsigned long long me = cand[c];
+            int rank = 0;
+            for (int e = 0; e < base; ++e) rank += cand[e] < me ? 1 : 0;
+            if (rank < kappa) sel[(int)(me & 0xffffffffu)] = 1;
+        }
+    }
+    __syncwarp();
+    int ob = 0;
+    for (int j0 = 0; j0 < tn; j0 += 32) {
+        const int j = j0 + lane;
+        const bool f = (j < tn) && sel[j];
+        if (mask_row && j < tn) mask_row[j] = f ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (f) idx_row[ob + __popc(bal & ((1u << lane) - 1u))] = j;
+        ob += __popc(bal);
+    }
+}
+
 // Warp-local top-k on one row held in shared memory as 64-bit keys (value desc, column asc).
 // Bitonic sort by one warp (npow2 / 64 compare-exchanges per lane per stage), then the kept
 // columns are flagged and compacted in ascending order with ballots.
@@ -719,7 +820,7 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
     float* sq = vals + RROWS * tn;                       // [8][d]
     uint8_t* keyb = reinterpret_cast<uint8_t*>(sq + RROWS * d);
     // per-row top-k scratch: 64-bit sort keys for the bitonic path, selection flags otherwise
-    const size_t key_stride = TK > 0 ? (((size_t)tn + 15) & ~size_t(15)) : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
+    const size_t key_stride = TK > 0 ? (((size_t)tn + 15) & ~size_t(15)) + 512 : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
     const int i0 = blockIdx.x * RROWS;
     const int64_t bh = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -873,14 +974,20 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(keyb + warp * key_stride);
     uint8_t* mrow = mask_out ? mask_out + (bh * tm + i) * (int64_t)tn : nullptr;
     int32_t* irow = idx_out + (bh * tm + i) * (int64_t)kappa;
-    if constexpr (TK > 0) warp_topk_small<TK>(v, tn, kappa, mrow, irow, reinterpret_cast<uint8_t*>(keys));
+    if constexpr (TK > 0) {
+        uint8_t* selb = reinterpret_cast<uint8_t*>(keys);
+        unsigned long long* cand = reinterpret_cast<unsigned long long*>(selb + (((size_t)tn + 15) & ~size_t(15)));
+        if (kappa <= 32) warp_topk_cand<1>(v, tn, kappa, mrow, irow, selb, cand);
+        else if (kappa <= 64) warp_topk_cand<2>(v, tn, kappa, mrow, irow, selb, cand);
+        else warp_topk_small<TK>(v, tn, kappa, mrow, irow, selb);
+    }
     else warp_topk_row(v, tn, kappa, keys, npow2, mrow, irow);
 }
 
 size_t router_rows_smem(int tn, int d, bool radix) {
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
-    const size_t key_stride = radix ? (((size_t)tn + 15) & ~size_t(15)) : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
+    const size_t key_stride = radix ? (((size_t)tn + 15) & ~size_t(15)) + 512 : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
     return (size_t)RROWS * tn * 4 + (size_t)RROWS * d * 4 + RROWS * key_stride + 16;
 }
 

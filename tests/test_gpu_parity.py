@@ -43,6 +43,29 @@ def test_router_bitexact_bf16(cuda, N, k_percent, sigma, seed):
         assert np.array_equal(idx[0, h], ridx)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("k_percent", [3.0, 30.0, 60.0])
+def test_router_topk_ties_and_paths(cuda, k_percent):
+    """The router's top-k paths (candidate bound with 1 or 2 minima per lane, the radix
+    fallback on overflow, kappa > 64) on rows with exact ties: zero query blocks give uniform
+    rows (every key equal), duplicated key blocks give equal scores inside a row."""
+    torch = _torch()
+    B, H, N, d, bq, bk = 1, 2, 8192, 128, 128, 64
+    q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 77)
+    q[:, :, : 4 * bq] = 0.0
+    k[:, :, 9 * bk: 10 * bk] = k[:, :, 5 * bk: 6 * bk]
+    k[:, :, 20 * bk: 21 * bk] = k[:, :, 5 * bk: 6 * bk]
+    pc, mask, idx = sla2.router(to_dev(q, torch.bfloat16, cuda), to_dev(k, torch.bfloat16, cuda),
+                                to_dev(pq, torch.float32, cuda), to_dev(pk, torch.float32, cuda),
+                                k_percent=k_percent, bq=bq, bk=bk)
+    for h in range(H):
+        rpc, rmask, kappa = oracle_router_head(q[0, h], k[0, h], pq[h], pk[h], bq, bk, k_percent)
+        assert np.array_equal(pc.cpu().numpy()[0, h].view(np.uint32), rpc.view(np.uint32))
+        assert np.array_equal(mask.cpu().numpy()[0, h], rmask), (h, kappa)
+        assert np.array_equal(idx.cpu().numpy()[0, h], np.stack(mask_to_idx(rmask)))
+
+
+@pytest.mark.gpu
 def test_router_bitexact_f32_cfg1(cuda):
     torch = _torch()
     B, H, N, d, bq, bk, kp = 1, 2, 4096, 64, 64, 64, 10.0
