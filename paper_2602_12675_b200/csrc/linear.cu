@@ -469,51 +469,65 @@ __global__ void __launch_bounds__(256) htot_simt_kernel(const float* __restrict_
 }
 
 // Htot[bh] = sum_chunk hpart[bh][chunk] (chunk ascending); Ztot[bh] = sum_j zblk[bh][j].
-__global__ void lin_reduce_kernel(const float* __restrict__ hpart, const float* __restrict__ zblk,
+// The first CTAs of a head: Htot, four consecutive elements per thread (float4), up to 12
+// partials in flight per thread; the last ceil(d / 32): Ztot. blockDim 256, d * d % 4 == 0.
+__global__ void __launch_bounds__(256) lin_reduce_kernel(const float* __restrict__ hpart, const float* __restrict__ zblk,
                                   float* __restrict__ htot, __nv_bfloat16* __restrict__ htot16,
                                   float* __restrict__ ztot, int nchunk, int d, int tn) {
     const int64_t bh = blockIdx.y;
     const int dd = d * d;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
-        float s = 0.0f;
-        int c = 0;
-        for (; c + 8 <= nchunk; c += 8) {  // independent loads batched, summed in chunk order
-            float t[8];
+    if (blockIdx.x + (d + 31) / 32 < gridDim.x) {
+        const int e4 = blockIdx.x * blockDim.x + threadIdx.x;  // float4 index
+        if (e4 * 4 >= dd) return;
+        const float4* src = reinterpret_cast<const float4*>(hpart + bh * nchunk * (int64_t)dd) + e4;
+        const int stride4 = dd / 4;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c0 = 0; c0 < nchunk; c0 += 12) {  // loads batched, summed in chunk order
+            float4 t[12];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = hpart[(bh * nchunk + c + u) * (int64_t)dd + e];
+            for (int u = 0; u < 12; ++u)
+                if (c0 + u < nchunk) t[u] = src[(int64_t)(c0 + u) * stride4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) s += t[u];
-        }
-        for (; c < nchunk; ++c) s += hpart[(bh * nchunk + c) * (int64_t)dd + e];
-        htot[bh * dd + e] = s;
-        if (htot16) htot16[bh * dd + e] = __float2bfloat16_rn(s);
-    }
-    if (blockIdx.x == 0) {
-        // Ztot[f] = sum_j z_j[f]: blockDim / d threads per feature over strided j (16 loads in
-        // flight per thread), then combined in part order
-        __shared__ float zs[1024];
-        const int parts = blockDim.x / d;
-        const int f = threadIdx.x % d, part = threadIdx.x / d;
-        float s = 0.0f;
-        if (part < parts) {
-            for (int j0 = part; j0 < tn; j0 += 16 * parts) {
-                float t[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int j = j0 + u * parts;
-                    t[u] = j < tn ? zblk[(bh * tn + j) * d + f] : 0.0f;
+            for (int u = 0; u < 12; ++u)
+                if (c0 + u < nchunk) {
+                    s.x += t[u].x;
+                    s.y += t[u].y;
+                    s.z += t[u].z;
+                    s.w += t[u].w;
                 }
+        }
+        reinterpret_cast<float4*>(htot + bh * dd)[e4] = s;
+        if (htot16) {
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(htot16 + bh * dd + e4 * 4);
+            h2[0] = __floats2bfloat162_rn(s.x, s.y);
+            h2[1] = __floats2bfloat162_rn(s.z, s.w);
+        }
+        return;
+    }
+    // Ztot[f] = sum_j z_j[f]: the last ceil(d / 32) CTAs of the head, 32 features x 8 parts each;
+    // part p sums j = p, p + 8, ... (16 loads in flight per thread), parts combined in order
+    __shared__ float zs[256];
+    const int zc = blockIdx.x - (gridDim.x - (d + 31) / 32);
+    const int f = zc * 32 + (threadIdx.x & 31), part = threadIdx.x >> 5;
+    float s = 0.0f;
+    if (f < d) {
+        for (int j0 = part; j0 < tn; j0 += 16 * 8) {
+            float t[16];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) s += t[u];
+            for (int u = 0; u < 16; ++u) {
+                const int j = j0 + u * 8;
+                t[u] = j < tn ? zblk[(bh * tn + j) * d + f] : 0.0f;
             }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s += t[u];
         }
-        zs[threadIdx.x] = s;
-        __syncthreads();
-        if (threadIdx.x < d) {
-            float t = 0.0f;
-            for (int p = 0; p < parts; ++p) t += zs[p * d + threadIdx.x];
-            ztot[bh * d + threadIdx.x] = t;
-        }
+    }
+    zs[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < 32 && f < d) {
+        float t = 0.0f;
+        for (int p = 0; p < 8; ++p) t += zs[p * 32 + threadIdx.x];
+        ztot[bh * d + f] = t;
     }
 }
 
@@ -740,8 +754,9 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
         htot_simt_kernel<float><<<dim3(a.nchunk, (unsigned)a.BH), 256, smem, st>>>(
             (const float*)a.phik, (const float*)a.v, a.hpart, a.N, a.d, rows, a.nchunk);
     }
-    const int rthreads = a.d <= 128 ? (1024 / a.d) * a.d : 1024;
-    lin_reduce_kernel<<<dim3((a.d * a.d + rthreads - 1) / rthreads, (unsigned)a.BH), rthreads, 0, st>>>(
+    // Htot CTAs of 256 threads x 4 elements, plus one Ztot CTA per head (blockDim a multiple of d)
+    const int hctas = (a.d * a.d / 4 + 255) / 256;
+    lin_reduce_kernel<<<dim3(hctas + (a.d + 31) / 32, (unsigned)a.BH), 256, 0, st>>>(
         a.hpart, a.zblk, a.htot, a.bf16 ? (__nv_bfloat16*)a.htot16 : nullptr, a.ztot, a.nchunk, a.d, tn);
     *launches += (a.phik_ready || (a.bf16 && a.tm_k)) ? 2 : 3;
     return cudaGetLastError();
