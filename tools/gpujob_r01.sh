@@ -1,4 +1,4 @@
-# Round-1 evidence job (analysis only): bench lines for every config, the reference arm, the
+# Round-1 evidence job (analysis only; rerun after each kernel change): bench lines for every config, the reference arm, the
 # ncu launch list of one default forward and one --set full capture of the sparse kernel.
 python bench.py > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
 python bench.py --config cfg2pad --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg2pad.json 2>&1
