@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(128, 1)
 // phi(K~) written once). z_j: the four row-group partials summed in fixed order.
 // Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2-5 phi(K~) then the partial's TMEM read-back.
 namespace kh {
-constexpr int D = 128, BK = 64, NS = 3;
+constexpr int D = 128, BK = 64, NS = 2;  // 2 stages: 64 KB per CTA leaves shared memory for
+                                         // the router CTAs running beside it (3 measured slower)
 constexpr uint32_t TILE = BK * D * 2;            // 16 KB
 constexpr uint32_t SMEM = NS * 2 * TILE + 1024;  // [K -> phi(K~)][V] per stage
 }  // namespace kh
