@@ -331,7 +331,7 @@ __global__ void colmean_finish_kernel(const double* __restrict__ part, float* __
 template <typename T>
 __global__ void pool_project_kernel(const T* __restrict__ x, const float* __restrict__ mu, const float* __restrict__ proj,
                                     float* __restrict__ xp, int N, int d, int H, int block,
-                                    float* __restrict__ xbar_out) {
+                                    float* __restrict__ xbar_out, __nv_bfloat16* __restrict__ phi_out) {
     extern __shared__ __align__(16) uint8_t psm[];
     float* sbar = reinterpret_cast<float*>(psm);
     T* tile = reinterpret_cast<T*>(psm + ((d * sizeof(float) + 15) & ~size_t(15)));  // [block][d]
@@ -352,6 +352,45 @@ __global__ void pool_project_kernel(const T* __restrict__ x, const float* __rest
         }
     }
     __syncthreads();
+    if (phi_out) {
+        // phi(Q) rows from the staged tile (bf16, d = 128): phiq_kernel's arithmetic (16 lanes
+        // per row, 8 features each), so Q is read from DRAM once for pooling and phi(Q)
+        const int sub = c & 15, rpp = (int)(blockDim.x >> 4);  // rows per pass
+        for (int r0 = 0; r0 < cnt; r0 += rpp) {  // every lane runs every pass (shuffles)
+            const int r = r0 + (c >> 4);
+            const bool live = r < cnt;
+            const int rr = live ? r : cnt - 1;
+            const uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(tile) + rr * 128 + sub * 8);
+            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+            float xv[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+                xv[2 * e] = f2.x;
+                xv[2 * e + 1] = f2.y;
+            }
+            float mx = fmaxf(fmaxf(fmaxf(xv[0], xv[1]), fmaxf(xv[2], xv[3])), fmaxf(fmaxf(xv[4], xv[5]), fmaxf(xv[6], xv[7])));
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            float sum = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                float y;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"((xv[e] - mx) * 1.4426950408889634f));
+                xv[e] = y;
+                sum += y;
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            const float inv = 1.0f / sum;
+            uint4 o4;
+            o4.x = pack_bf16(xv[0] * inv, xv[1] * inv);
+            o4.y = pack_bf16(xv[2] * inv, xv[3] * inv);
+            o4.z = pack_bf16(xv[4] * inv, xv[5] * inv);
+            o4.w = pack_bf16(xv[6] * inv, xv[7] * inv);
+            if (live) *reinterpret_cast<uint4*>(phi_out + (bh * N + (int64_t)g * block + r) * 128 + sub * 8) = o4;
+        }
+    }
     const float m = mu ? mu[bh * d + c] : 0.0f;
     double acc = 0.0;
     for (int r = 0; r < cnt; ++r) {
@@ -1061,12 +1100,14 @@ static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, 
 template <typename T>
 static bool launch_pool_project(const T* x, const float* mu, const float* proj, float* xp, int N, int d, int H,
                                 int block, int BH, float* scratch, cudaStream_t st, int* launches,
-                                bool want_t = false) {
+                                bool want_t = false, __nv_bfloat16* phi_out = nullptr) {
     const size_t smem = ((d * sizeof(float) + 15) & ~size_t(15)) + (size_t)block * d * sizeof(T);
     if (smem > 48 * 1024) cudaFuncSetAttribute(pool_project_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const bool split = scratch && (d % 16 == 0) && ((size_t)d * d + 32 * d) * 4 <= 200 * 1024;
+    // phi(Q) fused only where phiq_kernel would run: bf16, d = 128, whole warps of 16-lane rows
+    const bool phi = phi_out && sizeof(T) == 2 && d == 128;
     pool_project_kernel<T><<<dim3((N + block - 1) / block, BH), d, smem, st>>>(x, mu, proj, xp, N, d, H, block,
-                                                                  split ? scratch : nullptr);
+                                                                  split ? scratch : nullptr, phi ? phi_out : nullptr);
     ++*launches;
     if (split) {
         const int nrows = (N + block - 1) / block;
@@ -1118,8 +1159,11 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
             forked = true;
         }
     }
-    launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches);
-    if (a.phiq_out) launch_phiq(a.q, a.phiq_out, (int64_t)BH * a.N, st, launches);
+    // the query pooling also writes phi(Q) (one read of Q) when it can; else phiq_kernel
+    const bool phi_fused = a.phiq_out && sizeof(T) == 2 && a.d == 128;
+    launch_pool_project<T>((const T*)a.q, nullptr, a.proj_q, a.qp, a.N, a.d, a.H, a.bq, BH, a.qbar, st, launches,
+                           false, phi_fused ? (__nv_bfloat16*)a.phiq_out : nullptr);
+    if (a.phiq_out && !phi_fused) launch_phiq(a.q, a.phiq_out, (int64_t)BH * a.N, st, launches);
     timeline_mark(5, st);
     if (a.query_done) cudaEventRecord(a.query_done, st);
     if (forked) cudaStreamWaitEvent(st, ev_join, 0);
