@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(96) colmean_tma_kernel(const __grid_constant__
 // Transposed row of column c: 16 chunks of 8 rows, chunk rc at ((rc ^ key(c)) * 16): the XOR
 // key spreads both the transposer's stores and the chain threads' loads over all banks.
 namespace cmt {
-constexpr int ROWS = 128, COLS = 64, NST = 4, NTS = 4;
+constexpr int ROWS = 128, COLS = 64, NST = 8, NTS = 4;
 constexpr int TILE = ROWS * COLS * 2;  // 16 KB (both layouts)
 __device__ __forceinline__ uint32_t tpos(int c, int rc) {
     return (uint32_t)c * 256u + (uint32_t)((rc ^ ((c ^ (c >> 3)) & 7)) * 16);
