@@ -205,7 +205,10 @@ Geo geometry(const sla2_fwd_params* p) {
         // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
         // the output) is bit-identical however many heads share a call. (Measured at cfg2:
         // 8 -> 0.654-0.662 ms, 12 -> 0.641-0.644, 22 -> 0.637-0.649, 32 / 43 slower.)
-        constexpr int64_t per = SLA2_HT_PER;
+        static const int64_t per = [] {  // SLA2_HT_PER_ENV: experiment override
+            const char* e = std::getenv("SLA2_HT_PER_ENV");
+            return (int64_t)(e && std::atoi(e) > 0 ? std::atoi(e) : SLA2_HT_PER);
+        }();
         g.nchunk = (int)((g.tn + per - 1) / per);
     } else {
         g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
