@@ -205,10 +205,7 @@ Geo geometry(const sla2_fwd_params* p) {
         // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
         // the output) is bit-identical however many heads share a call. (Measured at cfg2:
         // 8 -> 0.654-0.662 ms, 12 -> 0.641-0.644, 22 -> 0.637-0.649, 32 / 43 slower.)
-        static const int64_t per = [] {  // SLA2_HT_PER_ENV: experiment override
-            const char* e = std::getenv("SLA2_HT_PER_ENV");
-            return (int64_t)(e && std::atoi(e) > 0 ? std::atoi(e) : SLA2_HT_PER);
-        }();
+        constexpr int64_t per = SLA2_HT_PER;  // (re-measured after the router changes: 12 / 16 / 32 not faster)
         g.nchunk = (int)((g.tn + per - 1) / per);
     } else {
         g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
@@ -416,7 +413,6 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
-    bool phiq_on_lin = false;  // phi(Q) on the linear stream (it has slack) instead of the query side
     cudaEvent_t early = nullptr;  // fork the linear precompute here, with its own parallel mean
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
@@ -490,7 +486,6 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
         }
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
-        if (plan.phiq_on_lin && w.phiq) SLA2_CUDA_TRY(launch_phiq(q, w.phiq, (int64_t)rows, lin, &g_launches));
         if (plan.early)
             SLA2_CUDA_TRY(launch_colmean_fast(k, g.bf16, w.mu_lin_part, w.mu_lin, (int)g.BH, (int)g.N, (int)g.d, lin,
                                               &g_launches));
@@ -693,17 +688,11 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         CUtensorMap mcol;
         fill_router(p, g, w, q, k, proj_q, proj_k, nullptr, mask_out, idx, &mcol, &ra);
         ra.kbar_ready = true;
-        static const bool phiq_lin = std::getenv("SLA2_PHIQ_LIN") != nullptr;  // experiment
-        ra.phiq_out = phiq_lin ? nullptr : w.phiq;  // phi(Q) on the query side, beside the serial column mean
+        // phi(Q) on the query side, beside the serial column mean (written by the query pooling).
+        // Measured alternatives: phi(Q) on the linear stream (mu 10 us earlier, but the router's
+        // back half 18 us later); the early fork below.
+        ra.phiq_out = w.phiq;
         LinPlan plan;
-        plan.phiq_on_lin = phiq_lin;
-        static const bool early_env = std::getenv("SLA2_EARLY_LIN_ENV") != nullptr;  // experiment
-        if (early_env && g.bf16 && p->smooth) {
-            thread_local cudaEvent_t ev_start2 = nullptr;
-            if (!ev_start2) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_start2, cudaEventDisableTiming));
-            SLA2_CUDA_TRY(cudaEventRecord(ev_start2, st));
-            plan.early = ev_start2;
-        }
 #if defined(SLA2_EARLY_LIN)
         // Experiment (measured slower, 0.649-0.708 vs 0.632 ms at cfg2): start the linear
         // precompute with the call, on its own parallel mean. Its CTAs then hold the SMs the
@@ -726,8 +715,7 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
 #endif
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;
-        plan.phiq_ready = w.phiq != nullptr && !phiq_lin;
-        if (phiq_lin) plan.phiq_ready = true;  // launched on the linear stream instead
+        plan.phiq_ready = w.phiq != nullptr;
         plan.kbar = w.kbar;
         plan.between = [&]() -> sla2_status {
             SLA2_CUDA_TRY(launch_router_back(ra, st, &g_launches));

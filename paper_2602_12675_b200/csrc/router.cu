@@ -1066,12 +1066,8 @@ static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, 
                       int* launches) {
     constexpr int COLS = 128 / sizeof(T);
     if (sizeof(T) == 2 && tmk && d % cmt::COLS == 0) {
-        // SLA2_CM_SMEM (experiment): pad the dynamic shared memory so no other CTA shares the SM
-        static const int smem = [] {
-            const char* e = std::getenv("SLA2_CM_SMEM");
-            const int base = (cmt::NST + cmt::NTS) * cmt::TILE;
-            return e ? (std::atoi(e) > base ? std::atoi(e) : base) : base;
-        }();
+        // (padding the shared memory so no other CTA shares the SM measured no faster)
+        const int smem = (cmt::NST + cmt::NTS) * cmt::TILE;
         static bool attr_t = false;
         if (!attr_t) {
             cudaFuncSetAttribute(colmean_tr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
