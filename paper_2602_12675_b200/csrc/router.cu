@@ -226,8 +226,10 @@ __global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__
         }
         return;
     }
-    if (warp >= 2) {  // transposers: thread t owns 8x8 blocks (rb, cb) = (t/8 + 8k, t%8), k = 0, 1
-        const int t = threadIdx.x - 64;
+    // warps 0-1 transpose, 2-3 run the chains: each chain warp has an SM sub-partition (warp
+    // scheduler) to itself; the TMA warp 4 shares scheduler 0 with a transposer
+    if (warp < 2) {  // transposers: thread t owns 8x8 blocks (rb, cb) = (t/8 + 8k, t%8), k = 0, 1
+        const int t = threadIdx.x;
         const int cb = t & 7;
         for (int c = 0; c < nchunk; ++c) {
             const int s = c % NST, ts = c % NTS;
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(160) colmean_tr_kernel(const __grid_constant__
     }
     // chain threads: column col, 8 rows per LDS.128. Loads run two groups (16 rows, ~72 cycles
     // of adds) ahead of the chain, across chunk boundaries, so no add waits on shared memory.
-    const int col = threadIdx.x;
+    const int col = threadIdx.x - 64;
     float acc = 0.0f;
     uint32_t g0[4], g1[4];
     mbar_wait(&tfull[0], 0);
