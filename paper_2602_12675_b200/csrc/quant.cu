@@ -395,10 +395,23 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_before();
             mbar_arrive(&bar_pv_free[j & 1]);
         };
+        // the block's K and V scales are gathered through its index (two dependent global
+        // loads): fetched one block ahead so the round trips leave the S -> P chain
+        float ks_n = 0.0f, vs_n = 0.0f;
+        if (nb > 0) {
+            const int kb0 = idx[0];
+            ks_n = ks[kb0];
+            vs_n = vs[kb0];
+        }
         for (int j = 0; j < nb; ++j) {
             const int b = j & 1;
-            const int kb = idx[j];
-            const float sqk = __fmul_rn(sQ_, ks[kb]);
+            const float ks_j = ks_n, vs_j = vs_n;
+            if (j + 1 < nb) {
+                const int kb1 = idx[j + 1];
+                ks_n = ks[kb1];
+                vs_n = vs[kb1];
+            }
+            const float sqk = __fmul_rn(sQ_, ks_j);
             mbar_wait(&bar_s_full[b], (j >> 1) & 1);
             __syncwarp();
             tc_fence_after();
@@ -461,7 +474,7 @@ __global__ void __launch_bounds__(256, 1)
             // fold the previous block's PV now that this block's S is out of the way
             if (j >= 1) consume_pv(j - 1, corr_prev, spv_prev);
             corr_prev = corr;
-            spv_prev = __fmul_rn(sP, vs[kb]);
+            spv_prev = __fmul_rn(sP, vs_j);
         }
         if (nb > 0) consume_pv(nb - 1, corr_prev, spv_prev);
         __syncwarp();
