@@ -149,3 +149,25 @@ def test_ragged_heads_do_not_bleed(cuda):
     one = sla2.forward(*(x[:, :1].contiguous() for x in dev[:3]), dev[3][:1].contiguous(), dev[4][:1].contiguous(),
                        dev[5][:1].contiguous(), k_percent=10.0)
     assert torch.equal(both[:, :1], one)
+
+
+@pytest.mark.gpu
+def test_ragged_batch_and_host_path(cuda):
+    """B = 2 ragged heads: every (b, h) slice against the oracle, and the host-buffer entry point
+    (pipelined per head) reproduces the device call bit for bit."""
+    import torch
+    import paper_2602_12675_b200 as sla2
+    from sla2_testlib import rel_err, to_dev
+    B, H, N, kp = 2, 2, 1000, 10.0
+    q, k, v, pq, pk, rho = _gpu_case(B, H, N, 11)
+    dev = [to_dev(x, torch.bfloat16, cuda) for x in (q, k, v)] + [to_dev(x, torch.float32, cuda) for x in (pq, pk, rho)]
+    out, mask = sla2.forward(*dev, k_percent=kp, return_mask=True)
+    for b in range(B):
+        for h in range(H):
+            r_out, r_mask = P.attention_ragged(q[b, h], k[b, h], v[b, h], 128, 64, pq[h], pk[h], rho[h], kp)[:2]
+            assert np.array_equal(mask.cpu().numpy()[b, h], r_mask), (b, h)
+            assert rel_err(out.float().cpu().numpy()[b, h], r_out)[0] <= 1e-2, (b, h)
+    host = [x.cpu().pin_memory() for x in dev]
+    hout, hmask = sla2.forward_host(*host, k_percent=kp, return_mask=True)
+    assert torch.equal(hout, out.cpu())
+    assert torch.equal(hmask, mask.cpu())
