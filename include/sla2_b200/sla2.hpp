@@ -371,6 +371,27 @@ inline SoftMask<float> soft_topk(const Matrix<float>& pc, double k_percent, floa
     return out;
 }
 
+// soft_topk_backward (router.hpp:197-212) on the device: upstream * v * (1 - v) / tau.
+inline Matrix<float> soft_topk_backward(const Matrix<float>& pc, const SoftMask<float>& softmask,
+                                        const Matrix<float>& upstream) {
+    if (pc.rows() != softmask.tm || pc.cols() != softmask.tn || !pc.same_shape(upstream))
+        throw shape_error("soft_topk_backward: shape mismatch");
+    const std::size_t tm = pc.rows(), tn = pc.cols();
+    sla2_fwd_params p;
+    sla2_default_params(&p, 1, 1, (int64_t)(tm * tn), 1);
+    p.bq = (int64_t)tn;
+    p.bk = (int64_t)tm;
+    p.dtype = SLA2_F32;
+    p.tau = softmask.tau;
+    b200::DeviceBuffer dv(pc.size() * 4), du(pc.size() * 4), dg(pc.size() * 4);
+    dv.upload(softmask.values.data().data(), pc.size() * 4);
+    du.upload(upstream.data().data(), pc.size() * 4);
+    b200::check(sla2_soft_topk_backward(&p, dv.as<float>(), du.as<float>(), dg.as<float>(), nullptr));
+    Matrix<float> grad(tm, tn);
+    dg.download(grad.data().data(), pc.size() * 4);
+    return grad;
+}
+
 // attention.hpp:423-560 (hard routing on the tcgen05 / fp32 kernels; SoftMask on the fp32
 // stage-1 kernels).
 inline std::pair<Matrix<float>, SLA2ForwardSaved<float>> sla2_forward_blockwise(const AttentionInputs<float>& inputs,

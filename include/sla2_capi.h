@@ -175,6 +175,10 @@ sla2_status sla2_backward(const sla2_fwd_params* p, const void* q, const void* k
  * the reference. Workspace: sla2_forward_soft_workspace_size(p) bytes.
  */
 sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* values, float* lambdas, void* stream);
+/* soft_topk_backward (router.hpp:197-212): the frozen-lambda gradient grad = upstream * v *
+ * (1 - v) / tau elementwise over [B,H,tm,tn] (values from sla2_soft_topk, tau = p->tau). */
+sla2_status sla2_soft_topk_backward(const sla2_fwd_params* p, const float* values, const float* upstream,
+                                    float* grad, void* stream);
 size_t sla2_forward_soft_workspace_size(const sla2_fwd_params* p);
 sla2_status sla2_forward_soft(const sla2_fwd_params* p, const void* q, const void* k, const void* v, const float* rho,
                               const float* values, void* out, const sla2_fwd_saved* saved, void* workspace,

@@ -185,6 +185,16 @@ int soft_topk_(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau, T*
     } catch (const std::exception& e) { return classify(e); }
 }
 
+// soft_topk_backward (router.hpp:197-212) on the reference's own SoftMask from soft_topk
+template <class T>
+int soft_topk_backward_(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau, const T* upstream, T* grad) {
+    try {
+        SoftMask<T> sm = soft_topk(wrap(pc, tm, tn), kp, tau);
+        copy_out(soft_topk_backward(wrap(pc, tm, tn), sm, wrap(upstream, tm, tn)), grad);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
 // sla2_forward_blockwise with Routing = SoftMask (attention.hpp:484-558), caller-given values
 template <class T>
 int forward_soft_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, std::size_t bq,
@@ -304,6 +314,10 @@ SLA2R_RTEN(double, d)
     int sla2r_soft_topk_##S(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau, T* values, \
                             T* lambdas) {                                                         \
         return soft_topk_<T>(pc, tm, tn, kp, tau, values, lambdas);                               \
+    }                                                                                             \
+    int sla2r_soft_topk_backward_##S(const T* pc, std::size_t tm, std::size_t tn, double kp, T tau,          \
+                                     const T* upstream, T* grad) {                                \
+        return soft_topk_backward_<T>(pc, tm, tn, kp, tau, upstream, grad);                       \
     }                                                                                             \
     int sla2r_forward_soft_##S(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,  \
                                std::size_t bq, std::size_t bk, const T* values, const T* rho,     \

@@ -99,6 +99,7 @@ def lib():
         "sla2_backward_workspace_size": ([P], sz),
         "sla2_soft_topk": ([P, vp, vp, vp, vp], C.c_int),
         "sla2_forward_soft_workspace_size": ([P], sz),
+        "sla2_soft_topk_backward": ([P, vp, vp, vp, vp], C.c_int),
         "sla2_forward_soft": ([P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_backward": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_last_error": ([], C.c_char_p),
@@ -429,6 +430,22 @@ def soft_topk(pc, k_percent=3.0, tau=0.1):
     lambdas = torch.empty((B, H, tm), dtype=torch.float32, device=pc.device)
     _raise(lib().sla2_soft_topk(C.byref(cp), _ptr(pc), _ptr(values), _ptr(lambdas), _stream(pc.device)))
     return values, lambdas
+
+
+def soft_topk_backward(values, upstream, tau=0.1):
+    """soft_topk_backward (router.hpp:197-212) on device: the frozen-lambda gradient
+    upstream * v * (1 - v) / tau of soft_topk's values [B,H,tm,tn] (fp32)."""
+    import torch
+    if values.dim() != 4 or values.dtype != torch.float32 or not values.is_contiguous():
+        raise ContractError("soft_topk_backward: contiguous fp32 values [B, H, tm, tn]")
+    if upstream.shape != values.shape or upstream.dtype != torch.float32 or not upstream.is_contiguous():
+        raise ShapeError("soft_topk_backward: shape mismatch")  # router.hpp:202-204
+    B, H, tm, tn = values.shape
+    p = FwdParams(B, H, tm * tn, 1, tn, tm, 100.0, False, False, False, True, tau)
+    cp = p.c()
+    grad = torch.empty_like(values)
+    _raise(lib().sla2_soft_topk_backward(C.byref(cp), _ptr(values), _ptr(upstream), _ptr(grad), _stream(values.device)))
+    return grad
 
 
 def forward_soft(q, k, v, rho, values, *, bq=64, bk=64, smooth=True, saved=False):

@@ -967,6 +967,22 @@ sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* val
     return SLA2_OK;
 }
 
+sla2_status sla2_soft_topk_backward(const sla2_fwd_params* p, const float* values, const float* upstream,
+                                    float* grad, void* stream) {
+    g_launches = 0;
+    sla2_status s = check_common(p);  // the score geometry tm x tn and tau (> 0)
+    if (s != SLA2_OK) return s;
+    if (p->N % p->bq != 0 || p->N % p->bk != 0)
+        return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!values || !upstream || !grad) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    const float inv_tau = 1.0f / p->tau;  // T(1) / softmask.tau in float (router.hpp:206)
+    SLA2_CUDA_TRY(launch_soft_topk_backward(values, upstream, grad, g.BH * g.tm * g.tn, inv_tau,
+                                            (cudaStream_t)stream, &g_launches));
+    return SLA2_OK;
+}
+
 static size_t carve_soft(const Geo& g, void* base, SoftLaunch* a, float** mu, float** phik) {
     Carver c{reinterpret_cast<uint8_t*>(base)};
     float* m = c.take<float>(g.BH * g.d);

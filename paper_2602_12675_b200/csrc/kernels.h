@@ -170,6 +170,8 @@ cudaError_t launch_keyblock_linear(const float* k, const float* v, const float* 
 // ---- stage-1 soft routing (soft.cu): soft_topk + the SoftMask forward, fp32, d / bq / bk <= 64
 cudaError_t launch_soft_topk(const float* pc, int rows, int tn, double kappa, double tau, float* values,
                              float* lambdas, int* fail, cudaStream_t st, int* launches);
+cudaError_t launch_soft_topk_backward(const float* values, const float* upstream, float* grad, int64_t n,
+                                      float inv_tau, cudaStream_t st, int* launches);
 struct SoftLaunch {
     int64_t BH, H;
     int N, d, bq, bk, tm, tn;

@@ -12,6 +12,7 @@
 // come from backward.cu's bwd_keyblock_kernel (launch_keyblock_linear).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -59,6 +60,16 @@ __global__ void soft_topk_kernel(const float* __restrict__ pc, int rows, int tn,
         double v = 1.0 / (1.0 + exp(-((double)p[j] / tau + lam)));
         v = fmin(fmax(v, DBL_MIN), 1.0 - DBL_EPSILON / 2);
         values[(int64_t)row * tn + j] = (float)v;
+    }
+}
+
+// soft_topk_backward (router.hpp:197-212): frozen-lambda diagonal Jacobian,
+// grad = upstream * v * (1 - v) * (1 / tau), left to right as the reference
+__global__ void soft_topk_backward_kernel(const float* __restrict__ values, const float* __restrict__ upstream,
+                                          float* __restrict__ grad, int64_t n, float inv_tau) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const float v = values[e];
+        grad[e] = __fmul_rn(__fmul_rn(__fmul_rn(upstream[e], v), __fsub_rn(1.0f, v)), inv_tau);
     }
 }
 
@@ -190,6 +201,14 @@ size_t soft_forward_smem() {
 cudaError_t launch_soft_topk(const float* pc, int rows, int tn, double kappa, double tau, float* values,
                              float* lambdas, int* fail, cudaStream_t st, int* launches) {
     soft_topk_kernel<<<(rows + 7) / 8, 256, 0, st>>>(pc, rows, tn, kappa, tau, values, lambdas, fail);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_soft_topk_backward(const float* values, const float* upstream, float* grad, int64_t n,
+                                      float inv_tau, cudaStream_t st, int* launches) {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    soft_topk_backward_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(values, upstream, grad, n, inv_tau);
     ++*launches;
     return cudaGetLastError();
 }

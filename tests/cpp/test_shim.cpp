@@ -258,6 +258,18 @@ static void soft_tests() {
             EXPECT(std::fabs(s - 3.0) <= 1e-5);
         }
         EXPECT(throws<numeric_error>([&] { soft_topk(pc, 25.0, 0.0f); }));
+        // soft_topk_backward (test_router.cpp:173-178): zero upstream -> zero; the diagonal rule
+        Matrix<float> zero(6, 12, 0.0f);
+        Matrix<float> g0 = soft_topk_backward(pc, sm, zero);
+        EXPECT(max_abs(g0) == 0.0f);
+        Matrix<float> up = uniform(6, 12, 134);
+        Matrix<float> g = soft_topk_backward(pc, sm, up);
+        float worst = 0.0f;
+        for (std::size_t e = 0; e < pc.size(); ++e) {
+            const float v = sm.values.data()[e];
+            worst = std::max(worst, std::fabs(g.data()[e] - up.data()[e] * v * (1.0f - v) * (1.0f / 0.1f)));
+        }
+        EXPECT(worst == 0.0f);
     }
     const std::size_t n = 32, d = 8, bq = 4, bk = 4, tm = n / bq, tn = n / bk;
     AttentionInputs<float> in{gaussian(n, d, 359), gaussian(n, d, 360), gaussian(n, d, 361), bq, bk};

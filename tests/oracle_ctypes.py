@@ -76,6 +76,8 @@ class Oracle:
                                              fp, fp], C.c_int)
                 self._sig(f"forward_soft_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, fp, fp, C.c_int, fp, fp, fp, fp],
                           C.c_int)
+                self._sig(f"soft_topk_backward_{s}", [fp, _sz, _sz, C.c_double, C.c_float if s == "f" else C.c_double,
+                                                      fp, fp], C.c_int)
                 self._sig(f"rten_save_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
                 self._sig(f"rten_load_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
         if prefix == "sla2o_":
@@ -232,6 +234,14 @@ class Oracle:
         _check(getattr(self, "_soft_topk_" + self._sfx(pc.dtype))(np.ascontiguousarray(pc), tm, tn, k_percent, tau,
                                                                   values, lambdas))
         return values, lambdas
+
+    def soft_topk_backward(self, pc, k_percent, tau, upstream):
+        """soft_topk_backward (router.hpp:197-212) on soft_topk(pc)'s mask, reference library only."""
+        tm, tn = pc.shape
+        grad = np.empty((tm, tn), pc.dtype)
+        _check(getattr(self, "_soft_topk_backward_" + self._sfx(pc.dtype))(
+            np.ascontiguousarray(pc), tm, tn, k_percent, tau, np.ascontiguousarray(upstream, dtype=pc.dtype), grad))
+        return grad
 
     def forward_soft(self, q, k, v, bq, bk, values, rho, smooth=True):
         """sla2_forward_blockwise with a SoftMask (attention.hpp:484-558), reference library only.

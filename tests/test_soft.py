@@ -224,3 +224,39 @@ def test_forward_soft_contract(cuda):
     with pytest.raises(sla2.ShapeError):  # N not divisible
         z = torch.zeros((1, 1, 250, 64), device=cuda)
         sla2.forward_soft(z, z, z, torch.zeros((1, 4), device=cuda), torch.zeros((1, 1, 4, 4), device=cuda))
+
+
+# ---------------------------------------------------------------- soft_topk_backward
+@needs_ref
+def test_soft_topk_backward_reference_properties_cpu():
+    """test_router.cpp:173-205 through the shim: zero upstream gives zero; doubling tau halves it."""
+    rng = np.random.default_rng(131)
+    pc = rng.uniform(-1, 1, (3, 6)).astype(np.float32)
+    assert np.all(R.soft_topk_backward(pc, 50.0, 0.2, np.zeros((3, 6), np.float32)) == 0)
+    up = rng.uniform(-1, 1, (3, 6)).astype(np.float32)
+    g1 = R.soft_topk_backward(pc.astype(np.float64), 50.0, 0.2, up.astype(np.float64))
+    v, _ = R.soft_topk(pc.astype(np.float64), 50.0, 0.2)
+    assert np.abs(g1 - up * v * (1 - v) / 0.2).max() <= 1e-15
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("tm,tn,kp,tau,seed", [(64, 32, 25.0, 0.1, 1), (16, 512, 3.0, 0.05, 2)])
+def test_soft_topk_backward_vs_reference(cuda, tm, tn, kp, tau, seed):
+    """Bit-exact against the reference's soft_topk_backward given the same values (same
+    elementwise order, no FMA)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((2, 2, tm, tn))
+    pc = (np.exp(x) / np.exp(x).sum(-1, keepdims=True)).astype(np.float32)
+    up = rng.standard_normal((2, 2, tm, tn)).astype(np.float32)
+    values, _ = sla2.soft_topk(_t(pc, cuda), k_percent=kp, tau=tau)
+    g = sla2.soft_topk_backward(values, _t(up, cuda), tau=tau).cpu().numpy()
+    vals = values.cpu().numpy()
+    for b in range(2):
+        for h in range(2):
+            rv, _ = R.soft_topk(pc[b, h], kp, tau)
+            rg = R.soft_topk_backward(pc[b, h], kp, tau, up[b, h])
+            if np.array_equal(vals[b, h], rv):  # same values -> same gradient bits
+                assert np.array_equal(g[b, h], rg), (b, h)
+            else:
+                assert np.abs(g[b, h] - rg).max() <= 1e-5 * max(1.0, np.abs(rg).max())
