@@ -260,3 +260,26 @@ def test_soft_topk_backward_vs_reference(cuda, tm, tn, kp, tau, seed):
                 assert np.array_equal(g[b, h], rg), (b, h)
             else:
                 assert np.abs(g[b, h] - rg).max() <= 1e-5 * max(1.0, np.abs(rg).max())
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_forward_soft_batch_heads_layout(cuda):
+    """B = 2, H = 3 (per-head rho rows, (b, h) slices) with and without smoothing: every slice
+    against the reference's SoftMask forward on the same values."""
+    import torch
+    from sla2_testlib import make_inputs, to_dev
+    B, H, N, d, bq, bk = 2, 3, 256, 32, 32, 32
+    for smooth in (True, False):
+        q, k, v, pq, pk, rho = make_inputs(B, H, N, d, 21, bf16=False, bq=bq, bk=bk)
+        rng = np.random.default_rng(22)
+        x = rng.standard_normal((B, H, N // bq, N // bk))
+        pc = (np.exp(x) / np.exp(x).sum(-1, keepdims=True)).astype(np.float32)
+        values, _ = sla2.soft_topk(_t(pc, cuda), k_percent=25.0, tau=0.1)
+        dev = [to_dev(t, torch.float32, cuda) for t in (q, k, v, rho)]
+        out = sla2.forward_soft(dev[0], dev[1], dev[2], dev[3], values, bq=bq, bk=bk, smooth=smooth).cpu().numpy()
+        vals = values.cpu().numpy()
+        for b in range(B):
+            for h in range(H):
+                ro = R.forward_soft(q[b, h], k[b, h], v[b, h], bq, bk, vals[b, h], rho[h], smooth=smooth)[0]
+                assert _rel(out[b, h], ro) <= TOL, (smooth, b, h)
