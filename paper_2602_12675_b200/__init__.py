@@ -234,9 +234,10 @@ def _check_like(ref, *ts):
 
 
 def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant=False, smooth=True,
-            exact_mu=True, return_mask=False, return_idx=False, saved=False, out=None):
+            exact_mu=True, return_mask=False, return_idx=False, saved=False, out=None, workspace=None):
     """Router + blockwise forward (tape.hpp:263-272). Returns out or a tuple with
-    (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested."""
+    (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested. `workspace` (a
+    uint8 CUDA tensor of at least workspace_bytes(...)) replaces the shared per-device cache."""
     import torch
     _check_like(q, k, v)
     p = _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu)
@@ -253,7 +254,12 @@ def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant
                "o_l": torch.empty(q.shape, dtype=torch.float32, device=dev),
                "big_l": torch.empty(q.shape[:3], dtype=torch.float32, device=dev)}
         sv = _Saved(svs["o_s"].data_ptr(), svs["o_l"].data_ptr(), svs["big_l"].data_ptr())
-    ws = _workspace(p, dev)
+    if workspace is not None:
+        if workspace.dtype != torch.uint8 or workspace.device != dev or workspace.numel() < workspace_bytes(p):
+            raise ContractError("workspace too small (see workspace_bytes)")
+        ws = workspace
+    else:
+        ws = _workspace(p, dev)
     rc = lib().sla2_forward(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(proj_q.contiguous()),
                             _ptr(proj_k.contiguous()), _ptr(rho.contiguous()), _ptr(out), _ptr(mask), _ptr(idx),
                             C.byref(sv) if sv is not None else None, _ptr(ws), ws.numel(), _stream(dev))
@@ -272,7 +278,8 @@ class CapturedForward:
     """forward() captured once into a CUDA graph and replayed: one graph launch per call instead
     of ~10 kernel launches, event records and host-side checks (the call is launch-bound at
     small shapes and pays ~20 us of host time at cfg2). The input / output tensors are fixed at
-    capture; write new inputs into them (copy_) between replays."""
+    capture; write new inputs into them (copy_) between replays. The graph owns its workspace
+    for its lifetime (a later forward() needing a bigger shared workspace cannot free it)."""
 
     def __init__(self, q, k, v, proj_q, proj_k, rho, **kw):
         import torch
@@ -280,6 +287,10 @@ class CapturedForward:
         if self.out is None:
             self.out = torch.empty_like(q)
         self.args = (q, k, v, proj_q, proj_k, rho)
+        p = _params_from(q, kw.get("bq", 128), kw.get("bk", 64), kw.get("k_percent", 3.0), kw.get("quant", False),
+                         kw.get("smooth", True), kw.get("exact_mu", True))
+        self.workspace = torch.empty(max(workspace_bytes(p), 1), dtype=torch.uint8, device=q.device)
+        kw["workspace"] = self.workspace
         self.kw = kw
         forward(*self.args, out=self.out, **kw)  # warm-up: streams, events, attributes, maps
         torch.cuda.synchronize(q.device)
@@ -432,9 +443,10 @@ def soft_topk(pc, k_percent=3.0, tau=0.1):
     return values, lambdas
 
 
-def soft_topk_backward(values, upstream, tau=0.1):
+def soft_topk_backward(values, upstream, *, tau):
     """soft_topk_backward (router.hpp:197-212) on device: the frozen-lambda gradient
-    upstream * v * (1 - v) / tau of soft_topk's values [B,H,tm,tn] (fp32)."""
+    upstream * v * (1 - v) / tau of soft_topk's values [B,H,tm,tn] (fp32). tau has no default:
+    it must be the tau soft_topk ran with (the reference reads it from the SoftMask)."""
     import torch
     if values.dim() != 4 or values.dtype != torch.float32 or not values.is_contiguous():
         raise ContractError("soft_topk_backward: contiguous fp32 values [B, H, tm, tn]")

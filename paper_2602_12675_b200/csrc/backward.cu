@@ -427,18 +427,10 @@ cudaError_t launch_backward(const BackwardLaunch& a, cudaStream_t st, int* launc
     bwd_keyblock_kernel<<<gk, 256, 0, st>>>(a.k, a.v, mu, a.phik, a.h, a.z, a.N, a.d, a.bk);
     bwd_total_kernel<<<dim3((a.d * a.d + 255) / 256, (unsigned)a.BH), 256, 0, st>>>(a.h, a.z, a.htot, a.ztot, tn, a.d);
     const int qsm = (int)(sizeof(float) * (bw::MAXD + 2 * bw::MAXB) * (bw::MAXD + 1));
-    static bool attr_q = false;
-    if (!attr_q) {
-        cudaFuncSetAttribute(bwd_qblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, qsm);
-        attr_q = true;
-    }
+    ensure_smem_attr((const void*)bwd_qblock_kernel, (int)(qsm));
     bwd_qblock_kernel<<<gq, 256, qsm, st>>>(a.q, a.d_out, a.o_s, a.o_l, a.mask, a.rho, a.h, a.z, a.htot, a.ztot, a.dq,
                                           a.dsr, a.dh, a.dz, a.drho, a.N, a.d, a.bq, tm, tn, (int)a.H);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(bwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_sparse_smem());
-        attr = true;
-    }
+    ensure_smem_attr((const void*)bwd_sparse_kernel, (int)((int)bwd_sparse_smem()));
     bwd_sparse_kernel<<<gq, 256, bwd_sparse_smem(), st>>>(a.q, a.k, a.v, mu, a.d_out, a.big_l, a.dsr, a.mask, a.rho,
                                                           a.dq, a.dk, a.dv, a.N, a.d, a.bq, a.bk, tm, tn, (int)a.H,
                                                           a.inv_sqrt_d);

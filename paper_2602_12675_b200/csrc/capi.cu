@@ -30,12 +30,23 @@ thread_local int g_launches = 0;
 constexpr int NEV = 9;
 thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[NEV] = {};
+thread_local int g_ev_dev = -1;  // device the timing events belong to
 thread_local bool g_ev_recorded = false;
 thread_local unsigned g_ev_mask = 0;
 // set by sla2_forward around its sla2_router call: the router records it once mu is ready
 thread_local cudaEvent_t g_mu_ready = nullptr;
 void mark(int i, cudaStream_t st) {
     if (!g_timing) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != g_ev_dev) {  // events are per device: recreate them on a device switch
+        for (auto& e : g_ev)
+            if (e) {
+                cudaEventDestroy(e);
+                e = nullptr;
+            }
+        g_ev_dev = dev;
+    }
     if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
     cudaEventRecord(g_ev[i], st);
     if (i == 0) g_ev_mask = 0;
@@ -176,9 +187,6 @@ bool make_map3(CUtensorMap* out, const void* ptr, uint64_t heads, uint64_t rows,
 }
 
 // ---------------------------------------------------------------- geometry + workspace
-#ifndef SLA2_HT_PER
-#define SLA2_HT_PER 22
-#endif
 struct Geo {
     int64_t B, H, BH, N, d, bq, bk, tm, tn, kappa;
     bool bf16, quant;
@@ -205,7 +213,7 @@ Geo geometry(const sla2_fwd_params* p) {
         // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
         // the output) is bit-identical however many heads share a call. (Measured at cfg2:
         // 8 -> 0.654-0.662 ms, 12 -> 0.641-0.644, 22 -> 0.637-0.649, 32 / 43 slower.)
-        constexpr int64_t per = SLA2_HT_PER;  // (re-measured after the router changes: 12 / 16 / 32 not faster)
+        constexpr int64_t per = 22;  // (re-measured after the router changes: 12 / 16 / 32 not faster)
         g.nchunk = (int)((g.tn + per - 1) / per);
     } else {
         g.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (g.N + 511) / 512));
@@ -228,8 +236,6 @@ struct Carver {
 struct Workspace {
     float* mu;
     double* mu_part;
-    float* mu_lin;        // the linear branch's mean (parallel, tolerance-level), bf16 path
-    double* mu_lin_part;
     float* qp;
     float* kp;
     float* qbar;
@@ -253,8 +259,6 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     Workspace t{};
     t.mu = c.take<float>(g.BH * g.d);
     t.mu_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
-    t.mu_lin = c.take<float>(g.BH * g.d);
-    t.mu_lin_part = c.take<double>(g.BH * ((g.N + 255) / 256) * g.d);
     t.qp = c.take<float>(g.BH * g.tm * g.d);
     t.kp = c.take<float>(g.BH * ((g.tn + 3) & ~int64_t(3)) * g.d);  // transposed rows padded to 4 keys
     t.qbar = c.take<float>(g.BH * g.tm * g.d);
@@ -304,6 +308,53 @@ float inv_sqrt(int64_t d) {
 
 namespace sla2dev {
 void timeline_mark(int slot, cudaStream_t st) { mark(slot, st); }
+
+static int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+cudaStream_t aux_stream(int slot, int prio) {
+    thread_local std::unordered_map<int64_t, cudaStream_t> streams;
+    const int64_t key = ((int64_t)current_device() << 16) | (int64_t)(slot & 0xffff);
+    auto it = streams.find(key);
+    if (it != streams.end()) return it->second;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio > 0 ? hi : prio < 0 ? lo : 0);
+    streams.emplace(key, s);
+    return s;
+}
+
+cudaEvent_t aux_event(int slot) {
+    thread_local std::unordered_map<int64_t, cudaEvent_t> events;
+    const int64_t key = ((int64_t)current_device() << 16) | (int64_t)(slot & 0xffff);
+    auto it = events.find(key);
+    if (it != events.end()) return it->second;
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    events.emplace(key, e);
+    return e;
+}
+
+cudaError_t ensure_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> done[64];  // per device: func -> largest size set
+    const int dev = current_device() & 63;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = done[dev].find(func);
+        if (it != done[dev].end() && it->second >= bytes) return cudaSuccess;
+    }
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    int& m = done[dev][func];
+    if (bytes > m) m = bytes;
+    return cudaSuccess;
+}
 }  // namespace sla2dev
 
 // =============================================================================================
@@ -360,7 +411,7 @@ int64_t sla2_topk_budget(double k_percent, int64_t tn) {
 
 // Checks the reference's own prologues make (shapes, budget, tau) plus the dtype/quant enums;
 // enough for the router entry points, which have no kernel-geometry limits.
-static sla2_status check_common(const sla2_fwd_params* p) {
+static sla2_status check_common(const sla2_fwd_params* p, bool hard_budget = true) {
     g_last_error.clear();
     if (!p) return fail(SLA2_CONTRACT_ERROR, "params is NULL");
     if (p->B <= 0 || p->H <= 0 || p->N <= 0 || p->d <= 0)
@@ -371,7 +422,7 @@ static sla2_status check_common(const sla2_fwd_params* p) {
         // the reference's rule (attention.hpp:39-41); the ragged extension (partial last blocks,
         // SURVEY.md 8f item 2) exists on the bf16 tcgen05 path only
         return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
-    if (!(p->k_percent > 0.0 && p->k_percent <= 100.0))
+    if (hard_budget && !(p->k_percent > 0.0 && p->k_percent <= 100.0))
         return fail(SLA2_SHAPE_ERROR, "hard_topk: k_percent must be in (0, 100]");  // router.hpp:108-110
     if (!(p->tau > 0.0f)) return fail(SLA2_NUMERIC_ERROR, "RouterParams: tau must be positive");  // router.hpp:32
     if (p->dtype != SLA2_F32 && p->dtype != SLA2_BF16) return fail(SLA2_CONTRACT_ERROR, "unknown dtype");
@@ -394,6 +445,11 @@ sla2_status sla2_check_params(const sla2_fwd_params* p) {
             return fail(SLA2_CONTRACT_ERROR, "INT8 QAT mode runs on the bf16 inputs path");
         if (p->d > 128 || p->bk > 128 || p->bq > 256 || p->bq < 1 || (256 % p->bq) != 0)
             return fail(SLA2_CONTRACT_ERROR, "fp32 path: d <= 128, bk <= 128, bq a power of two <= 256");
+        // per-thread register arrays of the CUDA-core kernel: TPR = 256 / bq threads per query
+        // row hold ceil(d / TPR) O columns and ceil(bk / TPR) scores, 64 each at most
+        const int64_t tpr = p->bq >= 8 ? 256 / p->bq : 32;
+        if ((p->d + tpr - 1) / tpr > 64 || (p->bk + tpr - 1) / tpr > 64)
+            return fail(SLA2_CONTRACT_ERROR, "fp32 path: ceil(d / (256 / bq)) and ceil(bk / (256 / bq)) must be <= 64");
         if (sparse_f32_smem_bytes((int)p->d, (int)p->bq, (int)p->bk) > 227 * 1024)
             return fail(SLA2_CONTRACT_ERROR, "fp32 path: bq*d + 3*bk*d + bq*bk exceeds shared memory");
     }
@@ -413,7 +469,6 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
-    cudaEvent_t early = nullptr;  // fork the linear precompute here, with its own parallel mean
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
     float* kbar = nullptr;
@@ -458,16 +513,8 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     la.tm_v = &mv;
     la.tm_k = (g.bf16 && g.d == 128 && g.bk == 64) ? &mk : nullptr;
     cudaEvent_t dep = plan.dep;
-    if (plan.early) {
-        // phi(K~) only feeds the linear branch (tolerance 1e-2): it smooths with a parallel fp64
-        // mean (a few ulps from the serial one) and starts with the call, beside the serial
-        // column mean, instead of after it. The router keeps the exact mean (bit-exact mask).
-        la.mu = w.mu_lin;
-        la.phik_ready = false;
-        dep = plan.early;
-    } else if (plan.kprep) {
-        thread_local cudaEvent_t ev_k = nullptr;
-        if (!ev_k) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming));
+    if (plan.kprep) {
+        cudaEvent_t ev_k = aux_event(10);
         // fork at mu: phi(K~), z_j and Htot on the linear stream, beside the router's pooled
         // keys (launch_kpool, below) and back half on st
         la.phik_ready = !(la.tm_k && la.mu);  // the fused kernel computes phi(K~) itself
@@ -475,24 +522,13 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         dep = ev_k;
     }
     if (dep) {
-        thread_local cudaStream_t lin = nullptr;
-        thread_local cudaEvent_t lin_done = nullptr;
-        if (!lin) {
-            // lowest priority: the block scheduler serves the router (the critical path) first;
-            // the linear precompute has slack
-            int lo = 0, hi = 0;
-            cudaDeviceGetStreamPriorityRange(&lo, &hi);
-            SLA2_CUDA_TRY(cudaStreamCreateWithPriority(&lin, cudaStreamNonBlocking, lo));
-            SLA2_CUDA_TRY(cudaEventCreateWithFlags(&lin_done, cudaEventDisableTiming));
-        }
+        // lowest priority: the block scheduler serves the router (the critical path) first;
+        // the linear precompute has slack
+        cudaStream_t lin = aux_stream(1, -1);
+        cudaEvent_t lin_done = aux_event(11);
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
-        if (plan.early)
-            SLA2_CUDA_TRY(launch_colmean_fast(k, g.bf16, w.mu_lin_part, w.mu_lin, (int)g.BH, (int)g.N, (int)g.d, lin,
-                                              &g_launches));
         if (plan.kprep && la.phik_ready) SLA2_CUDA_TRY(launch_kphi(la, lin, &g_launches));
-#ifndef SLA2_EXP_NOLIN  // experiment only: router timeline without the concurrent linear precompute
         SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
-#endif
         mark(8, lin);
         SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
         if (plan.kprep) {
@@ -678,9 +714,8 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
     mark(0, st);
     // the linear precompute needs only mu: the router records mu_ready and the precompute
     // forks off it, overlapping the router's key side (pooling, projection, scores, top-k)
-    thread_local cudaEvent_t ev_mu = nullptr;
-    if (!ev_mu && cudaEventCreateWithFlags(&ev_mu, cudaEventDisableTiming) != cudaSuccess)
-        return fail(SLA2_CUDA_ERROR, "cudaEventCreate failed");
+    cudaEvent_t ev_mu = aux_event(12);
+    if (!ev_mu) return fail(SLA2_CUDA_ERROR, "cudaEventCreate failed");
     if (g.d == 128 && 4 * g.bk * 128 * (g.bf16 ? 2 : 4) <= 200 * 1024) {
         // router front (mu, query side) -> pooled keys -> router back (projection, scores, top-k),
         // with phi(K~), z_j and Htot forked beside the router's back half
@@ -690,29 +725,11 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         ra.kbar_ready = true;
         // phi(Q) on the query side, beside the serial column mean (written by the query pooling).
         // Measured alternatives: phi(Q) on the linear stream (mu 10 us earlier, but the router's
-        // back half 18 us later); the early fork below.
+        // back half 18 us later); starting the linear precompute with the call on its own
+        // parallel mean (0.649-0.708 vs 0.632 ms: its CTAs hold the SMs the serial column mean
+        // and the router need).
         ra.phiq_out = w.phiq;
         LinPlan plan;
-#if defined(SLA2_EARLY_LIN)
-        // Experiment (measured slower, 0.649-0.708 vs 0.632 ms at cfg2): start the linear
-        // precompute with the call, on its own parallel mean. Its CTAs then hold the SMs the
-        // serial column mean and the router need, and the critical path grows.
-        thread_local cudaEvent_t ev_start = nullptr;
-        if (g.bf16 && p->smooth) {
-            if (!ev_start) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-            SLA2_CUDA_TRY(cudaEventRecord(ev_start, st));
-            plan.early = ev_start;
-        }
-#elif defined(SLA2_QUERY_LIN)
-        // Experiment (measured slower, 0.670 vs 0.649 ms): fork the linear precompute (own
-        // parallel mean) when the query side is done, ~15 us before the serial mean
-        thread_local cudaEvent_t ev_qd = nullptr;
-        if (g.bf16 && p->smooth) {
-            if (!ev_qd) SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_qd, cudaEventDisableTiming));
-            ra.query_done = ev_qd;
-            plan.early = ev_qd;
-        }
-#endif
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;
         plan.phiq_ready = w.phiq != nullptr;
@@ -946,7 +963,9 @@ static sla2_status check_soft(const sla2_fwd_params* p, const char* who) {
 
 sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* values, float* lambdas, void* stream) {
     g_launches = 0;
-    sla2_status s = check_common(p);  // only the score geometry tm x tn matters here
+    // only the score geometry tm x tn matters here; soft_topk clamps any k% through topk_budget
+    // (router.hpp:130-134) instead of hard_topk's (0, 100] check
+    sla2_status s = check_common(p, false);
     if (s != SLA2_OK) return s;
     if (p->N % p->bq != 0 || p->N % p->bk != 0)
         return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
@@ -954,7 +973,11 @@ sla2_status sla2_soft_topk(const sla2_fwd_params* p, const float* pc, float* val
     if (!pc || !values || !lambdas) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
     const Geo g = geometry(p);
     cudaStream_t st = (cudaStream_t)stream;
-    thread_local int* dfail = nullptr;
+    // per-device flag (a process may drive several GPUs)
+    thread_local std::unordered_map<int, int*> dfails;
+    int dev = 0;
+    SLA2_CUDA_TRY(cudaGetDevice(&dev));
+    int*& dfail = dfails[dev];
     if (!dfail) SLA2_CUDA_TRY(cudaMalloc(&dfail, sizeof(int)));
     SLA2_CUDA_TRY(cudaMemsetAsync(dfail, 0, sizeof(int), st));
     const double kappa = (double)sla2_topk_budget(p->k_percent, g.tn);
@@ -1065,35 +1088,29 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
     hp.B = 1;
     hp.H = 1;
     const size_t wsb = carve(geometry(&hp), nullptr, nullptr);
-    // one cached device arena and three streams per thread
-    thread_local void* arena = nullptr;
-    thread_local size_t arena_bytes = 0;
-    thread_local cudaStream_t st = nullptr, up = nullptr, up2 = nullptr, down = nullptr;
-    thread_local cudaEvent_t ev_in = nullptr, ev_in2 = nullptr, ev_out = nullptr;
-    // one upload stream: a second one (a head's V beside its K and Q, SLA2_H2D_STREAMS=2)
-    // measured slower, 7.08 vs 6.70 ms at cfg2 -- the copies already run at the link's rate
-    // (~45 GB/s pinned H2D on the box; tools/e2e_ab.py)
-    static const int n_up = [] {
-        const char* e = std::getenv("SLA2_H2D_STREAMS");
-        return (e && std::atoi(e) == 2) ? 2 : 1;
-    }();
+    // one cached device arena and three streams per (thread, device). One upload stream: a
+    // second one (a head's V beside its K and Q) measured slower, 7.08 vs 6.70 ms at cfg2 -- the
+    // copies already run at the link's rate (~45 GB/s pinned H2D on the box; tools/e2e_ab.py)
+    int dev = 0;
+    SLA2_CUDA_TRY(cudaGetDevice(&dev));
+    struct Arena {
+        void* ptr = nullptr;
+        size_t bytes = 0;
+    };
+    thread_local std::unordered_map<int, Arena> arenas;
+    Arena& ar = arenas[dev];
     const size_t need = 4 * tensor + 2 * projb + rhob + maskb + wsb + 10 * 256;
-    if (need > arena_bytes) {
-        if (arena) cudaFree(arena);
-        arena = nullptr;
-        arena_bytes = 0;
-        SLA2_CUDA_TRY(cudaMalloc(&arena, need));
-        arena_bytes = need;
+    if (need > ar.bytes) {
+        if (ar.ptr) cudaFree(ar.ptr);
+        ar.ptr = nullptr;
+        ar.bytes = 0;
+        SLA2_CUDA_TRY(cudaMalloc(&ar.ptr, need));
+        ar.bytes = need;
     }
-    if (!st) {
-        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&up2, cudaStreamNonBlocking));
-        SLA2_CUDA_TRY(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_in2, cudaEventDisableTiming));
-        SLA2_CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-    }
+    void* arena = ar.ptr;
+    cudaStream_t st = aux_stream(20, 0), up = aux_stream(21, 0), down = aux_stream(22, 0);
+    cudaEvent_t ev_in = aux_event(20), ev_out = aux_event(21);
+    if (!st || !up || !down || !ev_in || !ev_out) return fail(SLA2_CUDA_ERROR, "stream/event creation failed");
     Carver c{reinterpret_cast<uint8_t*>(arena)};
     uint8_t* dq = c.take<uint8_t>(tensor);
     uint8_t* dk = c.take<uint8_t>(tensor);
@@ -1114,16 +1131,11 @@ sla2_status sla2_forward_host(const sla2_fwd_params* p, const void* q, const voi
         const size_t o = (size_t)bh * head;
         const int64_t h = bh % g.H;
         // K first: the column mean, the head's latency-bound first stage, needs only K
-        cudaStream_t upv = n_up == 2 ? up2 : up;
         SLA2_CUDA_TRY(cudaMemcpyAsync(dk + o, hk + o, head, cudaMemcpyHostToDevice, up));
         SLA2_CUDA_TRY(cudaMemcpyAsync(dq + o, hq + o, head, cudaMemcpyHostToDevice, up));
-        SLA2_CUDA_TRY(cudaMemcpyAsync(dv + o, hv + o, head, cudaMemcpyHostToDevice, upv));
+        SLA2_CUDA_TRY(cudaMemcpyAsync(dv + o, hv + o, head, cudaMemcpyHostToDevice, up));
         SLA2_CUDA_TRY(cudaEventRecord(ev_in, up));
         SLA2_CUDA_TRY(cudaStreamWaitEvent(st, ev_in, 0));
-        if (n_up == 2) {
-            SLA2_CUDA_TRY(cudaEventRecord(ev_in2, upv));
-            SLA2_CUDA_TRY(cudaStreamWaitEvent(st, ev_in2, 0));
-        }
         uint8_t* hm = mask_out ? dmask + (size_t)bh * head_mask : nullptr;
         s = sla2_forward(&hp, dq + o, dk + o, dv + o, dpq + h * g.d * g.d, dpk + h * g.d * g.d, drho + h * g.tm,
                          dout + o, hm, nullptr, nullptr, dws, wsb, st);

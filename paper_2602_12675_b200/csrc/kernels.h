@@ -7,6 +7,15 @@
 
 namespace sla2dev {
 
+// ---- per-device host state (capi.cu)
+// Helper streams / events are cached per (thread, current device) and the >48 KB shared-memory
+// attribute is set once per (device, kernel): a process that drives two GPUs never queues
+// device-1 work on a device-0 stream nor launches on a device whose attribute was not set.
+// `slot` names the call site; prio: +1 highest stream priority, -1 lowest, 0 default.
+cudaStream_t aux_stream(int slot, int prio);
+cudaEvent_t aux_event(int slot);
+cudaError_t ensure_smem_attr(const void* func, int bytes);
+
 // ---- router (router.cu)
 struct RouterLaunch {
     const void* q;
@@ -42,8 +51,6 @@ cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches)
 cudaError_t launch_router_front(const RouterLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_router_back(const RouterLaunch& a, cudaStream_t st, int* launches);
 // parallel fp64 column mean (not the reference's serial order): the linear branch's mu
-cudaError_t launch_colmean_fast(const void* k, bool bf16, double* part, float* mu, int BH, int N, int d,
-                                cudaStream_t st, int* launches);
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,
                            cudaStream_t st, int* launches);
 cudaError_t launch_topk_only(const float* pc, int BH, int tm, int tn, int kappa, uint8_t* mask, int32_t* idx,

@@ -726,11 +726,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
     dim3 g1(tn, (unsigned)a.BH);
     if (a.bf16 && a.tm_k && !a.phik_ready) {
         // phi(K~), z_j and the Htot partials in one pass over K and V
-        static bool attr_f = false;
-        if (!attr_f) {
-            cudaFuncSetAttribute(kphi_htot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kh::SMEM);
-            attr_f = true;
-        }
+        ensure_smem_attr((const void*)kphi_htot_kernel, (int)(kh::SMEM));
         const int per = (tn + a.nchunk - 1) / a.nchunk;
         kphi_htot_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 192, kh::SMEM, st>>>(
             *a.tm_k, *a.tm_v, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.hpart, a.N, per, a.nchunk);
@@ -738,11 +734,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
         if (!a.phik_ready)
             phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(
                 (const __nv_bfloat16*)a.k, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.N, a.d, a.bk);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(htot_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ht::SMEM);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)htot_umma_kernel, (int)(ht::SMEM));
         const int per = (tn + a.nchunk - 1) / a.nchunk;
         htot_umma_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 128, ht::SMEM, st>>>(*a.tm_phik, *a.tm_v, a.hpart, a.N,
                                                                                  per, a.nchunk);

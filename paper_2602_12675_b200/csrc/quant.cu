@@ -581,11 +581,7 @@ cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* laun
     p.tn = a.s.tn;
     p.inv_sqrt_d = a.s.inv_sqrt_d;
     if (a.s.o_s == nullptr && a.s.o_l != nullptr) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(sla2_sparse_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, qp::SMEM_ALLOC);
-        attr = true;
-    }
+    ensure_smem_attr((const void*)sla2_sparse_i8_kernel, (int)(qp::SMEM_ALLOC));
     dim3 grid(a.s.tm, (unsigned)(a.s.B * a.s.H));
     sla2_sparse_i8_kernel<<<grid, 256, qp::SMEM_ALLOC, st>>>(*a.tm_qc, *a.s.tm_q, *a.tm_kc, *a.tm_vct, *a.s.tm_v,
                                                               *a.s.tm_phik, *a.s.tm_ht, p);

@@ -1070,19 +1070,11 @@ static void colmean_t(const void* k, const CUtensorMap* tmk, float* mu, int BH, 
     if (sizeof(T) == 2 && tmk && d % cmt::COLS == 0) {
         // (padding the shared memory so no other CTA shares the SM measured no faster)
         const int smem = (cmt::NST + cmt::NTS) * cmt::TILE;
-        static bool attr_t = false;
-        if (!attr_t) {
-            cudaFuncSetAttribute(colmean_tr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr_t = true;
-        }
+        ensure_smem_attr((const void*)colmean_tr_kernel, (int)(smem));
         colmean_tr_kernel<<<dim3(d / cmt::COLS, BH), 160, smem, st>>>(*tmk, mu, N, d);
     } else if (tmk && N % cm::ROWS == 0 && d % COLS == 0) {
         const int smem = cm::NST * cm::ROWS * 128;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(colmean_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)colmean_tma_kernel<T>, (int)(smem));
         colmean_tma_kernel<T><<<dim3(d / COLS, BH), (COLS / 32 + 1) * 32, smem, st>>>(*tmk, mu, N, d);
     } else {
         colmean_exact_kernel<T><<<dim3((d + 31) / 32, BH), 32, 0, st>>>((const T*)k, mu, N, d);
@@ -1121,17 +1113,10 @@ static cudaError_t router_front_t(const RouterLaunch& a, cudaStream_t st, int* l
     const int BH = (int)(a.B * a.H);
     // The exact column mean is a serial chain on a few SMs: run it on a side stream,
     // concurrently with the query-side pooling/projection, and join before the key side.
-    thread_local cudaStream_t side = nullptr;
-    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (!side) {
-        // highest priority: the block scheduler must place the colmean CTAs (the critical
-        // path) ahead of the query-side pooling grid launched right after them
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
-        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
-    }
+    // highest priority: the block scheduler must place the colmean CTAs (the critical path)
+    // ahead of the query-side pooling grid launched right after them
+    cudaStream_t side = aux_stream(2, +1);
+    cudaEvent_t ev_fork = aux_event(30), ev_join = aux_event(31);
     bool forked = false;
     if (a.mu_out) {
         if (a.exact_mu) {
@@ -1217,20 +1202,6 @@ cudaError_t launch_router_back(const RouterLaunch& a, cudaStream_t st, int* laun
 cudaError_t launch_router(const RouterLaunch& a, cudaStream_t st, int* launches) {
     const cudaError_t e = launch_router_front(a, st, launches);
     return e != cudaSuccess ? e : launch_router_back(a, st, launches);
-}
-
-cudaError_t launch_colmean_fast(const void* k, bool bf16, double* part, float* mu, int BH, int N, int d,
-                                cudaStream_t st, int* launches) {
-    // parallel column mean (fp64 partial sums, one rounding): within a few ulps of the serial
-    // mean, for the linear branch only (tolerance-level); the router keeps the exact serial mean
-    const int rows_per = 256, nch = (N + rows_per - 1) / rows_per;
-    if (bf16)
-        colmean_partial_kernel<__nv_bfloat16><<<dim3(nch, BH), d, 0, st>>>((const __nv_bfloat16*)k, part, N, d, rows_per);
-    else
-        colmean_partial_kernel<float><<<dim3(nch, BH), d, 0, st>>>((const float*)k, part, N, d, rows_per);
-    colmean_finish_kernel<<<BH, d, 0, st>>>(part, mu, nch, N, d);
-    *launches += 2;
-    return cudaGetLastError();
 }
 
 cudaError_t launch_colmean(const void* k, const CUtensorMap* tmk, bool bf16, float* mu, int BH, int N, int d,

@@ -215,11 +215,7 @@ cudaError_t launch_soft_topk_backward(const float* values, const float* upstream
 
 cudaError_t launch_soft_forward(const SoftLaunch& a, cudaStream_t st, int* launches) {
     if (a.d > sf::MAXD || a.bq > sf::MAXB || a.bk > sf::MAXB) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(soft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)soft_forward_smem());
-        attr = true;
-    }
+    ensure_smem_attr((const void*)soft_forward_kernel, (int)((int)soft_forward_smem()));
     soft_forward_kernel<<<dim3(a.tm, (unsigned)a.BH), 256, soft_forward_smem(), st>>>(
         a.q, a.k, a.v, a.mu, a.values, a.rho, a.h, a.z, a.out, a.o_s, a.o_l, a.big_l, a.N, a.d, a.bq, a.bk, a.tm,
         a.tn, (int)a.H, a.inv_sqrt_d);

@@ -44,13 +44,7 @@ namespace sla2dev {
 
 namespace sp {
 constexpr int BQ = 128, BK = 64, D = 128;
-#ifndef SLA2_NKP
-#define SLA2_NKP 2
-#endif
-#ifndef SLA2_NSV
-#define SLA2_NSV 4
-#endif
-constexpr int NKP = SLA2_NKP, NSV = SLA2_NSV;  // K pair ring (32 KB/stage), V+phi(K) ring (32 KB/stage)
+constexpr int NKP = 2, NSV = 4;  // K pair ring (32 KB/stage), V+phi(K) ring (32 KB/stage)
 constexpr uint32_t Q_BYTES = BQ * D * 2;     // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;  // 16 KB (one K, V or phi(K) tile)
 constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // K pair: [k_atom 2][128 rows][128 B]
@@ -62,15 +56,7 @@ constexpr uint32_t SMEM_BYTES = OFF_V + NSV * 2 * TILE_BYTES;  // 224 KB
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
 // TMEM columns (512 allocated)
 constexpr uint32_t TM_S = 0;    // 128: S fp32 of the current pair (block 2p in cols 0-63, 2p+1 in 64-127)
-#ifndef SLA2_Q_TMEM
 constexpr uint32_t TM_P = 128;  // 2 x 64: P bf16 of pairs n & 1 (block 2p in the first 32, 2p+1 next)
-#else
-// Experiment (-DSLA2_Q_TMEM, measured slower: 0.365 vs 0.355 ms at cfg2, the pair period grows
-// from 1.28 to 1.40 us): Q in TMEM as the A operand of Q K^T (TS MMA: shared memory feeds only K);
-// P then has one 64-column buffer
-constexpr uint32_t TM_P = 128;  // 64: P bf16 of the current pair
-constexpr uint32_t TM_Q = 192;  // 64: Q bf16, packed pairs along d
-#endif
 constexpr uint32_t TM_O = 256;  // 128: O accumulator
 constexpr uint32_t TM_H = 384;  // 128: Hsel accumulator
 constexpr uint32_t TM_L = 0;    // 128: phi(Q) Hc after the loop (the S columns are free then)
@@ -260,11 +246,7 @@ __global__ void __launch_bounds__(256, 1)
             if (linear) {
                 // phi(Q) over Q once nothing reads Q from shared memory any more (same layout)
                 tma_prefetch_desc(&tmPq);
-#ifndef SLA2_Q_TMEM
                 mbar_wait(&bar_qk_done, 0);
-#else
-                mbar_wait(&bar_qt, 0);
-#endif
                 mbar_arrive_expect_tx(&bar_pq, Q_BYTES);
                 tma_load_3d(sQ, &tmPq, 0, qrow, hz, &bar_pq);
                 tma_load_3d(sQ + 8192, &tmPq, 0, qrow + 64, hz, &bar_pq);
@@ -278,11 +260,7 @@ __global__ void __launch_bounds__(256, 1)
             tma_prefetch_desc(&tmV);
             if (!dense) tma_prefetch_desc(&tmPhi);
             const uint64_t pol_keep = policy_evict_last();
-#ifdef SLA2_EXP_NOPHIK
-            const bool ldphi = false;  // experiment: no phi(K) traffic (with SLA2_EXP_NOHS)
-#else
             const bool ldphi = !dense;
-#endif
             const uint32_t tx = ldphi ? 2 * TILE_BYTES : TILE_BYTES;
             // stages 0 .. NV0-1 were issued by thread 0 before the CTA barrier (with phi(K~) unless
             // dense; the SLA2_EXP_NOPHIK experiment loads V only from stage NV0 on)
@@ -336,11 +314,7 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t dQ = sdesc_sw128(sbase + OFF_Q, 16, 1024);
         const uint64_t dK0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
         const uint64_t dVm = sdesc_sw128(sbase + OFF_V, 8192, 1024);  // MN-major V / phi(K) tiles
-#ifndef SLA2_Q_TMEM
         mbar_wait(&bar_q, 0);
-#else
-        mbar_wait(&bar_qt, 0);
-#endif
         tc_fence_after();
         if (lane == 0) SLA2_TR(1);
         // Static issue order (the tensor pipe runs MMAs in issue order):
@@ -358,11 +332,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
-#ifndef SLA2_Q_TMEM
                 umma_bf16_ss_w(tm + TM_S, dQ + off, dK + off, idq, ks > 0);
-#else
-                umma_bf16_ts_w(tm + TM_S, tm + TM_Q + ks * 8, dK + off, idq, ks > 0);
-#endif
             }
             umma_commit_w(&bar_s_full);
             umma_commit_w(&bar_k_empty[s]);
@@ -386,11 +356,7 @@ __global__ void __launch_bounds__(256, 1)
                 tc_fence_after();
                 if (lane == 0 && j < 16) SLA2_TR(80 + j);
                 const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
-#ifndef SLA2_Q_TMEM
                 const uint32_t aP = tm + TM_P + (n & 1) * 64 + (j & 1) * 32;
-#else
-                const uint32_t aP = tm + TM_P + (j & 1) * 32;
-#endif
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
                     umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
@@ -403,14 +369,10 @@ __global__ void __launch_bounds__(256, 1)
                     const int sv = j % NSV;
                     const uint64_t dV = dVm + ((sv * 2 * TILE_BYTES) >> 4);
                     const uint64_t dP = dV + (TILE_BYTES >> 4);  // phi(K) tile follows V in the stage
-#ifndef SLA2_EXP_NOHS
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
                         umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
                                        (j > 0 || ks > 0));
-#else
-                    (void)dP;
-#endif
                     umma_commit_w(&bar_v_empty[sv]);  // after PV_j and HS_j
                 }
             }
@@ -463,23 +425,6 @@ __global__ void __launch_bounds__(256, 1)
         const float rho_i = linear ? p.rho[(int64_t)h * p.tm + i] : 0.0f;  // loaded now, used after the loop
         // ragged N: does this row keep the partial last key block? (one load, before the loop)
         const bool tail_kept = p.last_valid < BK && kblock(nb - 1) == p.tn - 1;
-#ifdef SLA2_Q_TMEM
-        {
-            // row r of Q (SW128 tile in sQ) -> TMEM lane r, 64 columns of packed bf16 pairs
-            mbar_wait(&bar_q, 0);
-            const uint32_t qb = smem_u32(sQ);
-            uint32_t qw[64];
-#pragma unroll
-            for (int ch = 0; ch < 16; ++ch)
-                ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), qw[4 * ch], qw[4 * ch + 1],
-                             qw[4 * ch + 2], qw[4 * ch + 3]);
-            tmem_st32(tmem + lane_base + TM_Q, *reinterpret_cast<uint32_t(*)[32]>(&qw[0]));
-            tmem_st32(tmem + lane_base + TM_Q + 32, *reinterpret_cast<uint32_t(*)[32]>(&qw[32]));
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&bar_qt);
-        }
-#endif
         float m2 = -INFINITY, l = 0.0f;
         for (int n = 0; n < npair; ++n) {
             const int b = n & 1;
@@ -548,7 +493,6 @@ __global__ void __launch_bounds__(256, 1)
                     m2 = mnew;
                 }
             }
-#ifndef SLA2_Q_TMEM
             // P = exp2(s * scale - m2) as packed bf16 into P buffer n & 1, last read by PV(n-2)
             if (n >= 2) {
                 mbar_wait(&bar_pv_done[b], ((n - 2) >> 1) & 1);
@@ -556,15 +500,6 @@ __global__ void __launch_bounds__(256, 1)
                 tc_fence_after();
             }
             const uint32_t pbase = tmem + lane_base + TM_P + b * 64;
-#else
-            // P = exp2(s * scale - m2) as packed bf16 into the P buffer, last read by PV(n-1)
-            if (n >= 1) {
-                mbar_wait(&bar_pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
-                __syncwarp();
-                tc_fence_after();
-            }
-            const uint32_t pbase = tmem + lane_base + TM_P;
-#endif
             float rs0 = 0.0f, rs1 = 0.0f;
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) {
@@ -759,11 +694,7 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
 #ifdef SLA2_TRACE
     p.trace = g_trace_buf;
 #endif
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(sla2_sparse_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::SMEM_ALLOC);
-        attr = true;
-    }
+    ensure_smem_attr((const void*)sla2_sparse_bf16_kernel, (int)(sp::SMEM_ALLOC));
     if (a.o_s == nullptr && a.o_l != nullptr) return cudaErrorInvalidValue;
     dim3 grid(a.tm, (unsigned)(a.B * a.H));
     if ((!a.dense && !a.tm_phiq) || !a.tm_out) return cudaErrorInvalidValue;

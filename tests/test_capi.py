@@ -51,6 +51,9 @@ def test_default_params_are_the_papers():
     (dict(d=64), sla2.ContractError),                     # bf16 kernels are d = 128 only
     (dict(bf16=False, bq=96, N=3072), sla2.ContractError),  # fp32 path: bq power of two
     (dict(bf16=False, quant=True), sla2.ContractError),
+    # fp32 path, bq = 256: one thread per query row holds d O columns and bk scores (<= 64 each)
+    (dict(bf16=False, bq=256, bk=16, N=4096), sla2.ContractError),   # d = 128 columns
+    (dict(bf16=False, bq=256, bk=128, d=16, N=4096), sla2.ContractError),  # 128 scores
 ])
 def test_validation_errors(kw, err):
     base = dict(B=1, H=2, N=4096, d=128)
@@ -60,6 +63,11 @@ def test_validation_errors(kw, err):
         setattr(p, k, v)
     with pytest.raises(err):
         sla2.workspace_bytes(p)
+
+
+def test_f32_bq256_within_register_arrays_accepted():
+    p = sla2.FwdParams(1, 1, 1024, 64, bq=256, bk=64, k_percent=25.0, bf16=False)
+    assert sla2.workspace_bytes(p) > 0
 
 
 def test_workspace_size_cfg2():

@@ -179,7 +179,8 @@ def test_forward_qat_vs_oracle(cuda, N, H, k_percent, seed):
 @pytest.mark.parametrize("N,d,bq,bk,k_percent", [(4096, 64, 64, 64, 10.0), (1024, 32, 32, 16, 25.0),
                                                  (64, 8, 8, 4, 10.0), (64, 8, 8, 4, 50.0),
                                                  (32, 8, 4, 4, 25.0), (32, 8, 4, 8, 25.0),   # bq < 8
-                                                 (2048, 128, 128, 64, 5.0)])                 # Wan blocks, fp32
+                                                 (2048, 128, 128, 64, 5.0),                  # Wan blocks, fp32
+                                                 (1024, 64, 256, 64, 25.0)])                 # bq 256: 1 thread/row
 def test_forward_f32_vs_oracle(cuda, N, d, bq, bk, k_percent):
     torch = _torch()
     B, H = 1, 2
