@@ -65,11 +65,21 @@ typedef struct {
     int32_t reserved[3];
 } sla2_fwd_params;
 
-/* Optional per-branch outputs (SLA2ForwardSaved, attention.hpp:345-358), fp32, device. */
+/* Optional saved state (SLA2ForwardSaved, attention.hpp:345-358), fp32, device; every member
+ * may be NULL. o_l requires o_s. The routing/flags/block sizes of the reference struct are the
+ * caller's own inputs (mask_out / kv_idx_out, p). */
 typedef struct {
-    float* o_s;   /* [B,H,N,d] sparse-branch output O_s, or NULL */
-    float* o_l;   /* [B,H,N,d] linear-branch output O_l, or NULL (rows of full mask rows = 0) */
-    float* big_l; /* [B,H,N] logsumexp L = m + log l, or NULL */
+    float* o_s;      /* [B,H,N,d] sparse-branch output O_s */
+    float* o_l;      /* [B,H,N,d] linear-branch output O_l (rows of full mask rows = 0) */
+    float* big_l;    /* [B,H,N] logsumexp L = m + log l */
+    float* h_blocks; /* [B,H,tm,d,d] per query block complement H_i = sum over unselected j of
+                      * h_j = phi(K~_j)^T V_j (attention.hpp:495-502; formed as total minus
+                      * selected, tolerance-level; zero for full rows) */
+    float* z_blocks; /* [B,H,tm,d] complement Z_i = sum over unselected j of colsum phi(K~_j) */
+    float* q_phi;    /* [B,H,N,d] phi(Q) = row_softmax(Q) (attention.hpp:456), exact arithmetic */
+    float* k_phi;    /* [B,H,N,d] phi(K~) = row_softmax(K - colmean K) (457), exact arithmetic */
+    float* qat_s_first; /* QAT only, parity hook: [B,H,tm,bq,bk] the dequantized scores S of each
+                      * query block's first kept key block (block_scores_qk, 372-394) */
 } sla2_fwd_saved;
 
 /* Fills p with the reference defaults for one (B, H, N, d) problem: bq = 128, bk = 64
@@ -121,6 +131,19 @@ sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_o
  */
 sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* mask_out,
                            int32_t* kv_idx_out, void* stream);
+
+/*
+ * The QAT operand quantization (quantize, quant.hpp:31-50, on the blocks block_scores_qk and
+ * block_product_pv quantize, attention.hpp:379-380,401): per query block Q_i (bq x d), per key
+ * block K~_j = K_j - colmean(K) (bk x d, when p->smooth) and V_j (bk x d), the absmax/127 scale
+ * and the round-half-away codes in [-127, 127], bit-exact with the reference. q/k/v bf16
+ * [B,H,N,d]; codes int8 [B,H,N,d] (row-major, each block's rows contiguous); scales fp32
+ * q [B,H,tm], k and v [B,H,tn]. p: dtype bf16, quant int8. Workspace: sla2_workspace_size(p).
+ * This is the precompute sla2_forward runs before the kind::i8 kernel (exposed for parity).
+ */
+sla2_status sla2_quantize(const sla2_fwd_params* p, const void* q, const void* k, const void* v, int8_t* q_codes,
+                          float* q_scales, int8_t* k_codes, float* k_scales, int8_t* v_codes, float* v_scales,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * sla2_forward_blockwise (attention.hpp:423-560) with a caller-given BlockMask (device

@@ -112,6 +112,44 @@ int forward_blockwise_(const T* q, const T* k, const T* v, std::size_t n, std::s
     } catch (const std::exception& e) { return classify(e); }
 }
 
+// sla2_forward_blockwise's full SLA2ForwardSaved (attention.hpp:345-358): h_blocks [tm][d][d],
+// z_blocks [tm][d], q_phi / k_phi [n][d] besides o_s, o_l, big_l.
+template <class T>
+int forward_saved_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, std::size_t bq,
+                   std::size_t bk, const std::uint8_t* mask, const T* rho, int quant, int smooth, T* out, T* o_s,
+                   T* o_l, T* big_l, T* h_blocks, T* z_blocks, T* q_phi, T* k_phi) {
+    try {
+        AttentionInputs<T> in{wrap(q, n, d), wrap(k, n, d), wrap(v, n, d), bq, bk};
+        MixRatio<T> mix{Vector<T>(std::vector<T>(rho, rho + n / bq))};
+        QuantConfig qc;
+        auto [o, saved] = sla2_forward_blockwise(in, Routing<T>{wrap_mask(mask, n / bq, n / bk)}, mix,
+                                                 quant ? &qc : nullptr, smooth != 0);
+        copy_out(o, out);
+        copy_out(saved.o_s, o_s);
+        copy_out(saved.o_l, o_l);
+        std::memcpy(big_l, saved.big_l.data().data(), sizeof(T) * n);
+        for (std::size_t i = 0; i < saved.h_blocks.size(); ++i) {
+            copy_out(saved.h_blocks[i], h_blocks + i * d * d);
+            std::memcpy(z_blocks + i * d, saved.z_blocks[i].data().data(), sizeof(T) * d);
+        }
+        copy_out(saved.q_phi, q_phi);
+        copy_out(saved.k_phi, k_phi);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
+// detail::block_scores_qk (attention.hpp:372-394) for one (query block, key block): S = Q_i K_j^T /
+// sqrt(d), or through quantize -> quantized_product -> scale when quant (the QAT scores).
+template <class T>
+int block_scores_qk_(const T* q, const T* k, std::size_t n, std::size_t d, std::size_t qi0, std::size_t bq,
+                     std::size_t kj0, std::size_t bk, int quant, T* s) {
+    try {
+        QuantConfig qc;
+        copy_out(detail::block_scores_qk(wrap(q, n, d), wrap(k, n, d), qi0, bq, kj0, bk, quant ? &qc : nullptr), s);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
 template <class T>
 int forward_naive_(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,
                    std::size_t bq, std::size_t bk, const std::uint8_t* mask, const T* rho,
@@ -245,6 +283,18 @@ extern "C" {
                                     int smooth, T* out, T* o_s, T* o_l, T* big_l) {              \
         return forward_blockwise_<T>(q, k, v, n, d, bq, bk, mask, rho, quant, smooth, out, o_s,  \
                                      o_l, big_l);                                                 \
+    }                                                                                             \
+    int sla2r_forward_saved_##S(const T* q, const T* k, const T* v, std::size_t n, std::size_t d,  \
+                                std::size_t bq, std::size_t bk, const std::uint8_t* mask,        \
+                                const T* rho, int quant, int smooth, T* out, T* o_s, T* o_l,     \
+                                T* big_l, T* hb, T* zb, T* qp, T* kp) {                          \
+        return forward_saved_<T>(q, k, v, n, d, bq, bk, mask, rho, quant, smooth, out, o_s, o_l, \
+                                 big_l, hb, zb, qp, kp);                                         \
+    }                                                                                             \
+    int sla2r_block_scores_qk_##S(const T* q, const T* k, std::size_t n, std::size_t d,         \
+                                  std::size_t qi0, std::size_t bq, std::size_t kj0, std::size_t bk, \
+                                  int quant, T* s) {                                             \
+        return block_scores_qk_<T>(q, k, n, d, qi0, bq, kj0, bk, quant, s);                      \
     }                                                                                             \
     int sla2r_forward_naive_##S(const T* q, const T* k, const T* v, std::size_t n, std::size_t d, \
                                 std::size_t bq, std::size_t bk, const std::uint8_t* mask,        \

@@ -27,7 +27,7 @@ from typing import Optional
 
 __all__ = [
     "ShapeError", "NumericError", "ContractError", "CudaError", "Sla2Error",
-    "lib", "library_path", "topk_budget", "smooth_k", "block_scores", "hard_topk",
+    "lib", "library_path", "topk_budget", "smooth_k", "quantize", "block_scores", "hard_topk",
     "sla2_forward_blockwise", "sla2_attention", "full_attention", "router", "forward",
     "FwdParams", "workspace_bytes", "last_launch_count",
 ]
@@ -64,7 +64,27 @@ class _Params(C.Structure):
 
 
 class _Saved(C.Structure):
-    _fields_ = [("o_s", C.c_void_p), ("o_l", C.c_void_p), ("big_l", C.c_void_p)]
+    _fields_ = [("o_s", C.c_void_p), ("o_l", C.c_void_p), ("big_l", C.c_void_p), ("h_blocks", C.c_void_p),
+                ("z_blocks", C.c_void_p), ("q_phi", C.c_void_p), ("k_phi", C.c_void_p),
+                ("qat_s_first", C.c_void_p)]
+
+
+def _saved_buffers(p, q, full, qat_s):
+    """Device buffers for SLA2ForwardSaved (attention.hpp:345-358): o_s, o_l, big_l; with full=True
+    also h_blocks [B,H,tm,d,d], z_blocks [B,H,tm,d], q_phi, k_phi [B,H,N,d]; qat_s: the QAT S hook."""
+    import torch
+    dev = q.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    svs = {"o_s": torch.empty(q.shape, **f32), "o_l": torch.empty(q.shape, **f32), "big_l": torch.empty(q.shape[:3], **f32)}
+    if full:
+        svs["h_blocks"] = torch.empty((p.B, p.H, p.tm, p.d, p.d), **f32)
+        svs["z_blocks"] = torch.empty((p.B, p.H, p.tm, p.d), **f32)
+        svs["q_phi"] = torch.empty(q.shape, **f32)
+        svs["k_phi"] = torch.empty(q.shape, **f32)
+    if qat_s:
+        svs["qat_s_first"] = torch.empty((p.B, p.H, p.tm, p.bq, p.bk), **f32)
+    sv = _Saved(*[svs[n].data_ptr() if n in svs else None for n, _ in _Saved._fields_])
+    return sv, svs
 
 
 _lib = None
@@ -93,6 +113,7 @@ def lib():
         "sla2_router": ([P, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_smooth_k": ([P, vp, vp, vp, vp], C.c_int),
         "sla2_hard_topk": ([P, vp, vp, vp, vp], C.c_int),
+        "sla2_quantize": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_sparse_fwd": ([P, vp, vp, vp, vp, vp, vp, C.POINTER(_Saved), vp, sz, vp], C.c_int),
         "sla2_dense_fwd": ([P, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_forward_host": ([P, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
@@ -236,7 +257,8 @@ def _check_like(ref, *ts):
 def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant=False, smooth=True,
             exact_mu=True, return_mask=False, return_idx=False, saved=False, out=None, workspace=None):
     """Router + blockwise forward (tape.hpp:263-272). Returns out or a tuple with
-    (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested. `workspace` (a
+    (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested; saved=True gives
+    o_s, o_l, big_l, saved="full" all of SLA2ForwardSaved (+ the QAT S hook). `workspace` (a
     uint8 CUDA tensor of at least workspace_bytes(...)) replaces the shared per-device cache."""
     import torch
     _check_like(q, k, v)
@@ -250,10 +272,7 @@ def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant
     sv = None
     svs = None
     if saved:
-        svs = {"o_s": torch.empty(q.shape, dtype=torch.float32, device=dev),
-               "o_l": torch.empty(q.shape, dtype=torch.float32, device=dev),
-               "big_l": torch.empty(q.shape[:3], dtype=torch.float32, device=dev)}
-        sv = _Saved(svs["o_s"].data_ptr(), svs["o_l"].data_ptr(), svs["big_l"].data_ptr())
+        sv, svs = _saved_buffers(p, q, saved == "full", bool(quant) and saved == "full")
     if workspace is not None:
         if workspace.dtype != torch.uint8 or workspace.device != dev or workspace.numel() < workspace_bytes(p):
             raise ContractError("workspace too small (see workspace_bytes)")
@@ -341,6 +360,29 @@ def router(q, k, proj_q, proj_k, *, k_percent=3.0, bq=128, bk=64, smooth=True, e
     return pc, mask, idx
 
 
+def quantize(q, k, v, *, bq=128, bk=64, smooth=True):
+    """The QAT operand quantization (quantize, quant.hpp:31-50) of every query block of Q and key
+    block of K~ = K - colmean(K) and V, on device: returns {"q_codes", "k_codes", "v_codes" int8
+    [B,H,N,d], "q_scales" fp32 [B,H,tm], "k_scales", "v_scales" fp32 [B,H,tn]}, bit-exact."""
+    import torch
+    _check_like(q, k, v)
+    p = _params_from(q, bq, bk, 3.0, True, smooth, True)
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    dev = q.device
+    res = {"q_codes": torch.empty(q.shape, dtype=torch.int8, device=dev),
+           "k_codes": torch.empty(q.shape, dtype=torch.int8, device=dev),
+           "v_codes": torch.empty(q.shape, dtype=torch.int8, device=dev),
+           "q_scales": torch.empty((p.B, p.H, p.tm), dtype=torch.float32, device=dev),
+           "k_scales": torch.empty((p.B, p.H, p.tn), dtype=torch.float32, device=dev),
+           "v_scales": torch.empty((p.B, p.H, p.tn), dtype=torch.float32, device=dev)}
+    ws = _workspace(p, dev)
+    _raise(lib().sla2_quantize(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(res["q_codes"]), _ptr(res["q_scales"]),
+                               _ptr(res["k_codes"]), _ptr(res["k_scales"]), _ptr(res["v_codes"]),
+                               _ptr(res["v_scales"]), _ptr(ws), ws.numel(), _stream(dev)))
+    return res
+
+
 def smooth_k(k):
     """quant.hpp:88-96 on device: returns (K - mu as fp32, mu [B,H,d] fp32)."""
     import torch
@@ -390,10 +432,7 @@ def sla2_forward_blockwise(q, k, v, mask, rho, *, bq=128, bk=64, quant=False, sm
     sv = None
     svs = None
     if saved:
-        svs = {"o_s": torch.empty(q.shape, dtype=torch.float32, device=dev),
-               "o_l": torch.empty(q.shape, dtype=torch.float32, device=dev),
-               "big_l": torch.empty(q.shape[:3], dtype=torch.float32, device=dev)}
-        sv = _Saved(svs["o_s"].data_ptr(), svs["o_l"].data_ptr(), svs["big_l"].data_ptr())
+        sv, svs = _saved_buffers(p, q, saved == "full", bool(quant) and saved == "full")
     ws = _workspace(p, dev)
     _raise(lib().sla2_sparse_fwd(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()),
                                  _ptr(mask.contiguous().to(torch.uint8)), _ptr(out),
@@ -485,7 +524,8 @@ def forward_soft(q, k, v, rho, values, *, bq=64, bk=64, smooth=True, saved=False
     if saved:
         keep = {"o_s": torch.empty_like(q), "o_l": torch.empty_like(q),
                 "big_l": torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=dev)}
-        sv = _Saved(keep["o_s"].data_ptr(), keep["o_l"].data_ptr(), keep["big_l"].data_ptr())
+        sv = _Saved(keep["o_s"].data_ptr(), keep["o_l"].data_ptr(), keep["big_l"].data_ptr(), None, None, None, None,
+                    None)
     _raise(lib().sla2_forward_soft(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()),
                                    _ptr(values.contiguous()), _ptr(out), C.byref(sv) if sv is not None else None,
                                    _ptr(ws), n, _stream(dev)))

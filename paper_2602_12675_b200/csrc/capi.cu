@@ -577,6 +577,9 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     sa.o_s = saved ? saved->o_s : nullptr;
     sa.o_l = saved ? saved->o_l : nullptr;
     sa.big_l = saved ? saved->big_l : nullptr;
+    sa.h_blocks = saved ? saved->h_blocks : nullptr;
+    sa.z_blocks = saved ? saved->z_blocks : nullptr;
+    sa.s_first = saved ? saved->qat_s_first : nullptr;
     sa.q = (const float*)q;
     sa.k = (const float*)k;
     sa.v = (const float*)v;
@@ -633,12 +636,29 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             ia.tm_kc = &mkc;
             ia.tm_vct = &mvc;
             SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
-            return SLA2_OK;
+        } else {
+            SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
         }
-        SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
     } else {
         SLA2_CUDA_TRY(launch_sparse_f32(sa, st, &g_launches));
     }
+    if (saved && saved->q_phi)
+        SLA2_CUDA_TRY(launch_phi_exact(q, g.bf16, nullptr, saved->q_phi, g.BH * g.N, (int)g.N, (int)g.d, st,
+                                       &g_launches));
+    if (saved && saved->k_phi)
+        SLA2_CUDA_TRY(launch_phi_exact(k, g.bf16, p->smooth ? w.mu : nullptr, saved->k_phi, g.BH * g.N, (int)g.N,
+                                       (int)g.d, st, &g_launches));
+    return SLA2_OK;
+}
+
+// The saved-state members each path can fill (sla2_fwd_saved).
+static sla2_status check_saved(const sla2_fwd_params* p, const sla2_fwd_saved* saved) {
+    if (!saved) return SLA2_OK;
+    if (saved->o_l && !saved->o_s) return fail(SLA2_CONTRACT_ERROR, "saved: o_l requires o_s");
+    if ((saved->h_blocks == nullptr) != (saved->z_blocks == nullptr))
+        return fail(SLA2_CONTRACT_ERROR, "saved: h_blocks and z_blocks go together");
+    if (saved->qat_s_first && p->quant != SLA2_QUANT_INT8)
+        return fail(SLA2_CONTRACT_ERROR, "saved: qat_s_first is the INT8 QAT path's hook");
     return SLA2_OK;
 }
 
@@ -705,6 +725,7 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
     const Geo g = geometry(p);
     if (!q || !k || !v || !proj_q || !proj_k || !rho || !out)
         return fail(SLA2_CONTRACT_ERROR, "NULL input/output pointer");
+    if ((s = check_saved(p, saved)) != SLA2_OK) return s;
     if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
         return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
     Workspace w;
@@ -773,6 +794,51 @@ sla2_status sla2_smooth_k(const sla2_fwd_params* p, const void* k, float* mean_o
     return SLA2_OK;
 }
 
+sla2_status sla2_quantize(const sla2_fwd_params* p, const void* q, const void* k, const void* v, int8_t* q_codes,
+                          float* q_scales, int8_t* k_codes, float* k_scales, int8_t* v_codes, float* v_scales,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if (p->dtype != SLA2_BF16 || p->quant != SLA2_QUANT_INT8)
+        return fail(SLA2_CONTRACT_ERROR, "sla2_quantize: the INT8 QAT path (dtype bf16, quant int8)");
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!q || !k || !v || !q_codes || !q_scales || !k_codes || !k_scales || !v_codes || !v_scales)
+        return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
+    Workspace w;
+    carve(g, workspace, &w);
+    cudaStream_t st = (cudaStream_t)stream;
+    CUtensorMap mcol;
+    if (p->smooth)  // K~ = K - mu with the reference's serial mean (quant.hpp:88-96)
+        SLA2_CUDA_TRY(launch_colmean(k, colmean_map(&mcol, k, true, g.BH, g.N, g.d), true, w.mu, (int)g.BH, (int)g.N,
+                                     (int)g.d, st, &g_launches));
+    QuantLaunch qa{};
+    qa.B = g.B;
+    qa.H = g.H;
+    qa.N = (int)g.N;
+    qa.d = (int)g.d;
+    qa.bq = (int)g.bq;
+    qa.bk = (int)g.bk;
+    qa.tm = (int)g.tm;
+    qa.tn = (int)g.tn;
+    qa.q = q;
+    qa.k = k;
+    qa.v = v;
+    qa.mu = w.mu;
+    qa.smooth = p->smooth;
+    qa.qc = q_codes;
+    qa.qs = q_scales;
+    qa.kc = k_codes;
+    qa.ks = k_scales;
+    qa.vct = v_codes;
+    qa.vs = v_scales;
+    SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+    return SLA2_OK;
+}
+
 sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* mask_out, int32_t* kv_idx_out,
                            void* stream) {
     g_launches = 0;
@@ -801,6 +867,7 @@ sla2_status sla2_sparse_fwd(const sla2_fwd_params* p, const void* q, const void*
     if ((s = check_device()) != SLA2_OK) return s;
     const Geo g = geometry(p);
     if (!q || !k || !v || !rho || !mask || !out) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    if ((s = check_saved(p, saved)) != SLA2_OK) return s;
     if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
         return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
     Workspace w;

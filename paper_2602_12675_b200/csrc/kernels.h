@@ -88,6 +88,9 @@ cudaError_t launch_kpool(const LinearLaunch& a, float* kbar, cudaStream_t st, in
 cudaError_t launch_kphi(const LinearLaunch& a, cudaStream_t st, int* launches);
 // phi(Q) rows (bf16, d = 128) for the sparse kernel's linear-branch MMA: [rows][128] -> [rows][128]
 cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches);
+// exact fp32 row softmax over d (SLA2ForwardSaved q_phi / k_phi; mu non-null: of K - mu)
+cudaError_t launch_phi_exact(const void* x, bool bf16, const float* mu, float* out, int64_t rows, int N, int d,
+                             cudaStream_t st, int* launches);
 
 // ---- sparse / dense attention (sparse_bf16.cu, sparse_f32.cu)
 struct SparseLaunch {
@@ -108,6 +111,9 @@ struct SparseLaunch {
     float* o_s;
     float* o_l;
     float* big_l;
+    float* h_blocks;  // [BH][tm][d][d] complement H_i = sum of unselected h_j (saved path), or null
+    float* z_blocks;  // [BH][tm][d] complement Z_i, or null
+    float* s_first;   // QAT only: [BH][tm][bq][bk] S of each query block's first kept key block, or null
     // bf16 path
     const CUtensorMap* tm_q;
     const CUtensorMap* tm_k;
@@ -139,7 +145,7 @@ struct QuantLaunch {
     float* qs;      // [BH][tm]
     int8_t* kc;     // [BH][N][d] K~ codes per key block
     float* ks;      // [BH][tn]
-    int8_t* vct;    // [BH][tn][d][bk] V codes per key block, transposed (d-major)
+    int8_t* vct;    // [BH][N][d] V codes per key block (row-major, the PV MMA's MN-major B tile)
     float* vs;      // [BH][tn]
 };
 cudaError_t launch_quant_prep(const QuantLaunch& a, cudaStream_t st, int* launches);
@@ -153,7 +159,7 @@ struct SparseI8Launch {
     const float* vs;
     const CUtensorMap* tm_qc;   // [BH*N][d] int8, box 128x128
     const CUtensorMap* tm_kc;   // [BH*N][d] int8, box 128(x) x 64(y)
-    const CUtensorMap* tm_vct;  // [BH*tn*d][bk] int8, box 64 x 128
+    const CUtensorMap* tm_vct;  // [BH*N][d] int8, box 128 x 64
 };
 cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* launches);
 

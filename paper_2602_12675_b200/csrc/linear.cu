@@ -20,6 +20,7 @@
 
 #include <cstdint>
 
+#include "expf_glibc.cuh"
 #include "kernels.h"
 #include "tc.cuh"
 
@@ -144,6 +145,53 @@ __global__ void __launch_bounds__(256) phiq_kernel(const __nv_bfloat16* __restri
 
 cudaError_t launch_phiq(const void* q, void* phiq, int64_t rows, cudaStream_t st, int* launches) {
     phiq_kernel<<<(unsigned)((rows + 15) / 16), 256, 0, st>>>((const __nv_bfloat16*)q, (__nv_bfloat16*)phiq, rows);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// phi = row_softmax over the d features in the reference's exact arithmetic (matrix.hpp:138-155):
+// max, e_j = expf(x_j - max) (the glibc port), a serial sum in j order, inv = 1 / sum, e_j * inv;
+// x = Q (mu null) or K~ = K - mu (fp32 subtraction, quant.hpp:88-96). For SLA2ForwardSaved's
+// q_phi / k_phi (attention.hpp:456-457): one warp per row, fp32 out [rows][d], d <= 128.
+template <typename InT>
+__global__ void __launch_bounds__(256) phi_exact_kernel(const InT* __restrict__ x, const float* __restrict__ mu,
+                                                        float* __restrict__ out, int64_t rows, int N, int d) {
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t bh = row / N;
+    float v[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int f = lane + 32 * u;
+        float a = -INFINITY;
+        if (f < d) {
+            a = (float)x[row * d + f];
+            if (mu) a = __fsub_rn(a, mu[bh * d + f]);
+            mx = fmaxf(mx, a);
+        }
+        v[u] = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (lane + 32 * u < d) ? expf_glibc(__fsub_rn(v[u], mx)) : 0.0f;
+    float sum = 0.0f;  // serial, j ascending (every lane runs the same chain)
+    for (int f = 0; f < d; ++f) sum = __fadd_rn(sum, __shfl_sync(0xffffffffu, v[f >> 5], f & 31));
+    const float inv = __fdiv_rn(1.0f, sum);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < d) out[row * d + lane + 32 * u] = __fmul_rn(v[u], inv);
+}
+
+cudaError_t launch_phi_exact(const void* x, bool bf16, const float* mu, float* out, int64_t rows, int N, int d,
+                             cudaStream_t st, int* launches) {
+    const unsigned grid = (unsigned)((rows + 7) / 8);
+    if (bf16)
+        phi_exact_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, mu, out, rows, N, d);
+    else
+        phi_exact_kernel<float><<<grid, 256, 0, st>>>((const float*)x, mu, out, rows, N, d);
     ++*launches;
     return cudaGetLastError();
 }

@@ -130,6 +130,10 @@ struct SparseI8Params {
     float* o_s;
     float* o_l;
     float* big_l;
+    float* h_blocks;
+    float* z_blocks;
+    float* s_first;
+    const float* htot32;
     int N, H, tm, tn;
     float inv_sqrt_d;
 };
@@ -318,6 +322,9 @@ __global__ void __launch_bounds__(256, 1)
             sZc[lane * 4 + 2] = zt.z - acc.z;
             sZc[lane * 4 + 3] = zt.w - acc.w;
             __syncwarp();
+            if (p.z_blocks)
+                *reinterpret_cast<float4*>(p.z_blocks + (bh * p.tm + i) * D + lane * 4) =
+                    make_float4(sZc[lane * 4], sZc[lane * 4 + 1], sZc[lane * 4 + 2], sZc[lane * 4 + 3]);
             mbar_wait(&bar_q, 0);
             __syncwarp();
             const uint32_t qb = smem_u32(sQ);
@@ -426,6 +433,10 @@ __global__ void __launch_bounds__(256, 1)
                 s[t] = __fmul_rn(__fmul_rn((float)(int)sr[t], sqk), p.inv_sqrt_d);  // attention.hpp:381
                 mx = fmaxf(mx, s[t]);
             }
+            if (p.s_first && j == 0) {  // parity hook: S of the first kept block, as the reference forms it
+                float* sd = p.s_first + ((bh * p.tm + i) * BQ + r) * BK;
+                for (int t = 0; t < 64; ++t) sd[t] = s[t];
+            }
             const float m_new = fmaxf(m, mx);
             const float corr = fexp2((m - m_new) * 1.4426950408889634f);  // 0 on the first block
             const float mnl = m_new * 1.4426950408889634f;
@@ -495,6 +506,11 @@ __global__ void __launch_bounds__(256, 1)
                 uint32_t hs[32];
                 tmem_ld32(tmem + lane_base + TM_H + c0, hs);
                 tmem_ld_wait();
+                if (p.h_blocks) {  // SLA2ForwardSaved h_blocks: fp32 Htot - Hsel, row f = r
+                    const float* ht = p.htot32 + bh * D * D + r * D + c0;
+                    float* hb_out = p.h_blocks + ((bh * p.tm + i) * D + r) * D + c0;
+                    for (int c = 0; c < 32; ++c) hb_out[c] = ht[c] - __uint_as_float(hs[c]);
+                }
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch) {
                     const int c = c0 + ch * 8;
@@ -518,6 +534,12 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&bar_lin_done, 0);
             __syncwarp();
             tc_fence_after();
+        }
+        if (!linear && p.h_blocks) {  // full row: empty complement
+            float* hb_out = p.h_blocks + ((bh * p.tm + i) * D + r) * D;
+            for (int c = 0; c < D; ++c) hb_out[c] = 0.0f;
+            if (r < 32) p.z_blocks[(bh * p.tm + i) * D + r * 4 + 0] = 0.0f, p.z_blocks[(bh * p.tm + i) * D + r * 4 + 1] = 0.0f,
+                        p.z_blocks[(bh * p.tm + i) * D + r * 4 + 2] = 0.0f, p.z_blocks[(bh * p.tm + i) * D + r * 4 + 3] = 0.0f;
         }
         const float inv_l = __fdiv_rn(1.0f, l);
         const float inv_den = 1.0f / den;
@@ -575,6 +597,10 @@ cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* laun
     p.o_s = a.s.o_s;
     p.o_l = a.s.o_l;
     p.big_l = a.s.big_l;
+    p.h_blocks = a.s.h_blocks;
+    p.z_blocks = a.s.z_blocks;
+    p.s_first = a.s.s_first;
+    p.htot32 = a.s.htot;
     p.N = a.s.N;
     p.H = (int)a.s.H;
     p.tm = a.s.tm;

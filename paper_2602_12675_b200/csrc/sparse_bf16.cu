@@ -76,6 +76,9 @@ struct SparseBf16Params {
     float* o_s;
     float* o_l;
     float* big_l;
+    float* h_blocks;
+    float* z_blocks;
+    const float* htot32;
     int N, H, tm, tn;
     int last_valid;  // keys in the last key block (BK unless N % BK != 0)
     float scale_log2;
@@ -418,6 +421,11 @@ __global__ void __launch_bounds__(256, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_zc);
         }
+        if (p.z_blocks) {  // SLA2ForwardSaved z_blocks (zero on full rows)
+            const float4 z = linear ? make_float4(sZc[lane * 4], sZc[lane * 4 + 1], sZc[lane * 4 + 2], sZc[lane * 4 + 3])
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(p.z_blocks + (bh * p.tm + i) * D + lane * 4) = z;
+        }
     } else if (warp >= 4) {
         // ===================== softmax / correction / epilogue =====================
         const int r = threadIdx.x - 128;  // query row within the block
@@ -570,6 +578,11 @@ __global__ void __launch_bounds__(256, 1)
             tmem_ld32(tmem + lane_base + TM_H + c0, *reinterpret_cast<uint32_t(*)[32]>(&hs[0]));
             tmem_ld32(tmem + lane_base + TM_H + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&hs[32]));
             tmem_ld_wait();
+            if (p.h_blocks) {  // SLA2ForwardSaved h_blocks: fp32 Htot - Hsel, row f = r
+                const float* ht = p.htot32 + bh * D * D + r * D + c0;
+                float* hb_out = p.h_blocks + ((bh * p.tm + i) * D + r) * D + c0;
+                for (int c = 0; c < 64; ++c) hb_out[c] = ht[c] - __uint_as_float(hs[c]);
+            }
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {
                 const uint32_t off = (c0 >> 6) * 16384 + sw128_off(r, ch * 8);
@@ -585,6 +598,10 @@ __global__ void __launch_bounds__(256, 1)
             }
             fence_proxy_async_smem();
             tc_fence_before();
+        }
+        if (!linear && p.h_blocks) {  // full row: the complement is empty (attention.hpp:495)
+            float* hb_out = p.h_blocks + ((bh * p.tm + i) * D + r) * D + c0;
+            for (int c = 0; c < 64; ++c) hb_out[c] = 0.0f;
         }
         mbar_arrive(&bar_lin_ready);  // also publishes sInvL (written by the softmax warps)
         mbar_wait(&bar_lin_ready, 0);
@@ -683,6 +700,9 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
     p.o_s = a.o_s;
     p.o_l = a.o_l;
     p.big_l = a.big_l;
+    p.h_blocks = a.dense ? nullptr : a.h_blocks;
+    p.z_blocks = a.dense ? nullptr : a.z_blocks;
+    p.htot32 = a.htot;
     p.N = a.N;
     p.H = (int)a.H;
     p.tm = a.tm;

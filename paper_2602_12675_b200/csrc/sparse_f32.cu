@@ -147,6 +147,12 @@ __global__ void __launch_bounds__(256) sla2_sparse_f32_kernel(SparseLaunch a) {
             sZc[f] = a.ztot[bh * d + f] - sel;
         }
     }
+    if (a.h_blocks) {  // SLA2ForwardSaved h_blocks / z_blocks (zero on full rows, attention.hpp:495)
+        __syncthreads();
+        const int64_t tile = bh * a.tm + i;
+        for (int e = tid; e < dd; e += 256) a.h_blocks[tile * dd + e] = full_row ? 0.0f : sHc[e];
+        for (int f = tid; f < d; f += 256) a.z_blocks[tile * d + f] = full_row ? 0.0f : sZc[f];
+    }
     __syncthreads();
     const int64_t grow = qrow0 + r;
     const float inv_l = 1.0f / l;

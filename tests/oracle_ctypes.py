@@ -78,6 +78,9 @@ class Oracle:
                           C.c_int)
                 self._sig(f"soft_topk_backward_{s}", [fp, _sz, _sz, C.c_double, C.c_float if s == "f" else C.c_double,
                                                       fp, fp], C.c_int)
+                self._sig(f"forward_saved_{s}", [fp, fp, fp, _sz, _sz, _sz, _sz, _u8p, fp, C.c_int, C.c_int, fp, fp,
+                                                 fp, fp, fp, fp, fp, fp], C.c_int)
+                self._sig(f"block_scores_qk_{s}", [fp, fp, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int, fp], C.c_int)
                 self._sig(f"rten_save_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
                 self._sig(f"rten_load_{s}", [C.c_char_p, _sz, _sz, fp], C.c_int)
         if prefix == "sla2o_":
@@ -162,6 +165,32 @@ class Oracle:
         _check(rc)
         return out, o_s, o_l, big_l
 
+    def forward_saved(self, q, k, v, bq, bk, mask, rho, quant=False, smooth=True):
+        """sla2_forward_blockwise with the whole SLA2ForwardSaved (reference only): dict of out,
+        o_s, o_l, big_l, h_blocks [tm,d,d], z_blocks [tm,d], q_phi, k_phi."""
+        n, d = q.shape
+        dt = q.dtype
+        tm = n // bq
+        r = {"out": np.empty((n, d), dt), "o_s": np.empty((n, d), dt), "o_l": np.empty((n, d), dt),
+             "big_l": np.empty(n, dt), "h_blocks": np.empty((tm, d, d), dt), "z_blocks": np.empty((tm, d), dt),
+             "q_phi": np.empty((n, d), dt), "k_phi": np.empty((n, d), dt)}
+        rc = getattr(self, "_forward_saved_" + self._sfx(dt))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v), n, d, bq, bk,
+            np.ascontiguousarray(mask, dtype=np.uint8), np.ascontiguousarray(rho, dtype=dt), int(quant), int(smooth),
+            r["out"], r["o_s"], r["o_l"], r["big_l"], r["h_blocks"], r["z_blocks"], r["q_phi"], r["k_phi"])
+        _check(rc)
+        return r
+
+    def block_scores_qk(self, q, k, qi0, bq, kj0, bk, quant=False):
+        """detail::block_scores_qk (attention.hpp:372-394) of one block pair (reference only); k is
+        the (smoothed) K~ the forward passes."""
+        n, d = q.shape
+        s = np.empty((bq, bk), q.dtype)
+        rc = getattr(self, "_block_scores_qk_" + self._sfx(q.dtype))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), n, d, qi0, bq, kj0, bk, int(quant), s)
+        _check(rc)
+        return s
+
     def forward_naive(self, q, k, v, bq, bk, mask, rho, smooth=True):
         n, d = q.shape
         dt = q.dtype
@@ -192,6 +221,19 @@ class Oracle:
         _check(rc)
         return out, mask, o_s, o_l, big_l
 
+
+    def block_scores_ragged(self, q, k, proj_q, proj_k, bq, bk, tau=0.1):
+        """Ragged extension of block_scores (C port only): partial last blocks pooled over their
+        own rows."""
+        n, d = q.shape
+        dt = q.dtype
+        pc = np.empty((-(-n // bq), -(-n // bk)), dtype=dt)
+        rc = getattr(self, "_block_scores_ragged_" + self._sfx(dt))(
+            np.ascontiguousarray(q), np.ascontiguousarray(k), n, d,
+            np.ascontiguousarray(proj_q, dtype=dt), np.ascontiguousarray(proj_k, dtype=dt),
+            tau, bq, bk, pc)
+        _check(rc)
+        return pc
 
     def attention_ragged(self, q, k, v, bq, bk, proj_q, proj_k, rho, k_percent, quant=False, smooth=True):
         """Ragged extension of attention(): n need not be divisible by bq / bk (C port only)."""

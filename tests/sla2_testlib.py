@@ -50,6 +50,34 @@ def oracle_router_head(q, k, pq, pk, bq, bk, k_percent, smooth=True, which="port
     return pc, mask, kappa
 
 
+def oracle_router_any(q, k, pq, pk, bq, bk, k_percent, smooth=True):
+    """Router for one (b, h) at any N: the unmodified reference (oracle/_ref) when N divides into
+    blocks and it was built here, else the C port's ragged extension (pinned to the reference on
+    divisible N, tests/test_ragged.py). Returns (pc, mask, kappa, which)."""
+    n = q.shape[0]
+    r = oc.ref()
+    if n % bq == 0 and n % bk == 0 and r is not None:
+        kt = r.smooth_k(k)[0] if smooth else k
+        pc = r.block_scores(q, kt, pq, pk, bq, bk)
+        mask, kappa = r.hard_topk(pc, k_percent)
+        return pc, mask, kappa, "reference"
+    o = oc.port()
+    kt = o.smooth_k(k)[0] if smooth else k
+    pc = o.block_scores_ragged(q, kt, pq, pk, bq, bk) if (n % bq or n % bk) else o.block_scores(q, kt, pq, pk, bq, bk)
+    mask, kappa = o.hard_topk(pc, k_percent)
+    return pc, mask, kappa, "port"
+
+
+def oracle_attention_any(q, k, v, pq, pk, rho, bq, bk, k_percent, quant=False):
+    """Tape::sla2_attention forward for one (b, h) at any N: the reference when N divides (and it
+    was built here), else the port's ragged extension. Returns (out, mask, o_s, o_l, L, which)."""
+    n = q.shape[0]
+    r = oc.ref()
+    if n % bq == 0 and n % bk == 0 and r is not None:
+        return (*r.attention(q, k, v, bq, bk, pq, pk, rho, k_percent, quant=quant), "reference")
+    return (*oc.port().attention_ragged(q, k, v, bq, bk, pq, pk, rho, k_percent, quant=quant), "port")
+
+
 def mask_to_idx(mask):
     return [np.nonzero(row)[0].astype(np.int32) for row in mask]
 
