@@ -24,7 +24,7 @@ TOL = 1e-2
 def _threads():
     n = os.cpu_count() or 1
     os.environ.setdefault("SLA2_THREADS", str(n))  # the reference reads it once (common.hpp:31-43)
-    oc.port().set_threads(n)
+    oc.port()._set_threads(n)
 
 
 def _inputs(B, H, N, seed):

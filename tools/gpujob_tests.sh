@@ -2,6 +2,6 @@
 # GPU test job: the whole -m gpu suite with per-test durations (analysis helper)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout ${T:-1500} python -m pytest tests -m gpu -q -x --durations=25 ${ARGS} > gpurun_out/gputests.log 2>&1
+timeout ${T:-1500} python -m pytest ${ARGS:-tests} -m gpu -q -x --durations=25 > gpurun_out/gputests.log 2>&1
 echo "rc=$?" >> gpurun_out/gputests.log
 tail -40 gpurun_out/gputests.log
