@@ -11,8 +11,16 @@
 #include <string>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "../../oracle/sla2_oracle.h"
 #include "sla2_b200/sla2.hpp"
+#ifdef SLA2_B200_MODE_REFERENCE
+// built on the reference's own types (oracle/Makefile `dropin`): its RTEN1 I/O and the
+// drop-in's composition helper
+#include "sla2/tensor_io.hpp"
+using sla2::b200::sla2_attention;
+#endif
 
 using namespace sla2;
 
