@@ -133,6 +133,21 @@ sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* m
                            int32_t* kv_idx_out, void* stream);
 
 /*
+ * The linear branch's key-side precompute (attention.hpp:456-475): K~ = K - colmean(K) (p->smooth),
+ * phi(K~) = row_softmax(K~) and, per key block j, z_j = colsum phi(K~_j), with the head totals
+ * H = sum_j phi(K~_j)^T V_j (d x d) and Z = sum_j z_j that the forward's complements are formed
+ * from ("total minus selected", attention.hpp:495-502). Outputs (device, fp32, each nullable):
+ * k_phi_out [B,H,N,d] (exact row softmax), z_blocks_out [B,H,tn,d], h_total_out [B,H,d,d],
+ * z_total_out [B,H,d]. On the bf16 path z_j and H are accumulated from the bf16-rounded phi(K~)
+ * the sparse kernel reads (tolerance-level). The per-key-block h_j matrices are not
+ * materialized (the forward needs only H and the selected sums). Workspace:
+ * sla2_workspace_size(p).
+ */
+sla2_status sla2_linear_precompute(const sla2_fwd_params* p, const void* k, const void* v, float* k_phi_out,
+                                   float* z_blocks_out, float* h_total_out, float* z_total_out, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
+/*
  * The QAT operand quantization (quantize, quant.hpp:31-50, on the blocks block_scores_qk and
  * block_product_pv quantize, attention.hpp:379-380,401): per query block Q_i (bq x d), per key
  * block K~_j = K_j - colmean(K) (bk x d, when p->smooth) and V_j (bk x d), the absmax/127 scale

@@ -27,7 +27,7 @@ from typing import Optional
 
 __all__ = [
     "ShapeError", "NumericError", "ContractError", "CudaError", "Sla2Error",
-    "lib", "library_path", "topk_budget", "smooth_k", "quantize", "block_scores", "hard_topk",
+    "lib", "library_path", "topk_budget", "smooth_k", "quantize", "linear_precompute", "block_scores", "hard_topk",
     "sla2_forward_blockwise", "sla2_attention", "full_attention", "router", "forward",
     "FwdParams", "workspace_bytes", "last_launch_count",
 ]
@@ -114,6 +114,7 @@ def lib():
         "sla2_smooth_k": ([P, vp, vp, vp, vp], C.c_int),
         "sla2_hard_topk": ([P, vp, vp, vp, vp], C.c_int),
         "sla2_quantize": ([P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
+        "sla2_linear_precompute": ([P, vp, vp, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_sparse_fwd": ([P, vp, vp, vp, vp, vp, vp, C.POINTER(_Saved), vp, sz, vp], C.c_int),
         "sla2_dense_fwd": ([P, vp, vp, vp, vp, vp, sz, vp], C.c_int),
         "sla2_forward_host": ([P, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
@@ -380,6 +381,26 @@ def quantize(q, k, v, *, bq=128, bk=64, smooth=True):
     _raise(lib().sla2_quantize(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(res["q_codes"]), _ptr(res["q_scales"]),
                                _ptr(res["k_codes"]), _ptr(res["k_scales"]), _ptr(res["v_codes"]),
                                _ptr(res["v_scales"]), _ptr(ws), ws.numel(), _stream(dev)))
+    return res
+
+
+def linear_precompute(k, v, *, bq=128, bk=64, smooth=True):
+    """The linear branch's key-side precompute (attention.hpp:456-475) on device: returns
+    {"k_phi" [B,H,N,d] (exact row softmax of K~), "z_blocks" [B,H,tn,d] (z_j per key block),
+    "h_total" [B,H,d,d] (sum_j phi(K~_j)^T V_j), "z_total" [B,H,d]}, fp32."""
+    import torch
+    _check_like(k, v)
+    p = _params_from(k, bq, bk, 3.0, False, smooth, True)
+    cp = p.c()
+    _raise(lib().sla2_check_params(C.byref(cp)))
+    dev = k.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    res = {"k_phi": torch.empty(k.shape, **f32), "z_blocks": torch.empty((p.B, p.H, p.tn, p.d), **f32),
+           "h_total": torch.empty((p.B, p.H, p.d, p.d), **f32), "z_total": torch.empty((p.B, p.H, p.d), **f32)}
+    ws = _workspace(p, dev)
+    _raise(lib().sla2_linear_precompute(C.byref(cp), _ptr(k), _ptr(v), _ptr(res["k_phi"]), _ptr(res["z_blocks"]),
+                                        _ptr(res["h_total"]), _ptr(res["z_total"]), _ptr(ws), ws.numel(),
+                                        _stream(dev)))
     return res
 
 

@@ -839,6 +839,62 @@ sla2_status sla2_quantize(const sla2_fwd_params* p, const void* q, const void* k
     return SLA2_OK;
 }
 
+sla2_status sla2_linear_precompute(const sla2_fwd_params* p, const void* k, const void* v, float* k_phi_out,
+                                   float* z_blocks_out, float* h_total_out, float* z_total_out, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+    g_launches = 0;
+    sla2_status s = sla2_check_params(p);
+    if (s != SLA2_OK) return s;
+    if ((s = check_device()) != SLA2_OK) return s;
+    if (!k || !v) return fail(SLA2_CONTRACT_ERROR, "NULL pointer");
+    const Geo g = geometry(p);
+    if (workspace_bytes < carve(g, nullptr, nullptr) || !workspace)
+        return fail(SLA2_CONTRACT_ERROR, "workspace too small (see sla2_workspace_size)");
+    Workspace w;
+    carve(g, workspace, &w);
+    cudaStream_t st = (cudaStream_t)stream;
+    CUtensorMap mcol, mk, mv, mphi;
+    if (p->smooth)  // the exact serial mean (quant.hpp:88-96), as the forward uses
+        SLA2_CUDA_TRY(launch_colmean(k, colmean_map(&mcol, k, g.bf16, g.BH, g.N, g.d), g.bf16, w.mu, (int)g.BH,
+                                     (int)g.N, (int)g.d, st, &g_launches));
+    LinearLaunch la{};
+    la.k = k;
+    la.v = v;
+    la.bf16 = g.bf16;
+    la.BH = g.BH;
+    la.N = (int)g.N;
+    la.d = (int)g.d;
+    la.bk = (int)g.bk;
+    la.mu = p->smooth ? w.mu : nullptr;
+    la.phik = w.phik;
+    la.zblk = w.zblk;
+    la.ztot = w.ztot;
+    la.hpart = w.hpart;
+    la.htot = w.htot;
+    la.htot16 = w.htot16;
+    la.nchunk = g.nchunk;
+    if (g.bf16) {
+        const uint64_t BH = (uint64_t)g.BH, N = (uint64_t)g.N;
+        if (!make_map3(&mk, k, BH, N, g.d, 64, 64, 2) || !make_map3(&mv, v, BH, N, g.d, 64, 64, 2) ||
+            !make_map3(&mphi, w.phik, BH, N, g.d, 64, 64, 2))
+            return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (pointers must be 16-byte aligned)");
+        la.tm_k = &mk;
+        la.tm_v = &mv;
+        la.tm_phik = &mphi;
+    }
+    SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+    const size_t dd = (size_t)(g.d * g.d) * 4;
+    if (z_blocks_out)
+        SLA2_CUDA_TRY(cudaMemcpyAsync(z_blocks_out, w.zblk, (size_t)(g.BH * g.tn * g.d) * 4, cudaMemcpyDeviceToDevice, st));
+    if (h_total_out) SLA2_CUDA_TRY(cudaMemcpyAsync(h_total_out, w.htot, (size_t)g.BH * dd, cudaMemcpyDeviceToDevice, st));
+    if (z_total_out)
+        SLA2_CUDA_TRY(cudaMemcpyAsync(z_total_out, w.ztot, (size_t)(g.BH * g.d) * 4, cudaMemcpyDeviceToDevice, st));
+    if (k_phi_out)
+        SLA2_CUDA_TRY(launch_phi_exact(k, g.bf16, p->smooth ? w.mu : nullptr, k_phi_out, g.BH * g.N, (int)g.N, (int)g.d,
+                                       st, &g_launches));
+    return SLA2_OK;
+}
+
 sla2_status sla2_hard_topk(const sla2_fwd_params* p, const float* pc, uint8_t* mask_out, int32_t* kv_idx_out,
                            void* stream) {
     g_launches = 0;

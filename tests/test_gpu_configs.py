@@ -197,3 +197,29 @@ def test_saved_state_vs_reference(cuda, case):
     for n in ("o_s", "o_l"):
         assert rel_err(got[n], ref[n])[0] <= (tol if case != "f32" else 1e-4), n
     np.testing.assert_allclose(got["big_l"], ref["big_l"], atol=2e-2 if case != "f32" else 1e-4, rtol=2e-3)
+
+
+@pytest.mark.skipif(oc.ref() is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", ["bf16", "f32"])
+def test_linear_precompute_vs_reference(cuda, case):
+    """sla2_linear_precompute (attention.hpp:456-475): phi(K~) bit-exact with the reference's
+    k_phi; z_j per key block and the totals H = sum_j phi(K~_j)^T V_j, Z = sum_j z_j against the
+    reference's phi(K~) and V (float64 sums) within the branch tolerance."""
+    import torch
+    r = oc.ref()
+    if case == "f32":
+        N, d, bq, bk, dt, tol = 1024, 64, 64, 64, torch.float32, 1e-5
+        q, k, v, pq, pk, rho = make_inputs(1, 1, N, d, 110, bf16=False, bq=bq, bk=bk)
+    else:
+        N, d, bq, bk, dt, tol = 4096, 128, 128, 64, torch.bfloat16, TOL
+        q, k, v, pq, pk, rho = make_inputs(1, 1, N, d, 111, bq=bq, bk=bk)
+    res = sla2.linear_precompute(to_dev(k, dt, cuda), to_dev(v, dt, cuda), bq=bq, bk=bk)
+    got = {n: t[0, 0].cpu().numpy() for n, t in res.items()}
+    mask = np.ones((N // bq, N // bk), np.uint8)
+    ref = r.forward_saved(q[0, 0], k[0, 0], v[0, 0], bq, bk, mask, rho[0])
+    assert np.array_equal(got["k_phi"].view(np.uint32), ref["k_phi"].view(np.uint32))
+    kphi = ref["k_phi"].astype(np.float64)
+    zb = kphi.reshape(N // bk, bk, d).sum(axis=1)
+    assert rel_err(got["z_blocks"], zb)[0] <= tol
+    assert rel_err(got["z_total"], zb.sum(axis=0))[0] <= tol
+    assert rel_err(got["h_total"], kphi.T @ v[0, 0].astype(np.float64))[0] <= tol
