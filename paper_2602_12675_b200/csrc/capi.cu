@@ -636,6 +636,8 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             ia.tm_kc = &mkc;
             ia.tm_vct = &mvc;
             SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
+        } else if (sparse_v2_eligible(sa)) {
+            SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
         } else {
             SLA2_CUDA_TRY(launch_sparse_bf16(sa, st, &g_launches));
         }

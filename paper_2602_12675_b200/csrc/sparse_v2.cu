@@ -1,0 +1,645 @@
+// sparse_v2.cu -- the persistent SLA2 sparse + linear + alpha-blend forward (sm_100a, bf16).
+//
+// Same algorithm as sparse_bf16.cu (the per-query-block loop of sla2_forward_blockwise,
+// attention.hpp:484-558, with block_scores_qk / block_product_pv, 372-415), restructured so
+// that one query block's epilogue and the next one's prologue run UNDER the neighbouring
+// key-block loops instead of between them:
+//
+//  * persistent CTAs (one per SM) walk the (b, h, query block) tiles round robin;
+//  * three warpgroups: WG0 = TMA producers (Q / K pairs / phi(Q); V / phi(K~) ring), the MMA
+//    issuer and the Zc warp; WG1 = softmax (thread per query row) of tile k; WG2 = epilogue
+//    (thread per row) of tile k-1, concurrently; setmaxnreg moves registers to WG1/WG2;
+//  * two Q buffers: Q of tile k+1 arrives while tile k runs; the buffer then takes phi(Q) and
+//    finally the bf16 output block for the TMA store;
+//  * the linear branch lands in the sparse accumulator: with c_r = (1 - a) l_r / (a den_r),
+//        out = a / l (O + (c phi(Q)) (Htot - Hsel))
+//    so the epilogue scales the phi(Q) rows by c, one MMA accumulates (c phi(Q)) Hc into O, and
+//    O is read from TMEM once (attention.hpp:532-557: O_s = O / l, O_l = phi(Q) Hc / den,
+//    out = a O_s + (1 - a) O_l);
+//  * TMEM (512 columns): S 128 | P 2 x 64 | O 128 | Hsel 128. The epilogue of tile k reads
+//    Hsel (then frees it for tile k+1's first phi(K~)^T V) and O (then frees it for tile k+1's
+//    first PV); tile k+1's first Q K^T and softmax run meanwhile.
+//
+// Key blocks are processed in pairs (S = Q [K_2p; K_2p+1]^T, M128 N128 K128) exactly as in
+// sparse_bf16.cu; see the comments there for the per-pair pipeline. The saved-state outputs
+// (O_s, O_l, L, H_i, Z_i) and the dense mode stay on sparse_bf16.cu.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "expf_glibc.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace sla2dev {
+
+namespace v2 {
+constexpr int BQ = 128, BK = 64, D = 128;
+constexpr int NKP = 2, NSV = 3;                // K pair ring, V / phi(K~) ring (one slot per tile holds Hc)
+constexpr uint32_t Q_BYTES = BQ * D * 2;       // 32 KB
+constexpr uint32_t TILE_BYTES = BK * D * 2;    // 16 KB
+constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // a K pair
+constexpr uint32_t VS_BYTES = 2 * TILE_BYTES;  // V + phi(K~), or Hc (bf16 128 x 128)
+constexpr uint32_t OFF_Q = 0;                  // 2 Q buffers
+constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr uint32_t OFF_V = OFF_K + NKP * KP_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_V + NSV * VS_BYTES;  // 224 KB
+constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 256, TM_H = 384;
+constexpr float RESCALE_LOG2 = 8.0f;
+constexpr int NTHREADS = 384;
+}  // namespace v2
+
+struct SparseV2Params {
+    const int32_t* kv_idx;
+    const int32_t* kv_cnt;
+    int kstride, kappa;
+    const float* rho;
+    const float* ztot;
+    const float* zblk;
+    const float* htot32;  // [BH][D][D] fp32 (the epilogue forms Hc = Htot - Hsel from it)
+    int N, H, tm, tn, ntiles;
+    int last_valid;
+    float scale_log2;
+};
+
+__device__ __forceinline__ float v2_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+template <uint32_t N>
+__device__ __forceinline__ void reg_alloc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void reg_dealloc() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+
+// Everything about tile t every role needs (all roles walk the same tile sequence).
+struct V2Tile {
+    int64_t bh;
+    int i, nb, npair;
+    bool linear;
+    const int32_t* idx;
+};
+__device__ __forceinline__ V2Tile v2_tile(const SparseV2Params& p, int t) {
+    V2Tile r;
+    r.bh = t / p.tm;
+    r.i = t - (int)r.bh * p.tm;
+    r.nb = p.kv_cnt ? p.kv_cnt[r.bh * p.tm + r.i] : p.kappa;
+    r.npair = (r.nb + 1) >> 1;
+    r.linear = r.nb != p.tn;
+    r.idx = p.kv_idx + (r.bh * p.tm + r.i) * (int64_t)p.kstride;
+    return r;
+}
+
+__global__ void __launch_bounds__(384, 1)
+    sla2_sparse_v2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
+                          const __grid_constant__ CUtensorMap tmPq, const __grid_constant__ CUtensorMap tmO,
+                          const SparseV2Params p) {
+    using namespace v2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_q_full[2], bar_q_empty[2], bar_qk_done[2], bar_pq_full[2], bar_k_full[NKP],
+        bar_k_empty[NKP], bar_v_full[NSV], bar_v_empty[NSV], bar_s_full, bar_s_free, bar_p_full[2], bar_pv_done[2],
+        bar_tile_done, bar_sm_done[2], bar_h_free, bar_lin_ready, bar_lin_done, bar_o_free, bar_zc_ready[2],
+        bar_zc_free[2];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float sZc[2][D];
+    __shared__ float sL[2][BQ];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = p.ntiles, G = gridDim.x;
+    auto sQ = [&](int b) { return smem + OFF_Q + b * Q_BYTES; };
+    auto sKp = [&](int s) { return smem + OFF_K + s * KP_BYTES; };
+    auto sV = [&](int s) { return smem + OFF_V + s * VS_BYTES; };
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&bar_q_full[b], 1);
+            mbar_init(&bar_q_empty[b], 1);
+            mbar_init(&bar_qk_done[b], 1);
+            mbar_init(&bar_pq_full[b], 1);
+            mbar_init(&bar_p_full[b], 128);
+            mbar_init(&bar_pv_done[b], 1);
+            mbar_init(&bar_sm_done[b], 128);
+            mbar_init(&bar_zc_ready[b], 1);
+            mbar_init(&bar_zc_free[b], 128);
+        }
+        for (int s = 0; s < NKP; ++s) {
+            mbar_init(&bar_k_full[s], 1);
+            mbar_init(&bar_k_empty[s], 1);
+        }
+        for (int s = 0; s < NSV; ++s) {
+            mbar_init(&bar_v_full[s], 1);
+            mbar_init(&bar_v_empty[s], 1);
+        }
+        mbar_init(&bar_s_full, 1);
+        mbar_init(&bar_s_free, 128);
+        mbar_init(&bar_tile_done, 1);
+        mbar_init(&bar_h_free, 128);
+        mbar_init(&bar_lin_ready, 128);
+        mbar_init(&bar_lin_done, 1);
+        mbar_init(&bar_o_free, 128);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(&tmem_base_sh, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp < 4) {
+        reg_dealloc<64>();
+        if (warp == 0 && lane == 0) {
+            // ============ TMA producer: Q (two buffers), K pairs, phi(Q) over the tile's Q ============
+            tma_prefetch_desc(&tmQ);
+            tma_prefetch_desc(&tmK);
+            tma_prefetch_desc(&tmPq);
+            const uint64_t pol = policy_evict_last();
+            auto load_q = [&](const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int qrow, int hz) {
+                mbar_arrive_expect_tx(bar, Q_BYTES);
+                tma_load_3d(dst, map, 0, qrow, hz, bar);
+                tma_load_3d(dst + 8192, map, 0, qrow + 64, hz, bar);
+                tma_load_3d(dst + 16384, map, 64, qrow, hz, bar);
+                tma_load_3d(dst + 24576, map, 64, qrow + 64, hz, bar);
+            };
+            int64_t gk = 0;
+            int t = blockIdx.x;
+            if (t < nt) {
+                const V2Tile T0 = v2_tile(p, t);
+                load_q(&tmQ, &bar_q_full[0], sQ(0), T0.i * BQ, (int)T0.bh);
+            }
+            for (int k = 0; t < nt; ++k, t += G) {
+                const V2Tile T = v2_tile(p, t);
+                const int pb = k & 1;
+                for (int n = 0; n < T.npair; ++n, ++gk) {
+                    const int s = (int)(gk % NKP);
+                    if (gk >= NKP) mbar_wait(&bar_k_empty[s], (uint32_t)(((gk / NKP) - 1) & 1));
+                    const int cnt = min(2, T.nb - 2 * n);
+                    mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
+                    for (int b = 0; b < cnt; ++b) {
+                        const int krow = T.idx[2 * n + b] * BK;
+                        tma_load_3d_hint(sKp(s) + b * 8192, &tmK, 0, krow, (int)T.bh, &bar_k_full[s], pol);
+                        tma_load_3d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, (int)T.bh, &bar_k_full[s], pol);
+                    }
+                }
+                // Q of the next tile into the other buffer (free once tile k-1's output left it)
+                if (t + G < nt) {
+                    const V2Tile T1 = v2_tile(p, t + G);
+                    const int k1 = k + 1;
+                    if (k1 >= 2) mbar_wait(&bar_q_empty[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
+                    load_q(&tmQ, &bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
+                }
+                // phi(Q) of this tile over its Q once the last Q K^T has read Q
+                mbar_wait(&bar_qk_done[pb], (uint32_t)((k >> 1) & 1));
+                if (T.linear) load_q(&tmPq, &bar_pq_full[pb], sQ(pb), T.i * BQ, (int)T.bh);
+                else mbar_arrive(&bar_pq_full[pb]);
+            }
+        } else if (warp == 2 && lane == 0) {
+            // ============ TMA producer: V / phi(K~) ring; one slot per tile for the epilogue's Hc ============
+            tma_prefetch_desc(&tmV);
+            tma_prefetch_desc(&tmPhi);
+            const uint64_t pol = policy_evict_last();
+            int64_t gv = 0;
+            for (int t = blockIdx.x; t < nt; t += G) {
+                const V2Tile T = v2_tile(p, t);
+                for (int j = 0; j <= T.nb; ++j, ++gv) {
+                    const int s = (int)(gv % NSV);
+                    if (gv >= NSV) mbar_wait(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
+                    if (j == T.nb) {  // the Hc slot: allocated, not loaded
+                        mbar_arrive(&bar_v_full[s]);
+                        continue;
+                    }
+                    const int krow = T.idx[j] * BK, hz = (int)T.bh;
+                    mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
+                    tma_load_3d_hint(sV(s), &tmV, 0, krow, hz, &bar_v_full[s], pol);
+                    tma_load_3d_hint(sV(s) + 8192, &tmV, 64, krow, hz, &bar_v_full[s], pol);
+                    if (T.linear) {
+                        tma_load_3d_hint(sV(s) + TILE_BYTES, &tmPhi, 0, krow, hz, &bar_v_full[s], pol);
+                        tma_load_3d_hint(sV(s) + TILE_BYTES + 8192, &tmPhi, 64, krow, hz, &bar_v_full[s], pol);
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            // ============ MMA issuer (whole warp; elect.sync inside each tcgen05 op) ============
+            constexpr uint32_t ID_QK2 = idesc_bf16(128, 128, false, false);
+            constexpr uint32_t ID_QK1 = idesc_bf16(128, 64, false, false);
+            constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
+            constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
+            constexpr uint32_t ID_LIN = idesc_bf16(128, 128, false, true);
+            const uint32_t tm = warp_uniform(tmem);
+            const uint32_t sbase = warp_uniform(smem_u32(smem));
+            const uint64_t dK0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
+            const uint64_t dVm = sdesc_sw128(sbase + OFF_V, 8192, 1024);
+            int64_t g = 0, gv = 0;
+            int k = 0;
+            bool prev_linear = false;
+            int prev_hc = 0;
+            auto issue_qk = [&](int64_t gg, int pb, int nbu, int n) {
+                if (gg > 0) {
+                    mbar_wait(&bar_s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in registers
+                    tc_fence_after();
+                }
+                const int s = (int)(gg % NKP);
+                mbar_wait(&bar_k_full[s], (uint32_t)((gg / NKP) & 1));
+                tc_fence_after();
+                const uint32_t idq = (2 * n + 1 < nbu) ? ID_QK2 : ID_QK1;
+                const uint64_t dQ = sdesc_sw128(sbase + OFF_Q + pb * Q_BYTES, 16, 1024);
+                const uint64_t dK = dK0 + ((s * KP_BYTES) >> 4);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+                    umma_bf16_ss_w(tm + TM_S, dQ + off, dK + off, idq, ks > 0);
+                }
+                umma_commit_w(&bar_s_full);
+                umma_commit_w(&bar_k_empty[s]);
+            };
+            auto lin_mma = [&](int kk) {  // O += (c phi(Q)) Hc of tile kk (epilogue inputs ready)
+                mbar_wait(&bar_lin_ready, (uint32_t)(kk & 1));
+                tc_fence_after();
+                if (prev_linear) {
+                    const uint64_t dA = sdesc_sw128(sbase + OFF_Q + (kk & 1) * Q_BYTES, 16, 1024);
+                    const uint64_t dB = sdesc_sw128(sbase + OFF_V + prev_hc * VS_BYTES, 16384, 1024);
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+                        umma_bf16_ss_w(tm + TM_O, dA + off, dB + ((ks * 2048) >> 4), ID_LIN, 1);
+                    }
+                }
+                umma_commit_w(&bar_lin_done);
+            };
+            for (int t = blockIdx.x; t < nt; t += G, ++k) {
+                const V2Tile T = v2_tile(p, t);
+                const int nbu = (int)warp_uniform((uint32_t)T.nb);
+                const int npu = (nbu + 1) >> 1;
+                const bool lin = T.linear;
+                const int pb = k & 1;
+                mbar_wait(&bar_q_full[pb], (uint32_t)((k >> 1) & 1));
+                tc_fence_after();
+                issue_qk(g, pb, nbu, 0);
+                if (npu == 1) umma_commit_w(&bar_qk_done[pb]);
+                if (k > 0) lin_mma(k - 1);
+                for (int n = 0; n < npu; ++n) {
+                    const int64_t gg = g + n;
+                    if (n + 1 < npu) {
+                        issue_qk(gg + 1, pb, nbu, n + 1);
+                        if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
+                    }
+                    mbar_wait(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
+                    tc_fence_after();
+                    if (n == 0 && k > 0) {
+                        mbar_wait(&bar_o_free, (uint32_t)((k - 1) & 1));  // tile k-1's O left TMEM
+                        tc_fence_after();
+                    }
+                    const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
+                    for (int j = j0; j < j1; ++j) {
+                        const int64_t v = gv + j;
+                        const int sv = (int)(v % NSV);
+                        mbar_wait(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
+                        tc_fence_after();
+                        const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
+                        const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 32);
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
+                    }
+                    umma_commit_w(&bar_pv_done[gg & 1]);
+                    if (n == 0 && k > 0) {
+                        mbar_wait(&bar_h_free, (uint32_t)((k - 1) & 1));  // tile k-1's Hsel left TMEM
+                        tc_fence_after();
+                    }
+                    for (int j = j0; j < j1; ++j) {
+                        const int sv = (int)((gv + j) % NSV);
+                        if (lin) {
+                            const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
+                            const uint64_t dP = dV + (TILE_BYTES >> 4);
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
+                                               (j > 0 || ks > 0));
+                        }
+                        umma_commit_w(&bar_v_empty[sv]);
+                    }
+                }
+                umma_commit_w(&bar_tile_done);
+                g += npu;
+                gv += nbu;
+                prev_hc = (int)(gv % NSV);  // the tile's Hc slot
+                gv += 1;
+                prev_linear = lin;
+            }
+            if (k > 0) lin_mma(k - 1);
+        } else if (warp == 3) {
+            // ============ Zc = Ztot - sum_sel z_j per tile (the linear denominators) ============
+            int k = 0;
+            for (int t = blockIdx.x; t < nt; t += G, ++k) {
+                const V2Tile T = v2_tile(p, t);
+                const int pb = k & 1;
+                if (k >= 2) mbar_wait(&bar_zc_free[pb], (uint32_t)(((k >> 1) - 1) & 1));
+                if (T.linear) {
+                    const float* zb = p.zblk + T.bh * (int64_t)p.tn * D + lane * 4;
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int j0 = 0; j0 < T.nb; j0 += 32) {
+                        const int myj = (j0 + lane < T.nb) ? T.idx[j0 + lane] : 0;
+                        const int cnt = min(32, T.nb - j0);
+                        for (int u = 0; u < cnt; ++u) {
+                            const float4 z =
+                                *reinterpret_cast<const float4*>(zb + (int64_t)__shfl_sync(0xffffffffu, myj, u) * D);
+                            acc.x += z.x;
+                            acc.y += z.y;
+                            acc.z += z.z;
+                            acc.w += z.w;
+                        }
+                    }
+                    const float4 zt = *reinterpret_cast<const float4*>(p.ztot + T.bh * D + lane * 4);
+                    sZc[pb][lane * 4 + 0] = zt.x - acc.x;
+                    sZc[pb][lane * 4 + 1] = zt.y - acc.y;
+                    sZc[pb][lane * 4 + 2] = zt.z - acc.z;
+                    sZc[pb][lane * 4 + 3] = zt.w - acc.w;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_zc_ready[pb]);
+            }
+        }
+    } else if (warp < 8) {
+        reg_alloc<256>();
+        // ============ softmax: thread = query row r of tile k ============
+        const int r = threadIdx.x - 128;
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        int64_t g = 0;
+        int k = 0;
+        for (int t = blockIdx.x; t < nt; t += G, ++k) {
+            const V2Tile T = v2_tile(p, t);
+            const int nb = T.nb, npair = T.npair;
+            const bool tail_kept = p.last_valid < BK && T.idx[nb - 1] == p.tn - 1;
+            float m2 = -INFINITY, l = 0.0f;
+            for (int n = 0; n < npair; ++n) {
+                const int64_t gg = g + n;
+                const int b = (int)(gg & 1);
+                const bool two = 2 * n + 1 < nb;
+                mbar_wait(&bar_s_full, (uint32_t)(gg & 1));
+                __syncwarp();
+                tc_fence_after();
+                const uint32_t sbase = tmem + lane_base + TM_S;
+                if (tail_kept && n == npair - 1) {
+                    // ragged N: keys past N in the partial last key block get -inf (see sparse_bf16.cu)
+                    const uint32_t col0 = (uint32_t)(((nb - 1) - 2 * n) * 64);
+                    for (int tt = p.last_valid; tt < BK; ++tt) tmem_st1(sbase + col0 + tt, __float_as_uint(-INFINITY));
+                    tmem_st_wait();
+                }
+                uint32_t sr[128];
+                tmem_ld32(sbase, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                tmem_ld32(sbase + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+                if (two) {
+                    tmem_ld32(sbase + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+                    tmem_ld32(sbase + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+                }
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&bar_s_free);
+                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int tt = 0; tt < 64; tt += 8) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(sr[tt + 2 * u]), __uint_as_float(sr[tt + 2 * u + 1])));
+                }
+                if (two) {
+#pragma unroll
+                    for (int tt = 64; tt < 128; tt += 8) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            m4[u] = fmaxf(m4[u],
+                                          fmaxf(__uint_as_float(sr[tt + 2 * u]), __uint_as_float(sr[tt + 2 * u + 1])));
+                    }
+                }
+                float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                mx *= p.scale_log2;
+                if (n == 0) {
+                    m2 = mx;
+                } else {
+                    const bool need = mx > m2 + RESCALE_LOG2;
+                    if (__any_sync(0xffffffffu, need)) {
+                        const float mnew = fmaxf(m2, mx);
+                        const float corr = v2_exp2(m2 - mnew);
+                        mbar_wait(&bar_pv_done[(gg - 1) & 1], (uint32_t)(((gg - 1) >> 1) & 1));  // PVs so far
+                        __syncwarp();
+                        tc_fence_after();
+#pragma unroll
+                        for (int c0 = 0; c0 < 128; c0 += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(tmem + lane_base + TM_O + c0, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * corr);
+                            tmem_st32(tmem + lane_base + TM_O + c0, o);
+                        }
+                        l *= corr;
+                        m2 = mnew;
+                    }
+                }
+                if (gg >= 2) {  // P buffer b was last read by PV(gg - 2)
+                    mbar_wait(&bar_pv_done[b], (uint32_t)(((gg - 2) >> 1) & 1));
+                    __syncwarp();
+                    tc_fence_after();
+                }
+                const uint32_t pbase = tmem + lane_base + TM_P + b * 64;
+                float rs0 = 0.0f, rs1 = 0.0f;
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    if (blk == 1 && !two) break;
+                    uint32_t w[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float p0 = v2_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e]), p.scale_log2, -m2));
+                        const float p1 = v2_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e + 1]), p.scale_log2, -m2));
+                        rs0 += p0;
+                        rs1 += p1;
+                        w[e] = pack_bf16(p0, p1);
+                    }
+                    tmem_st32(pbase + blk * 32, w);
+                }
+                l += rs0 + rs1;
+                if (n == npair - 1) sL[k & 1][r] = l;  // before the last P: the epilogue's 1 / l
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&bar_p_full[b]);
+            }
+            mbar_arrive(&bar_sm_done[k & 1]);
+            g += npair;
+        }
+    } else {
+        reg_alloc<192>();
+        // ============ epilogue of tile k (thread = row r), one tile behind the softmax ============
+        const int r = threadIdx.x - 256;
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        int64_t gv = 0;
+        int k = 0;
+        for (int t = blockIdx.x; t < nt; t += G, ++k) {
+            const V2Tile T = v2_tile(p, t);
+            const int pb = k & 1;
+            const int64_t vhc = gv + T.nb;  // the tile's Hc slot
+            const int hcs = (int)(vhc % NSV);
+            gv = vhc + 1;
+            mbar_wait(&bar_tile_done, (uint32_t)(k & 1));  // every PV / phi(K~)^T V of the tile
+            __syncwarp();
+            tc_fence_after();
+            if (T.linear) {
+                // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
+                mbar_wait(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
+                const uint32_t hb = smem_u32(sV(hcs));
+                const float* ht = p.htot32 + T.bh * D * D + (int64_t)r * D;
+#pragma unroll
+                for (int c0 = 0; c0 < 128; c0 += 32) {
+                    uint32_t hs[32];
+                    tmem_ld32(tmem + lane_base + TM_H + c0, hs);
+                    float4 tv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) tv[u] = *reinterpret_cast<const float4*>(ht + c0 + 4 * u);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const int c = c0 + ch * 8;
+                        const float* t8 = reinterpret_cast<const float*>(&tv[2 * ch]);
+                        uint32_t o4[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            o4[e] = pack_bf16(t8[2 * e] - __uint_as_float(hs[ch * 8 + 2 * e]),
+                                              t8[2 * e + 1] - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
+                        st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), o4[0], o4[1], o4[2], o4[3]);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&bar_h_free);
+            mbar_wait(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
+            const float l = sL[pb][r];
+            float alpha = 1.0f;
+            if (T.linear) {
+                // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
+                const float x = p.rho[(int64_t)(T.bh % p.H) * p.tm + T.i];
+                float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
+                alpha = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
+                mbar_wait(&bar_zc_ready[pb], (uint32_t)((k >> 1) & 1));
+                mbar_wait(&bar_pq_full[pb], (uint32_t)((k >> 1) & 1));
+                // den = phi(Q)_r . Zc from the bf16 phi(Q) the MMA reads, then phi(Q)_r *= c
+                const uint32_t qb = smem_u32(sQ(pb));
+                uint32_t w[64];
+                float d4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {
+                    ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[4 * ch], w[4 * ch + 1],
+                                 w[4 * ch + 2], w[4 * ch + 3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[4 * ch + e]));
+                        const int f = ch * 8 + 2 * e;
+                        d4[e] = fmaf(f2.y, sZc[pb][f + 1], fmaf(f2.x, sZc[pb][f], d4[e]));
+                    }
+                }
+                const float den = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+                const bool live = T.i * BQ + r < p.N && den > 0.0f;
+                const float c = live ? (1.0f - alpha) * l / (alpha * den) : 0.0f;
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {
+                    uint32_t o4[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[4 * ch + e]));
+                        o4[e] = pack_bf16(f2.x * c, f2.y * c);
+                    }
+                    st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), o4[0], o4[1], o4[2], o4[3]);
+                }
+                fence_proxy_async_smem();  // the scaled phi(Q) and Hc are read by the async proxy
+            }
+            mbar_arrive(&bar_zc_free[pb]);
+            mbar_arrive(&bar_lin_ready);
+            mbar_wait(&bar_lin_done, (uint32_t)(k & 1));
+            __syncwarp();
+            tc_fence_after();
+            // out = alpha / l * O, bf16 into the tile's Q buffer (SW128), one TMA store
+            const float sc = alpha / l;
+            const uint32_t ob = smem_u32(sQ(pb));
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t o[64];
+                tmem_ld32(tmem + lane_base + TM_O + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+                tmem_ld32(tmem + lane_base + TM_O + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+                tmem_ld_wait();
+                if (half == 1) {
+                    tc_fence_before();
+                    mbar_arrive(&bar_o_free);  // the next tile's first PV may overwrite O
+                }
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch)
+                    st_shared_v4(ob + half * 16384 + sw128_off(r, ch * 8),
+                                 pack_bf16(__uint_as_float(o[ch * 8 + 0]) * sc, __uint_as_float(o[ch * 8 + 1]) * sc),
+                                 pack_bf16(__uint_as_float(o[ch * 8 + 2]) * sc, __uint_as_float(o[ch * 8 + 3]) * sc),
+                                 pack_bf16(__uint_as_float(o[ch * 8 + 4]) * sc, __uint_as_float(o[ch * 8 + 5]) * sc),
+                                 pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (r == 0) {
+                const int orow0 = T.i * BQ, hz = (int)T.bh;  // rows past N (ragged tail) are dropped
+                tma_store_3d(&tmO, 0, orow0, hz, sQ(pb));
+                tma_store_3d(&tmO, 0, orow0 + 64, hz, sQ(pb) + 8192);
+                tma_store_3d(&tmO, 64, orow0, hz, sQ(pb) + 16384);
+                tma_store_3d(&tmO, 64, orow0 + 64, hz, sQ(pb) + 24576);
+                tma_store_commit();
+                tma_store_wait_read();
+                mbar_arrive(&bar_q_empty[pb]);   // Q of tile k+2 may land here
+                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring
+            }
+        }
+        if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_free(tmem, 512);
+    }
+}
+
+bool sparse_v2_eligible(const SparseLaunch& a) {
+    return !a.dense && a.bq == 128 && a.bk == 64 && a.d == 128 && a.o_s == nullptr && a.o_l == nullptr &&
+           a.big_l == nullptr && a.h_blocks == nullptr && a.z_blocks == nullptr && a.tm_phiq != nullptr;
+}
+
+cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launches) {
+    SparseV2Params p;
+    p.kv_idx = a.kv_idx;
+    p.kv_cnt = a.kv_cnt;
+    p.kstride = a.kstride;
+    p.kappa = a.kappa;
+    p.rho = a.rho;
+    p.ztot = a.ztot;
+    p.zblk = a.zblk;
+    p.htot32 = a.htot;
+    p.N = a.N;
+    p.H = (int)a.H;
+    p.tm = a.tm;
+    p.tn = a.tn;
+    p.ntiles = (int)(a.B * a.H) * a.tm;
+    p.last_valid = a.N - (a.tn - 1) * v2::BK;
+    p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
+    cudaError_t e = ensure_smem_attr((const void*)sla2_sparse_v2_kernel, (int)v2::SMEM_ALLOC);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = p.ntiles < sms ? p.ntiles : sms;
+    sla2_sparse_v2_kernel<<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v, *a.tm_phik,
+                                                                      *a.tm_phiq, *a.tm_out, p);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace sla2dev

@@ -135,22 +135,33 @@ __global__ void __launch_bounds__(256, 1) umma_kernel(int mode, int reps, int tr
             stop = 1;
         }
     } else if (warp == 2 && traffic) {
-        // bulk copies global (L2-resident 1 MB window) -> smem region [160 KB, 192 KB)
+        // `traffic` bulk copies of 8 KB in flight, global (an L2-resident 1 MB window) -> smem
+        // region [160 KB, 160 KB + 8 KB * traffic): the TMA producers' smem writes
         if (threadIdx.x == 64) {
-            uint32_t ph = 0;
-            const uint32_t dst = smem_u32(smem + 163840);
-            int n = 0;
-            while (!stop) {
-                mbar_arrive_expect_tx(&tbar, 32768);
-                const uint8_t* src = gsrc + ((size_t)((blockIdx.x * 7 + n) & 31) << 15);
+            __shared__ uint64_t tb[8];
+            for (int s = 0; s < traffic; ++s) mbar_init(&tb[s], 1);
+            fence_barrier_init();
+            uint32_t ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            long n = 0;
+            auto issue = [&](int s) {
+                mbar_arrive_expect_tx(&tb[s], 8192);
+                const uint8_t* src = gsrc + ((size_t)((blockIdx.x * 8191 + n * 37) & 8191) << 13);  // 64 MB window
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(src), "r"(32768), "r"(smem_u32(&tbar))
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(smem + 163840 + s * 8192)),
+                    "l"(src), "r"(8192), "r"(smem_u32(&tb[s]))
                     : "memory");
-                mbar_wait(&tbar, ph);
-                ph ^= 1;
                 ++n;
+            };
+            for (int s = 0; s < traffic; ++s) issue(s);
+            int s = 0;
+            while (!stop) {
+                mbar_wait(&tb[s], ph[s]);
+                ph[s] ^= 1;
+                issue(s);
+                s = (s + 1) % traffic;
             }
+            for (int u = 0; u < traffic; ++u) mbar_wait(&tb[u], ph[u]);
             out[148 + blockIdx.x] = n;
         }
     }
@@ -166,8 +177,8 @@ int main() {
     unsigned long long* d_out;
     uint8_t* g;
     cudaMalloc(&d_out, 2 * 148 * sizeof(unsigned long long));
-    cudaMalloc(&g, 1 << 20);
-    cudaMemset(g, 1, 1 << 20);
+    cudaMalloc(&g, 64 << 20);
+    cudaMemset(g, 1, 64 << 20);
     cudaFuncSetAttribute(umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B + 1024);
     const char* names[] = {"SS K/K N128 1acc",   "TS N128 1acc",        "SS K/K N256 1acc", "SS MN/MN N128",
                            "SS N128 2acc alt",   "pair mix QK8 PV8 HS8", "f8 SS MN N128 K32", "SS K/K N64 1acc",
@@ -176,8 +187,9 @@ int main() {
                                2.0 * 128 * 128 * 16, 2.0 * 128 * 128 * 16, 2.0 * 128 * 128 * 32, 2.0 * 128 * 64 * 16,
                                2.0 * 128 * 128 * 16, 2.0 * 128 * 256 * 16};
     const int reps = 24 * 400;
-    for (int traffic = 0; traffic < 2; ++traffic) {
+    for (int traffic : {0, 1, 2, 4, 6}) {
         for (int mode = 0; mode < 10; ++mode) {
+            if (traffic && mode != 0 && mode != 1 && mode != 3 && mode != 5) continue;
             umma_kernel<<<148, 256, SMEM_B + 1024>>>(mode, reps, traffic, g, d_out);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
@@ -191,7 +203,7 @@ int main() {
             double fpc = (mode == 8 ? (16 * 2.0 * 128 * 128 * 16 + 4 * 2.0 * 128 * 128 * 32) / 20 : flop_per[mode]) / cyc;
             printf("traffic %d  %-22s cycles/MMA %6.1f  flop/clk %7.0f (peak bf16 8192)%s", traffic, names[mode], cyc,
                    fpc, traffic ? "" : "\n");
-            if (traffic) printf("  copies %.1f KB/kcyc\n", (double)h[148] * 32.0 / ((double)h[0] / 1000.0));
+            if (traffic) printf("  copies %.1f B/clk\n", (double)h[148] * 8192.0 / (double)h[0]);
         }
     }
     return 0;
