@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "expf_glibc.cuh"
 #include "kernels.h"
@@ -46,7 +47,7 @@ constexpr uint32_t OFF_Q = 0;                  // 2 Q buffers
 constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr uint32_t OFF_V = OFF_K + NKP * KP_BYTES;
 constexpr uint32_t SMEM_BYTES = OFF_V + NSV * VS_BYTES;  // 224 KB
-constexpr uint32_t SMEM_ALLOC = SMEM_BYTES + 1024;
+constexpr uint32_t SMEM_ALLOC = SMEM_BYTES;  // + 3 KB static = the 227 KB limit: no alignment slack
 constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 256, TM_H = 384;
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int NTHREADS = 384;
@@ -79,6 +80,29 @@ __device__ __forceinline__ void reg_dealloc() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
 }
 
+// Bounded waits in analysis builds (-DSLA2_V2_WATCHDOG): a wait that spins ~seconds records
+// (block, warp, site, parity) in g_v2_hang and traps instead of hanging the GPU.
+#ifdef SLA2_V2_WATCHDOG
+__device__ unsigned long long g_v2_hang[4];
+__device__ __forceinline__ void v2_wait(uint64_t* bar, uint32_t parity, int site) {
+    for (long long it = 0; !mbar_try_wait(bar, parity); ++it) {
+        if (it == (1ll << 26)) {
+            g_v2_hang[0] = blockIdx.x;
+            g_v2_hang[1] = threadIdx.x >> 5;
+            g_v2_hang[2] = (unsigned long long)site;
+            g_v2_hang[3] = parity;
+            __threadfence_system();
+            printf("sla2_sparse_v2 HANG block %d warp %d lane %d line %d parity %u\n", blockIdx.x, threadIdx.x >> 5,
+                   threadIdx.x & 31, site, parity);
+            __trap();
+        }
+    }
+}
+#define V2_WAIT(bar, par) v2_wait(bar, par, __LINE__)
+#else
+#define V2_WAIT(bar, par) mbar_wait(bar, par)
+#endif
+
 // Everything about tile t every role needs (all roles walk the same tile sequence).
 struct V2Tile {
     int64_t bh;
@@ -104,7 +128,7 @@ __global__ void __launch_bounds__(384, 1)
                           const SparseV2Params p) {
     using namespace v2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw;  // 1024-aligned (static shared memory is a multiple of 1 KB; checked below)
     __shared__ uint64_t bar_q_full[2], bar_q_empty[2], bar_qk_done[2], bar_pq_full[2], bar_k_full[NKP],
         bar_k_empty[NKP], bar_v_full[NSV], bar_v_empty[NSV], bar_s_full, bar_s_free, bar_p_full[2], bar_pv_done[2],
         bar_tile_done, bar_sm_done[2], bar_h_free, bar_lin_ready, bar_lin_done, bar_o_free, bar_zc_ready[2],
@@ -120,6 +144,7 @@ __global__ void __launch_bounds__(384, 1)
     auto sV = [&](int s) { return smem + OFF_V + s * VS_BYTES; };
 
     if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar_q_full[b], 1);
             mbar_init(&bar_q_empty[b], 1);
@@ -154,6 +179,8 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
 
+    // register budget per thread: 64 (producers, MMA, Zc) + 248 (softmax) + 192 (epilogue) = 504 =
+    // 3 x 168, the CTA's launch allocation (setmaxnreg.inc can only take what .dec released)
     if (warp < 4) {
         reg_dealloc<64>();
         if (warp == 0 && lane == 0) {
@@ -180,7 +207,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int pb = k & 1;
                 for (int n = 0; n < T.npair; ++n, ++gk) {
                     const int s = (int)(gk % NKP);
-                    if (gk >= NKP) mbar_wait(&bar_k_empty[s], (uint32_t)(((gk / NKP) - 1) & 1));
+                    if (gk >= NKP) V2_WAIT(&bar_k_empty[s], (uint32_t)(((gk / NKP) - 1) & 1));
                     const int cnt = min(2, T.nb - 2 * n);
                     mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
                     for (int b = 0; b < cnt; ++b) {
@@ -193,11 +220,11 @@ __global__ void __launch_bounds__(384, 1)
                 if (t + G < nt) {
                     const V2Tile T1 = v2_tile(p, t + G);
                     const int k1 = k + 1;
-                    if (k1 >= 2) mbar_wait(&bar_q_empty[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
+                    if (k1 >= 2) V2_WAIT(&bar_q_empty[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
                     load_q(&tmQ, &bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
                 }
                 // phi(Q) of this tile over its Q once the last Q K^T has read Q
-                mbar_wait(&bar_qk_done[pb], (uint32_t)((k >> 1) & 1));
+                V2_WAIT(&bar_qk_done[pb], (uint32_t)((k >> 1) & 1));
                 if (T.linear) load_q(&tmPq, &bar_pq_full[pb], sQ(pb), T.i * BQ, (int)T.bh);
                 else mbar_arrive(&bar_pq_full[pb]);
             }
@@ -211,7 +238,7 @@ __global__ void __launch_bounds__(384, 1)
                 const V2Tile T = v2_tile(p, t);
                 for (int j = 0; j <= T.nb; ++j, ++gv) {
                     const int s = (int)(gv % NSV);
-                    if (gv >= NSV) mbar_wait(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
+                    if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
                     if (j == T.nb) {  // the Hc slot: allocated, not loaded
                         mbar_arrive(&bar_v_full[s]);
                         continue;
@@ -243,11 +270,11 @@ __global__ void __launch_bounds__(384, 1)
             int prev_hc = 0;
             auto issue_qk = [&](int64_t gg, int pb, int nbu, int n) {
                 if (gg > 0) {
-                    mbar_wait(&bar_s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in registers
+                    V2_WAIT(&bar_s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in registers
                     tc_fence_after();
                 }
                 const int s = (int)(gg % NKP);
-                mbar_wait(&bar_k_full[s], (uint32_t)((gg / NKP) & 1));
+                V2_WAIT(&bar_k_full[s], (uint32_t)((gg / NKP) & 1));
                 tc_fence_after();
                 const uint32_t idq = (2 * n + 1 < nbu) ? ID_QK2 : ID_QK1;
                 const uint64_t dQ = sdesc_sw128(sbase + OFF_Q + pb * Q_BYTES, 16, 1024);
@@ -261,7 +288,7 @@ __global__ void __launch_bounds__(384, 1)
                 umma_commit_w(&bar_k_empty[s]);
             };
             auto lin_mma = [&](int kk) {  // O += (c phi(Q)) Hc of tile kk (epilogue inputs ready)
-                mbar_wait(&bar_lin_ready, (uint32_t)(kk & 1));
+                V2_WAIT(&bar_lin_ready, (uint32_t)(kk & 1));
                 tc_fence_after();
                 if (prev_linear) {
                     const uint64_t dA = sdesc_sw128(sbase + OFF_Q + (kk & 1) * Q_BYTES, 16, 1024);
@@ -280,7 +307,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int npu = (nbu + 1) >> 1;
                 const bool lin = T.linear;
                 const int pb = k & 1;
-                mbar_wait(&bar_q_full[pb], (uint32_t)((k >> 1) & 1));
+                V2_WAIT(&bar_q_full[pb], (uint32_t)((k >> 1) & 1));
                 tc_fence_after();
                 issue_qk(g, pb, nbu, 0);
                 if (npu == 1) umma_commit_w(&bar_qk_done[pb]);
@@ -291,17 +318,17 @@ __global__ void __launch_bounds__(384, 1)
                         issue_qk(gg + 1, pb, nbu, n + 1);
                         if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
                     }
-                    mbar_wait(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
+                    V2_WAIT(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
                     tc_fence_after();
                     if (n == 0 && k > 0) {
-                        mbar_wait(&bar_o_free, (uint32_t)((k - 1) & 1));  // tile k-1's O left TMEM
+                        V2_WAIT(&bar_o_free, (uint32_t)((k - 1) & 1));  // tile k-1's O left TMEM
                         tc_fence_after();
                     }
                     const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
                     for (int j = j0; j < j1; ++j) {
                         const int64_t v = gv + j;
                         const int sv = (int)(v % NSV);
-                        mbar_wait(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
+                        V2_WAIT(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
                         tc_fence_after();
                         const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
                         const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 32);
@@ -311,7 +338,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     umma_commit_w(&bar_pv_done[gg & 1]);
                     if (n == 0 && k > 0) {
-                        mbar_wait(&bar_h_free, (uint32_t)((k - 1) & 1));  // tile k-1's Hsel left TMEM
+                        V2_WAIT(&bar_h_free, (uint32_t)((k - 1) & 1));  // tile k-1's Hsel left TMEM
                         tc_fence_after();
                     }
                     for (int j = j0; j < j1; ++j) {
@@ -341,7 +368,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int t = blockIdx.x; t < nt; t += G, ++k) {
                 const V2Tile T = v2_tile(p, t);
                 const int pb = k & 1;
-                if (k >= 2) mbar_wait(&bar_zc_free[pb], (uint32_t)(((k >> 1) - 1) & 1));
+                if (k >= 2) V2_WAIT(&bar_zc_free[pb], (uint32_t)(((k >> 1) - 1) & 1));
                 if (T.linear) {
                     const float* zb = p.zblk + T.bh * (int64_t)p.tn * D + lane * 4;
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -368,7 +395,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp < 8) {
-        reg_alloc<256>();
+        reg_alloc<248>();
         // ============ softmax: thread = query row r of tile k ============
         const int r = threadIdx.x - 128;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
@@ -383,7 +410,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int64_t gg = g + n;
                 const int b = (int)(gg & 1);
                 const bool two = 2 * n + 1 < nb;
-                mbar_wait(&bar_s_full, (uint32_t)(gg & 1));
+                V2_WAIT(&bar_s_full, (uint32_t)(gg & 1));
                 __syncwarp();
                 tc_fence_after();
                 const uint32_t sbase = tmem + lane_base + TM_S;
@@ -428,7 +455,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (__any_sync(0xffffffffu, need)) {
                         const float mnew = fmaxf(m2, mx);
                         const float corr = v2_exp2(m2 - mnew);
-                        mbar_wait(&bar_pv_done[(gg - 1) & 1], (uint32_t)(((gg - 1) >> 1) & 1));  // PVs so far
+                        V2_WAIT(&bar_pv_done[(gg - 1) & 1], (uint32_t)(((gg - 1) >> 1) & 1));  // PVs so far
                         __syncwarp();
                         tc_fence_after();
 #pragma unroll
@@ -445,7 +472,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
                 if (gg >= 2) {  // P buffer b was last read by PV(gg - 2)
-                    mbar_wait(&bar_pv_done[b], (uint32_t)(((gg - 2) >> 1) & 1));
+                    V2_WAIT(&bar_pv_done[b], (uint32_t)(((gg - 2) >> 1) & 1));
                     __syncwarp();
                     tc_fence_after();
                 }
@@ -487,12 +514,12 @@ __global__ void __launch_bounds__(384, 1)
             const int64_t vhc = gv + T.nb;  // the tile's Hc slot
             const int hcs = (int)(vhc % NSV);
             gv = vhc + 1;
-            mbar_wait(&bar_tile_done, (uint32_t)(k & 1));  // every PV / phi(K~)^T V of the tile
+            V2_WAIT(&bar_tile_done, (uint32_t)(k & 1));  // every PV / phi(K~)^T V of the tile
             __syncwarp();
             tc_fence_after();
             if (T.linear) {
                 // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
-                mbar_wait(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
+                V2_WAIT(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
                 const uint32_t hb = smem_u32(sV(hcs));
                 const float* ht = p.htot32 + T.bh * D * D + (int64_t)r * D;
 #pragma unroll
@@ -518,7 +545,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             tc_fence_before();
             mbar_arrive(&bar_h_free);
-            mbar_wait(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
+            V2_WAIT(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
             const float l = sL[pb][r];
             float alpha = 1.0f;
             if (T.linear) {
@@ -526,8 +553,8 @@ __global__ void __launch_bounds__(384, 1)
                 const float x = p.rho[(int64_t)(T.bh % p.H) * p.tm + T.i];
                 float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
                 alpha = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
-                mbar_wait(&bar_zc_ready[pb], (uint32_t)((k >> 1) & 1));
-                mbar_wait(&bar_pq_full[pb], (uint32_t)((k >> 1) & 1));
+                V2_WAIT(&bar_zc_ready[pb], (uint32_t)((k >> 1) & 1));
+                V2_WAIT(&bar_pq_full[pb], (uint32_t)((k >> 1) & 1));
                 // den = phi(Q)_r . Zc from the bf16 phi(Q) the MMA reads, then phi(Q)_r *= c
                 const uint32_t qb = smem_u32(sQ(pb));
                 uint32_t w[64];
@@ -560,7 +587,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             mbar_arrive(&bar_zc_free[pb]);
             mbar_arrive(&bar_lin_ready);
-            mbar_wait(&bar_lin_done, (uint32_t)(k & 1));
+            V2_WAIT(&bar_lin_done, (uint32_t)(k & 1));
             __syncwarp();
             tc_fence_after();
             // out = alpha / l * O, bf16 into the tile's Q buffer (SW128), one TMA store
