@@ -567,6 +567,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     sa.kappa = (int)g.kappa;
     sa.rho = rho;
     sa.htot = w.htot;
+    sa.htot16 = w.htot16;
     sa.ztot = w.ztot;
     sa.zblk = w.zblk;
     sa.mu = w.mu;
@@ -591,6 +592,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.tm_phik = &mphi;
         sa.tm_ht = &mht;
         sa.tm_phiq = w.phiq ? &mpq : nullptr;
+        sa.phiq = w.phiq;
         sa.tm_out = &mo;
         if (g.quant) {
             // INT8 QAT (QuantConfig, quant.hpp:15-19): per-tile codes + scales, then the kind::i8 kernel

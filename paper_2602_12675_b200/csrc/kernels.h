@@ -101,6 +101,7 @@ struct SparseLaunch {
     int kstride, kappa;
     const float* rho;   // [H][tm]
     const float* htot;  // [BH][d][d]
+    const void* htot16;  // [BH][d][d] bf16 copy (bf16 path)
     const float* ztot;  // [BH][d]
     const float* zblk;  // [BH][tn][d]
     const float* mu;    // [BH][d] (for L correction / f32 K~), may be null when smooth == 0
@@ -121,6 +122,7 @@ struct SparseLaunch {
     const CUtensorMap* tm_phik;
     const CUtensorMap* tm_ht;  // Htot bf16 as [BH*d][d], box 64 x 128, SW128
     const CUtensorMap* tm_phiq;  // phi(Q) bf16 as [BH*N][d] (launch_phiq), box 64 x 64, SW128
+    const void* phiq;            // the same phi(Q) rows (bf16 [BH][N][d])
     const CUtensorMap* tm_out;   // out bf16 as [BH*N][d], box 64 x 64, SW128 (TMA-stored blocks)
     // f32 path
     const float* q;

@@ -60,10 +60,15 @@ struct SparseV2Params {
     const float* rho;
     const float* ztot;
     const float* zblk;
-    const float* htot32;  // [BH][D][D] fp32 (the epilogue forms Hc = Htot - Hsel from it)
+    const __nv_bfloat16* htot16;  // [BH][D][D] bf16 (the epilogue forms Hc = Htot - Hsel from it)
+    const __nv_bfloat16* phiq;    // [BH][N][D] bf16 phi(Q) rows (router front)
+    __nv_bfloat16* out;           // [BH][N][D]
     int N, H, tm, tn, ntiles;
     int last_valid;
     float scale_log2;
+#ifdef SLA2_TRACE
+    unsigned long long* trace;  // [grid][8 tiles][32 events] %globaltimer stamps (analysis build)
+#endif
 };
 
 __device__ __forceinline__ float v2_exp2(float x) {
@@ -103,6 +108,19 @@ __device__ __forceinline__ void v2_wait(uint64_t* bar, uint32_t parity, int site
 #define V2_WAIT(bar, par) mbar_wait(bar, par)
 #endif
 
+#ifdef SLA2_TRACE
+__device__ __forceinline__ unsigned long long v2_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// event e of this CTA's k-th tile (k < 8)
+#define V2_TR(k, e) \
+    if ((k) < 8) p.trace[((size_t)blockIdx.x * 8 + (k)) * 32 + (e)] = v2_gtimer()
+#else
+#define V2_TR(k, e)
+#endif
+
 // Everything about tile t every role needs (all roles walk the same tile sequence).
 struct V2Tile {
     int64_t bh;
@@ -121,17 +139,57 @@ __device__ __forceinline__ V2Tile v2_tile(const SparseV2Params& p, int t) {
     return r;
 }
 
+// MMA-issuer steps (whole warp; elect.sync inside each tcgen05 op). Plain functions with
+// by-value state: the counters stay in registers (lambdas capturing them by reference put them
+// on the stack).
+__device__ __forceinline__ void v2_issue_qk(uint64_t* s_free, uint64_t* k_full, uint64_t* k_empty, uint64_t* s_full,
+                                            int gg, uint32_t sbase, uint32_t tm, int pb, int nbu, int n) {
+    using namespace v2;
+    if (gg > 0) {
+        V2_WAIT(s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in the softmax's registers
+        tc_fence_after();
+    }
+    const int s = gg % NKP;
+    V2_WAIT(&k_full[s], (uint32_t)((gg / NKP) & 1));
+    tc_fence_after();
+    const uint32_t idq = (2 * n + 1 < nbu) ? idesc_bf16(128, 128, false, false) : idesc_bf16(128, 64, false, false);
+    const uint64_t dQ = sdesc_sw128(sbase + OFF_Q + pb * Q_BYTES, 16, 1024);
+    const uint64_t dK = sdesc_sw128(sbase + OFF_K + s * KP_BYTES, 16, 1024);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
+        umma_bf16_ss_w(tm + TM_S, dQ + off, dK + off, idq, ks > 0);
+    }
+    umma_commit_w(s_full);
+    umma_commit_w(&k_empty[s]);
+}
+// O += (c phi(Q)) Hc of tile kk once the epilogue has built both operands: A = c phi(Q) rows in
+// the first 64 Hsel columns of TMEM (TS), B = Hc (MN-major) in the tile's Hc slot. The tile's
+// Hsel was read before, and the next tile's phi(K~)^T V MMAs follow this one in the tensor pipe.
+__device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_done, int kk, bool linear, int hc,
+                                           uint32_t sbase, uint32_t tm) {
+    using namespace v2;
+    V2_WAIT(lin_ready, (uint32_t)(kk & 1));
+    tc_fence_after();
+    if (linear) {
+        const uint64_t dB = sdesc_sw128(sbase + OFF_V + hc * VS_BYTES, 16384, 1024);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+            umma_bf16_ts_w(tm + TM_O, tm + TM_H + ks * 8, dB + ((ks * 2048) >> 4), idesc_bf16(128, 128, false, true), 1);
+    }
+    umma_commit_w(lin_done);
+}
+
 __global__ void __launch_bounds__(384, 1)
     sla2_sparse_v2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
-                          const __grid_constant__ CUtensorMap tmPq, const __grid_constant__ CUtensorMap tmO,
                           const SparseV2Params p) {
     using namespace v2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;  // 1024-aligned (static shared memory is a multiple of 1 KB; checked below)
-    __shared__ uint64_t bar_q_full[2], bar_q_empty[2], bar_qk_done[2], bar_pq_full[2], bar_k_full[NKP],
+    __shared__ uint64_t bar_q_full[2], bar_qk_done[2], bar_k_full[NKP],
         bar_k_empty[NKP], bar_v_full[NSV], bar_v_empty[NSV], bar_s_full, bar_s_free, bar_p_full[2], bar_pv_done[2],
-        bar_tile_done, bar_sm_done[2], bar_h_free, bar_lin_ready, bar_lin_done, bar_o_free, bar_zc_ready[2],
+        bar_tile_done, bar_sm_done[2], bar_lin_ready, bar_lin_done, bar_o_free, bar_zc_ready[2],
         bar_zc_free[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ float sZc[2][D];
@@ -147,9 +205,7 @@ __global__ void __launch_bounds__(384, 1)
         if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need 1 KB alignment
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bar_q_full[b], 1);
-            mbar_init(&bar_q_empty[b], 1);
             mbar_init(&bar_qk_done[b], 1);
-            mbar_init(&bar_pq_full[b], 1);
             mbar_init(&bar_p_full[b], 128);
             mbar_init(&bar_pv_done[b], 1);
             mbar_init(&bar_sm_done[b], 128);
@@ -167,7 +223,6 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(&bar_s_full, 1);
         mbar_init(&bar_s_free, 128);
         mbar_init(&bar_tile_done, 1);
-        mbar_init(&bar_h_free, 128);
         mbar_init(&bar_lin_ready, 128);
         mbar_init(&bar_lin_done, 1);
         mbar_init(&bar_o_free, 128);
@@ -179,15 +234,14 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
 
-    // register budget per thread: 64 (producers, MMA, Zc) + 248 (softmax) + 192 (epilogue) = 504 =
+    // register budget per thread: 72 (producers, MMA, Zc) + 224 (softmax) + 208 (epilogue) = 504 =
     // 3 x 168, the CTA's launch allocation (setmaxnreg.inc can only take what .dec released)
     if (warp < 4) {
-        reg_dealloc<64>();
+        reg_dealloc<72>();
         if (warp == 0 && lane == 0) {
             // ============ TMA producer: Q (two buffers), K pairs, phi(Q) over the tile's Q ============
             tma_prefetch_desc(&tmQ);
             tma_prefetch_desc(&tmK);
-            tma_prefetch_desc(&tmPq);
             const uint64_t pol = policy_evict_last();
             auto load_q = [&](const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int qrow, int hz) {
                 mbar_arrive_expect_tx(bar, Q_BYTES);
@@ -216,17 +270,13 @@ __global__ void __launch_bounds__(384, 1)
                         tma_load_3d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, (int)T.bh, &bar_k_full[s], pol);
                     }
                 }
-                // Q of the next tile into the other buffer (free once tile k-1's output left it)
+                // Q of the next tile into the other buffer, free once tile k-1's last Q K^T read it
                 if (t + G < nt) {
                     const V2Tile T1 = v2_tile(p, t + G);
                     const int k1 = k + 1;
-                    if (k1 >= 2) V2_WAIT(&bar_q_empty[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
+                    if (k1 >= 2) V2_WAIT(&bar_qk_done[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
                     load_q(&tmQ, &bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
                 }
-                // phi(Q) of this tile over its Q once the last Q K^T has read Q
-                V2_WAIT(&bar_qk_done[pb], (uint32_t)((k >> 1) & 1));
-                if (T.linear) load_q(&tmPq, &bar_pq_full[pb], sQ(pb), T.i * BQ, (int)T.bh);
-                else mbar_arrive(&bar_pq_full[pb]);
             }
         } else if (warp == 2 && lane == 0) {
             // ============ TMA producer: V / phi(K~) ring; one slot per tile for the epilogue's Hc ============
@@ -262,45 +312,12 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t ID_LIN = idesc_bf16(128, 128, false, true);
             const uint32_t tm = warp_uniform(tmem);
             const uint32_t sbase = warp_uniform(smem_u32(smem));
-            const uint64_t dK0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
+            uint64_t* bar_s_free_p = &bar_s_free;
             const uint64_t dVm = sdesc_sw128(sbase + OFF_V, 8192, 1024);
-            int64_t g = 0, gv = 0;
+            int g = 0, gv = 0;  // global pair / V-slot counters (< 2^31 per CTA)
             int k = 0;
             bool prev_linear = false;
             int prev_hc = 0;
-            auto issue_qk = [&](int64_t gg, int pb, int nbu, int n) {
-                if (gg > 0) {
-                    V2_WAIT(&bar_s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in registers
-                    tc_fence_after();
-                }
-                const int s = (int)(gg % NKP);
-                V2_WAIT(&bar_k_full[s], (uint32_t)((gg / NKP) & 1));
-                tc_fence_after();
-                const uint32_t idq = (2 * n + 1 < nbu) ? ID_QK2 : ID_QK1;
-                const uint64_t dQ = sdesc_sw128(sbase + OFF_Q + pb * Q_BYTES, 16, 1024);
-                const uint64_t dK = dK0 + ((s * KP_BYTES) >> 4);
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
-                    umma_bf16_ss_w(tm + TM_S, dQ + off, dK + off, idq, ks > 0);
-                }
-                umma_commit_w(&bar_s_full);
-                umma_commit_w(&bar_k_empty[s]);
-            };
-            auto lin_mma = [&](int kk) {  // O += (c phi(Q)) Hc of tile kk (epilogue inputs ready)
-                V2_WAIT(&bar_lin_ready, (uint32_t)(kk & 1));
-                tc_fence_after();
-                if (prev_linear) {
-                    const uint64_t dA = sdesc_sw128(sbase + OFF_Q + (kk & 1) * Q_BYTES, 16, 1024);
-                    const uint64_t dB = sdesc_sw128(sbase + OFF_V + prev_hc * VS_BYTES, 16384, 1024);
-#pragma unroll
-                    for (int ks = 0; ks < 8; ++ks) {
-                        const uint32_t off = ((ks >> 2) * 16384 + (ks & 3) * 32) >> 4;
-                        umma_bf16_ss_w(tm + TM_O, dA + off, dB + ((ks * 2048) >> 4), ID_LIN, 1);
-                    }
-                }
-                umma_commit_w(&bar_lin_done);
-            };
             for (int t = blockIdx.x; t < nt; t += G, ++k) {
                 const V2Tile T = v2_tile(p, t);
                 const int nbu = (int)warp_uniform((uint32_t)T.nb);
@@ -309,25 +326,28 @@ __global__ void __launch_bounds__(384, 1)
                 const int pb = k & 1;
                 V2_WAIT(&bar_q_full[pb], (uint32_t)((k >> 1) & 1));
                 tc_fence_after();
-                issue_qk(g, pb, nbu, 0);
+                if (lane == 0) V2_TR(k, 0);
+                v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, g, sbase, tm, pb, nbu, 0);
                 if (npu == 1) umma_commit_w(&bar_qk_done[pb]);
-                if (k > 0) lin_mma(k - 1);
                 for (int n = 0; n < npu; ++n) {
-                    const int64_t gg = g + n;
+                    const int gg = g + n;
                     if (n + 1 < npu) {
-                        issue_qk(gg + 1, pb, nbu, n + 1);
+                        v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, gg + 1, sbase, tm, pb, nbu, n + 1);
                         if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
                     }
+                    if (n == 0 && k > 0)  // tile k-1's linear term, before PV(0)
+                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
                     V2_WAIT(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
                     tc_fence_after();
                     if (n == 0 && k > 0) {
                         V2_WAIT(&bar_o_free, (uint32_t)((k - 1) & 1));  // tile k-1's O left TMEM
                         tc_fence_after();
                     }
+                    if (lane == 0 && n < 8) V2_TR(k, 25 + (n < 2 ? n : 2));
                     const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
                     for (int j = j0; j < j1; ++j) {
-                        const int64_t v = gv + j;
-                        const int sv = (int)(v % NSV);
+                        const int v = gv + j;
+                        const int sv = v % NSV;
                         V2_WAIT(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
                         tc_fence_after();
                         const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
@@ -337,10 +357,6 @@ __global__ void __launch_bounds__(384, 1)
                             umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
                     }
                     umma_commit_w(&bar_pv_done[gg & 1]);
-                    if (n == 0 && k > 0) {
-                        V2_WAIT(&bar_h_free, (uint32_t)((k - 1) & 1));  // tile k-1's Hsel left TMEM
-                        tc_fence_after();
-                    }
                     for (int j = j0; j < j1; ++j) {
                         const int sv = (int)((gv + j) % NSV);
                         if (lin) {
@@ -355,13 +371,14 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
                 umma_commit_w(&bar_tile_done);
+                if (lane == 0) V2_TR(k, 28);
                 g += npu;
                 gv += nbu;
-                prev_hc = (int)(gv % NSV);  // the tile's Hc slot
+                prev_hc = gv % NSV;  // the tile's Hc slot
                 gv += 1;
                 prev_linear = lin;
             }
-            if (k > 0) lin_mma(k - 1);
+            if (k > 0) v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
         } else if (warp == 3) {
             // ============ Zc = Ztot - sum_sel z_j per tile (the linear denominators) ============
             int k = 0;
@@ -375,13 +392,21 @@ __global__ void __launch_bounds__(384, 1)
                     for (int j0 = 0; j0 < T.nb; j0 += 32) {
                         const int myj = (j0 + lane < T.nb) ? T.idx[j0 + lane] : 0;
                         const int cnt = min(32, T.nb - j0);
-                        for (int u = 0; u < cnt; ++u) {
-                            const float4 z =
-                                *reinterpret_cast<const float4*>(zb + (int64_t)__shfl_sync(0xffffffffu, myj, u) * D);
-                            acc.x += z.x;
-                            acc.y += z.y;
-                            acc.z += z.z;
-                            acc.w += z.w;
+                        for (int u0 = 0; u0 < cnt; u0 += 8) {  // 8 rows in flight per lane
+                            float4 z[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int jj = __shfl_sync(0xffffffffu, myj, (u0 + u) & 31);
+                                z[u] = u0 + u < cnt ? *reinterpret_cast<const float4*>(zb + (int64_t)jj * D)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                acc.x += z[u].x;
+                                acc.y += z[u].y;
+                                acc.z += z[u].z;
+                                acc.w += z[u].w;
+                            }
                         }
                     }
                     const float4 zt = *reinterpret_cast<const float4*>(p.ztot + T.bh * D + lane * 4);
@@ -395,7 +420,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp < 8) {
-        reg_alloc<248>();
+        reg_alloc<224>();
         // ============ softmax: thread = query row r of tile k ============
         const int r = threadIdx.x - 128;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
@@ -413,6 +438,7 @@ __global__ void __launch_bounds__(384, 1)
                 V2_WAIT(&bar_s_full, (uint32_t)(gg & 1));
                 __syncwarp();
                 tc_fence_after();
+                if (r == 0 && n < 8) V2_TR(k, 1 + n);
                 const uint32_t sbase = tmem + lane_base + TM_S;
                 if (tail_kept && n == npair - 1) {
                     // ragged N: keys past N in the partial last key block get -inf (see sparse_bf16.cu)
@@ -497,102 +523,113 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&bar_p_full[b]);
+                if (r == 0 && n < 8) V2_TR(k, 9 + n);
             }
             mbar_arrive(&bar_sm_done[k & 1]);
             g += npair;
         }
     } else {
-        reg_alloc<192>();
+        reg_alloc<208>();
         // ============ epilogue of tile k (thread = row r), one tile behind the softmax ============
         const int r = threadIdx.x - 256;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        int64_t gv = 0;
+        int gv = 0;
         int k = 0;
         for (int t = blockIdx.x; t < nt; t += G, ++k) {
             const V2Tile T = v2_tile(p, t);
             const int pb = k & 1;
-            const int64_t vhc = gv + T.nb;  // the tile's Hc slot
-            const int hcs = (int)(vhc % NSV);
+            const int vhc = gv + T.nb;  // the tile's Hc slot
+            const int hcs = vhc % NSV;
             gv = vhc + 1;
-            V2_WAIT(&bar_tile_done, (uint32_t)(k & 1));  // every PV / phi(K~)^T V of the tile
-            __syncwarp();
-            tc_fence_after();
+            const int64_t grow = T.bh * (int64_t)p.N + (int64_t)T.i * BQ + r;
+            const bool row_live = T.i * BQ + r < p.N;  // ragged N: the last block's rows past N
+            float alpha = 1.0f, l = 1.0f;
+            uint32_t cq[64];  // c phi(Q)_r as packed bf16 pairs (the lin MMA's A row)
+            uint4 htr[16];    // Htot row f = r (bf16)
             if (T.linear) {
-                // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
-                V2_WAIT(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
-                const uint32_t hb = smem_u32(sV(hcs));
-                const float* ht = p.htot32 + T.bh * D * D + (int64_t)r * D;
+                // loads in flight first: Htot row r and phi(Q) row r (global / L2)
+                const uint4* ht = reinterpret_cast<const uint4*>(p.htot16 + (T.bh * D + r) * D);
 #pragma unroll
-                for (int c0 = 0; c0 < 128; c0 += 32) {
-                    uint32_t hs[32];
-                    tmem_ld32(tmem + lane_base + TM_H + c0, hs);
-                    float4 tv[8];
+                for (int u = 0; u < 16; ++u) htr[u] = ht[u];
+                const uint4* pq = reinterpret_cast<const uint4*>(p.phiq + grow * D);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) tv[u] = *reinterpret_cast<const float4*>(ht + c0 + 4 * u);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        const int c = c0 + ch * 8;
-                        const float* t8 = reinterpret_cast<const float*>(&tv[2 * ch]);
-                        uint32_t o4[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            o4[e] = pack_bf16(t8[2 * e] - __uint_as_float(hs[ch * 8 + 2 * e]),
-                                              t8[2 * e + 1] - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
-                        st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), o4[0], o4[1], o4[2], o4[3]);
-                    }
+                for (int u = 0; u < 16; ++u) {
+                    const uint4 w = row_live ? pq[u] : make_uint4(0u, 0u, 0u, 0u);
+                    cq[4 * u] = w.x;
+                    cq[4 * u + 1] = w.y;
+                    cq[4 * u + 2] = w.z;
+                    cq[4 * u + 3] = w.w;
                 }
-            }
-            tc_fence_before();
-            mbar_arrive(&bar_h_free);
-            V2_WAIT(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
-            const float l = sL[pb][r];
-            float alpha = 1.0f;
-            if (T.linear) {
                 // alpha = sigmoid(rho_i) with the reference's clamp (attention.hpp:17-22)
                 const float x = p.rho[(int64_t)(T.bh % p.H) * p.tm + T.i];
                 float a = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf_glibc(-x)));
                 alpha = fminf(fmaxf(a, 1.17549435e-38f), 1.0f - 5.9604645e-08f);
                 V2_WAIT(&bar_zc_ready[pb], (uint32_t)((k >> 1) & 1));
-                V2_WAIT(&bar_pq_full[pb], (uint32_t)((k >> 1) & 1));
-                // den = phi(Q)_r . Zc from the bf16 phi(Q) the MMA reads, then phi(Q)_r *= c
-                const uint32_t qb = smem_u32(sQ(pb));
-                uint32_t w[64];
-                float d4[4] = {0.f, 0.f, 0.f, 0.f};
+                if (r == 0) V2_TR(k, 29);
+                float d4[4] = {0.f, 0.f, 0.f, 0.f};  // den = phi(Q)_r . Zc (the bf16 phi(Q) the MMA uses)
 #pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    ld_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), w[4 * ch], w[4 * ch + 1],
-                                 w[4 * ch + 2], w[4 * ch + 3]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[4 * ch + e]));
-                        const int f = ch * 8 + 2 * e;
-                        d4[e] = fmaf(f2.y, sZc[pb][f + 1], fmaf(f2.x, sZc[pb][f], d4[e]));
-                    }
+                for (int e = 0; e < 64; ++e) {
+                    const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cq[e]));
+                    d4[e & 3] = fmaf(f2.y, sZc[pb][2 * e + 1], fmaf(f2.x, sZc[pb][2 * e], d4[e & 3]));
                 }
                 const float den = (d4[0] + d4[1]) + (d4[2] + d4[3]);
-                const bool live = T.i * BQ + r < p.N && den > 0.0f;
-                const float c = live ? (1.0f - alpha) * l / (alpha * den) : 0.0f;
+                V2_WAIT(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
+                if (r == 0) V2_TR(k, 31);
+                l = sL[pb][r];
+                const float c = (row_live && den > 0.0f) ? (1.0f - alpha) * l / (alpha * den) : 0.0f;
 #pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    uint32_t o4[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[4 * ch + e]));
-                        o4[e] = pack_bf16(f2.x * c, f2.y * c);
-                    }
-                    st_shared_v4(qb + (ch >> 3) * 16384 + sw128_off(r, (ch & 7) * 8), o4[0], o4[1], o4[2], o4[3]);
+                for (int e = 0; e < 64; ++e) {
+                    const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cq[e]));
+                    cq[e] = pack_bf16(f2.x * c, f2.y * c);
                 }
-                fence_proxy_async_smem();  // the scaled phi(Q) and Hc are read by the async proxy
+            } else {
+                V2_WAIT(&bar_sm_done[pb], (uint32_t)((k >> 1) & 1));
+                l = sL[pb][r];
             }
             mbar_arrive(&bar_zc_free[pb]);
+            V2_WAIT(&bar_tile_done, (uint32_t)(k & 1));  // every PV / phi(K~)^T V of the tile
+            __syncwarp();
+            tc_fence_after();
+            if (r == 0) V2_TR(k, 17);
+            if (T.linear) {
+                // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
+                V2_WAIT(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
+                const uint32_t hb = smem_u32(sV(hcs));
+#pragma unroll
+                for (int c0 = 0; c0 < 128; c0 += 32) {
+                    uint32_t hs[32];
+                    tmem_ld32(tmem + lane_base + TM_H + c0, hs);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const int c = c0 + ch * 8;
+                        const uint32_t* t8 = reinterpret_cast<const uint32_t*>(&htr[c >> 3]);
+                        uint32_t o4[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t8[e]));
+                            o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
+                                              tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
+                        }
+                        st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), o4[0], o4[1], o4[2], o4[3]);
+                    }
+                }
+                // c phi(Q)_r into this lane's first 64 Hsel columns: the lin MMA's TMEM A operand
+                tmem_st32(tmem + lane_base + TM_H, *reinterpret_cast<uint32_t(*)[32]>(&cq[0]));
+                tmem_st32(tmem + lane_base + TM_H + 32, *reinterpret_cast<uint32_t(*)[32]>(&cq[32]));
+                tmem_st_wait();
+                fence_proxy_async_smem();  // Hc is read by the async proxy
+            }
+            tc_fence_before();
             mbar_arrive(&bar_lin_ready);
+            if (r == 0) V2_TR(k, 19);
             V2_WAIT(&bar_lin_done, (uint32_t)(k & 1));
             __syncwarp();
             tc_fence_after();
-            // out = alpha / l * O, bf16 into the tile's Q buffer (SW128), one TMA store
+            if (r == 0) V2_TR(k, 20);
+            // out = alpha / l * O straight to global (row r: 256 contiguous bytes)
             const float sc = alpha / l;
-            const uint32_t ob = smem_u32(sQ(pb));
+            uint4* orow = reinterpret_cast<uint4*>(p.out + grow * D);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t o[64];
@@ -602,30 +639,23 @@ __global__ void __launch_bounds__(384, 1)
                 if (half == 1) {
                     tc_fence_before();
                     mbar_arrive(&bar_o_free);  // the next tile's first PV may overwrite O
+                    if (r == 0) V2_TR(k, 21);
                 }
+                if (row_live) {
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
-                    st_shared_v4(ob + half * 16384 + sw128_off(r, ch * 8),
-                                 pack_bf16(__uint_as_float(o[ch * 8 + 0]) * sc, __uint_as_float(o[ch * 8 + 1]) * sc),
-                                 pack_bf16(__uint_as_float(o[ch * 8 + 2]) * sc, __uint_as_float(o[ch * 8 + 3]) * sc),
-                                 pack_bf16(__uint_as_float(o[ch * 8 + 4]) * sc, __uint_as_float(o[ch * 8 + 5]) * sc),
-                                 pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
+                    for (int ch = 0; ch < 8; ++ch)
+                        orow[half * 8 + ch] =
+                            make_uint4(pack_bf16(__uint_as_float(o[ch * 8 + 0]) * sc, __uint_as_float(o[ch * 8 + 1]) * sc),
+                                       pack_bf16(__uint_as_float(o[ch * 8 + 2]) * sc, __uint_as_float(o[ch * 8 + 3]) * sc),
+                                       pack_bf16(__uint_as_float(o[ch * 8 + 4]) * sc, __uint_as_float(o[ch * 8 + 5]) * sc),
+                                       pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
+                }
             }
-            fence_proxy_async_smem();
-            named_bar_sync(1, 128);
             if (r == 0) {
-                const int orow0 = T.i * BQ, hz = (int)T.bh;  // rows past N (ragged tail) are dropped
-                tma_store_3d(&tmO, 0, orow0, hz, sQ(pb));
-                tma_store_3d(&tmO, 0, orow0 + 64, hz, sQ(pb) + 8192);
-                tma_store_3d(&tmO, 64, orow0, hz, sQ(pb) + 16384);
-                tma_store_3d(&tmO, 64, orow0 + 64, hz, sQ(pb) + 24576);
-                tma_store_commit();
-                tma_store_wait_read();
-                mbar_arrive(&bar_q_empty[pb]);   // Q of tile k+2 may land here
-                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring
+                V2_TR(k, 22);
+                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring (the lin MMA is done)
             }
         }
-        if (r == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -637,7 +667,7 @@ __global__ void __launch_bounds__(384, 1)
 
 bool sparse_v2_eligible(const SparseLaunch& a) {
     return !a.dense && a.bq == 128 && a.bk == 64 && a.d == 128 && a.o_s == nullptr && a.o_l == nullptr &&
-           a.big_l == nullptr && a.h_blocks == nullptr && a.z_blocks == nullptr && a.tm_phiq != nullptr;
+           a.big_l == nullptr && a.h_blocks == nullptr && a.z_blocks == nullptr && a.phiq != nullptr;
 }
 
 cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launches) {
@@ -649,7 +679,9 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
     p.rho = a.rho;
     p.ztot = a.ztot;
     p.zblk = a.zblk;
-    p.htot32 = a.htot;
+    p.htot16 = (const __nv_bfloat16*)a.htot16;
+    p.phiq = (const __nv_bfloat16*)a.phiq;
+    p.out = (__nv_bfloat16*)a.out;
     p.N = a.N;
     p.H = (int)a.H;
     p.tm = a.tm;
@@ -657,14 +689,17 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
     p.ntiles = (int)(a.B * a.H) * a.tm;
     p.last_valid = a.N - (a.tn - 1) * v2::BK;
     p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
+#ifdef SLA2_TRACE
+    extern unsigned long long* g_trace_buf;
+    p.trace = g_trace_buf;
+#endif
     cudaError_t e = ensure_smem_attr((const void*)sla2_sparse_v2_kernel, (int)v2::SMEM_ALLOC);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = p.ntiles < sms ? p.ntiles : sms;
-    sla2_sparse_v2_kernel<<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v, *a.tm_phik,
-                                                                      *a.tm_phiq, *a.tm_out, p);
+    sla2_sparse_v2_kernel<<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v, *a.tm_phik, p);
     ++*launches;
     return cudaGetLastError();
 }
