@@ -638,6 +638,10 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             ia.tm_kc = &mkc;
             ia.tm_vct = &mvc;
             SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
+#ifdef SLA2_V3  // experiment build: make variant NAME=v3 DEFS=-DSLA2_V3
+        } else if (sparse_v3_eligible(sa)) {
+            SLA2_CUDA_TRY(launch_sparse_v3(sa, st, &g_launches));
+#endif
         } else if (sparse_v2_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
         } else {

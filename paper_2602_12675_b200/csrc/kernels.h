@@ -134,6 +134,9 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
 // persistent variant (sparse_v2.cu): the non-saved, non-dense bf16 path
 bool sparse_v2_eligible(const SparseLaunch& a);
 cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launches);
+// persistent variant with 8 softmax warps and double-buffered S (sparse_v3.cu)
+bool sparse_v3_eligible(const SparseLaunch& a);
+cudaError_t launch_sparse_v3(const SparseLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_sparse_f32(const SparseLaunch& a, cudaStream_t st, int* launches);
 size_t sparse_f32_smem_bytes(int d, int bq, int bk);
 

@@ -138,8 +138,9 @@ def test_soft_topk_errors(cuda):
         sla2.soft_topk(pc, k_percent=50.0, tau=1e-15)
     with pytest.raises(sla2.NumericError):  # tau must be positive (router.hpp:131)
         sla2.soft_topk(pc, k_percent=50.0, tau=0.0)
-    with pytest.raises(sla2.ShapeError):
-        sla2.soft_topk(pc, k_percent=0.0, tau=0.1)
+    # no k_percent range check: topk_budget clamps to kappa = 1 (router.hpp:36-40, 130-133)
+    v, _ = sla2.soft_topk(pc, k_percent=0.0, tau=0.1)
+    assert abs(float(v.sum()) - 1.0) < 1e-5
 
 
 @needs_ref
