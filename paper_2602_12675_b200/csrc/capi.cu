@@ -248,6 +248,7 @@ struct Workspace {
     float* htot;
     void* htot16;
     void* phiq;  // bf16 non-QAT path: phi(Q) rows, TMA-loaded by the sparse kernel
+    void* ol;    // bf16 non-QAT path: the linear branch's O_l rows (sparse_fa.cu), [BH][N][d]
     int8_t *qc, *kc, *vct;
     float *qs, *ks, *vs;
     int32_t* cnt;
@@ -273,6 +274,7 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.htot = c.take<float>(g.BH * g.d * g.d);
     t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
     t.phiq = (g.bf16 && !g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
+    t.ol = (g.bf16 && !g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
@@ -594,6 +596,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.tm_phiq = w.phiq ? &mpq : nullptr;
         sa.phiq = w.phiq;
         sa.tm_out = &mo;
+        sa.ol = w.ol;
         if (g.quant) {
             // INT8 QAT (QuantConfig, quant.hpp:15-19): per-tile codes + scales, then the kind::i8 kernel
             QuantLaunch qa{};
@@ -641,6 +644,10 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
 #ifdef SLA2_V3  // experiment build: make variant NAME=v3 DEFS=-DSLA2_V3
         } else if (sparse_v3_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v3(sa, st, &g_launches));
+#endif
+#ifdef SLA2_FA_SPARSE  // experiment build: the split linear-branch + two-lane attention forward
+        } else if (sparse_fa_eligible(sa)) {
+            SLA2_CUDA_TRY(launch_sparse_fa(sa, st, &g_launches));
 #endif
         } else if (sparse_v2_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
@@ -991,6 +998,10 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
     sa.tm_v = &mv;
     sa.tm_phik = &mk;
     sa.tm_out = &mo;
+    if (sparse_fa_eligible(sa)) {  // the two-query-block tcgen05 attention kernel (sparse_fa.cu)
+        SLA2_CUDA_TRY(launch_sparse_fa(sa, (cudaStream_t)stream, &g_launches));
+        return SLA2_OK;
+    }
     SLA2_CUDA_TRY(launch_sparse_bf16(sa, (cudaStream_t)stream, &g_launches));
     return SLA2_OK;
 }

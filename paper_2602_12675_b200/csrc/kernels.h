@@ -124,6 +124,7 @@ struct SparseLaunch {
     const CUtensorMap* tm_phiq;  // phi(Q) bf16 as [BH*N][d] (launch_phiq), box 64 x 64, SW128
     const void* phiq;            // the same phi(Q) rows (bf16 [BH][N][d])
     const CUtensorMap* tm_out;   // out bf16 as [BH*N][d], box 64 x 64, SW128 (TMA-stored blocks)
+    void* ol;                    // bf16 [BH][N][d] scratch: the linear branch's O_l (sparse_fa.cu)
     // f32 path
     const float* q;
     const float* k;
@@ -137,6 +138,10 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
 // persistent variant with 8 softmax warps and double-buffered S (sparse_v3.cu)
 bool sparse_v3_eligible(const SparseLaunch& a);
 cudaError_t launch_sparse_v3(const SparseLaunch& a, cudaStream_t st, int* launches);
+// split forward (sparse_fa.cu): linear-branch kernel (O_l) + two-query-block attention kernel;
+// also the dense mode (full_attention)
+bool sparse_fa_eligible(const SparseLaunch& a);
+cudaError_t launch_sparse_fa(const SparseLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_sparse_f32(const SparseLaunch& a, cudaStream_t st, int* launches);
 size_t sparse_f32_smem_bytes(int d, int bq, int bk);
 

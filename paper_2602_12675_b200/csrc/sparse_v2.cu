@@ -238,68 +238,73 @@ __global__ void __launch_bounds__(384, 1)
     // 3 x 168, the CTA's launch allocation (setmaxnreg.inc can only take what .dec released)
     if (warp < 4) {
         reg_dealloc<72>();
-        if (warp == 0 && lane == 0) {
-            // ============ TMA producer: Q (two buffers), K pairs, phi(Q) over the tile's Q ============
-            tma_prefetch_desc(&tmQ);
-            tma_prefetch_desc(&tmK);
+        if (warp == 0) {
+            // ============ TMA producer: Q (two buffers), K pairs ============
+            // one box per lane: bulk-tensor copies issued by one thread complete one after another
+            if (lane == 0) {
+                tma_prefetch_desc(&tmQ);
+                tma_prefetch_desc(&tmK);
+            }
             const uint64_t pol = policy_evict_last();
-            auto load_q = [&](const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int qrow, int hz) {
-                mbar_arrive_expect_tx(bar, Q_BYTES);
-                tma_load_3d(dst, map, 0, qrow, hz, bar);
-                tma_load_3d(dst + 8192, map, 0, qrow + 64, hz, bar);
-                tma_load_3d(dst + 16384, map, 64, qrow, hz, bar);
-                tma_load_3d(dst + 24576, map, 64, qrow + 64, hz, bar);
+            auto load_q = [&](uint64_t* bar, uint8_t* dst, int qrow, int hz) {
+                if (lane == 0) mbar_arrive_expect_tx(bar, Q_BYTES);
+                __syncwarp();
+                if (lane < 4) tma_load_3d(dst + lane * 8192, &tmQ, (lane >> 1) * 64, qrow + (lane & 1) * 64, hz, bar);
             };
             int64_t gk = 0;
             int t = blockIdx.x;
             if (t < nt) {
                 const V2Tile T0 = v2_tile(p, t);
-                load_q(&tmQ, &bar_q_full[0], sQ(0), T0.i * BQ, (int)T0.bh);
+                load_q(&bar_q_full[0], sQ(0), T0.i * BQ, (int)T0.bh);
             }
             for (int k = 0; t < nt; ++k, t += G) {
                 const V2Tile T = v2_tile(p, t);
-                const int pb = k & 1;
                 for (int n = 0; n < T.npair; ++n, ++gk) {
                     const int s = (int)(gk % NKP);
-                    if (gk >= NKP) V2_WAIT(&bar_k_empty[s], (uint32_t)(((gk / NKP) - 1) & 1));
                     const int cnt = min(2, T.nb - 2 * n);
-                    mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
-                    for (int b = 0; b < cnt; ++b) {
+                    if (lane == 0) {
+                        if (gk >= NKP) V2_WAIT(&bar_k_empty[s], (uint32_t)(((gk / NKP) - 1) & 1));
+                        mbar_arrive_expect_tx(&bar_k_full[s], cnt * TILE_BYTES);
+                    }
+                    __syncwarp();
+                    if (lane < 2 * cnt) {  // lane = (block b, 64-column half c)
+                        const int b = lane >> 1, c = lane & 1;
                         const int krow = T.idx[2 * n + b] * BK;
-                        tma_load_3d_hint(sKp(s) + b * 8192, &tmK, 0, krow, (int)T.bh, &bar_k_full[s], pol);
-                        tma_load_3d_hint(sKp(s) + 16384 + b * 8192, &tmK, 64, krow, (int)T.bh, &bar_k_full[s], pol);
+                        tma_load_3d_hint(sKp(s) + c * 16384 + b * 8192, &tmK, c * 64, krow, (int)T.bh, &bar_k_full[s], pol);
                     }
                 }
                 // Q of the next tile into the other buffer, free once tile k-1's last Q K^T read it
                 if (t + G < nt) {
                     const V2Tile T1 = v2_tile(p, t + G);
                     const int k1 = k + 1;
-                    if (k1 >= 2) V2_WAIT(&bar_qk_done[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
-                    load_q(&tmQ, &bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
+                    if (lane == 0 && k1 >= 2) V2_WAIT(&bar_qk_done[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
+                    load_q(&bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
                 }
             }
-        } else if (warp == 2 && lane == 0) {
+        } else if (warp == 2) {
             // ============ TMA producer: V / phi(K~) ring; one slot per tile for the epilogue's Hc ============
-            tma_prefetch_desc(&tmV);
-            tma_prefetch_desc(&tmPhi);
+            if (lane == 0) {
+                tma_prefetch_desc(&tmV);
+                tma_prefetch_desc(&tmPhi);
+            }
             const uint64_t pol = policy_evict_last();
             int64_t gv = 0;
             for (int t = blockIdx.x; t < nt; t += G) {
                 const V2Tile T = v2_tile(p, t);
                 for (int j = 0; j <= T.nb; ++j, ++gv) {
                     const int s = (int)(gv % NSV);
-                    if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
-                    if (j == T.nb) {  // the Hc slot: allocated, not loaded
-                        mbar_arrive(&bar_v_full[s]);
-                        continue;
+                    if (lane == 0) {
+                        if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
+                        if (j == T.nb)  // the Hc slot: allocated, not loaded
+                            mbar_arrive(&bar_v_full[s]);
+                        else
+                            mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
                     }
-                    const int krow = T.idx[j] * BK, hz = (int)T.bh;
-                    mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
-                    tma_load_3d_hint(sV(s), &tmV, 0, krow, hz, &bar_v_full[s], pol);
-                    tma_load_3d_hint(sV(s) + 8192, &tmV, 64, krow, hz, &bar_v_full[s], pol);
-                    if (T.linear) {
-                        tma_load_3d_hint(sV(s) + TILE_BYTES, &tmPhi, 0, krow, hz, &bar_v_full[s], pol);
-                        tma_load_3d_hint(sV(s) + TILE_BYTES + 8192, &tmPhi, 64, krow, hz, &bar_v_full[s], pol);
+                    __syncwarp();
+                    if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
+                        const int krow = T.idx[j] * BK, hz = (int)T.bh, c = lane & 1;
+                        tma_load_3d_hint(sV(s) + (lane >> 1) * TILE_BYTES + c * 8192, lane < 2 ? &tmV : &tmPhi, c * 64, krow,
+                                         hz, &bar_v_full[s], pol);
                     }
                 }
             }

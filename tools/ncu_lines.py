@@ -14,7 +14,12 @@ n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kern],
                      capture_output=True, text=True).stdout
 lines = txt.splitlines()
-rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
+# one block per profiled launch ("Kernel Name" line, header, rows): INST picks the launch
+starts = [k for k, ln in enumerate(lines) if ln.startswith('"Kernel Name"')] or [0]
+inst = int(os.environ.get("INST", "0"))
+lo = starts[inst]
+hi = starts[inst + 1] if inst + 1 < len(starts) else len(lines)
+rows = list(csv.reader(io.StringIO("\n".join(lines[lo + 1:hi]))))
 h = rows[0]
 ix = {k: i for i, k in enumerate(h)}
 body = [r for r in rows[1:] if len(r) == len(h)]
