@@ -247,8 +247,8 @@ struct Workspace {
     float* hpart;
     float* htot;
     void* htot16;
-    void* phiq;  // bf16 non-QAT path: phi(Q) rows, TMA-loaded by the sparse kernel
-    void* ol;    // bf16 non-QAT path: the linear branch's O_l rows (sparse_fa.cu), [BH][N][d]
+    void* phiq;  // bf16 path: phi(Q) rows, TMA-loaded by the sparse kernel
+    void* ol;    // bf16 path: the linear branch's O_l rows (sparse_fa.cu), [BH][N][d]
     int8_t *qc, *kc, *vct;
     float *qs, *ks, *vs;
     int32_t* cnt;
@@ -273,8 +273,8 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.hpart = c.take<float>(g.BH * g.nchunk * g.d * g.d);
     t.htot = c.take<float>(g.BH * g.d * g.d);
     t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
-    t.phiq = (g.bf16 && !g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
-    t.ol = (g.bf16 && !g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
+    t.phiq = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
+    t.ol = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
@@ -471,6 +471,7 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 //   between run on st right after the fork (the router's back half)
 struct LinPlan {
     cudaEvent_t dep = nullptr;
+    cudaEvent_t qv_codes = nullptr;  // QAT: Q and V codes were quantized on a side stream (done at this event)
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
     float* kbar = nullptr;
@@ -619,7 +620,13 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             qa.ks = w.ks;
             qa.vct = w.vct;
             qa.vs = w.vs;
-            SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+            if (plan.qv_codes) {  // Q / V codes are being made beside the router: K~ codes (need mu) only
+                qa.which = 2;
+                SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+                SLA2_CUDA_TRY(cudaStreamWaitEvent(st, plan.qv_codes, 0));
+            } else {
+                SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+            }
             // the INT8 kernel addresses its bf16 tiles with 2-D [B*H*N][d] maps (N divisible)
             CUtensorMap mq2, mv2, mphi2;
             if (!make_map(&mq2, q, rows, g.d, 64, 64, 2) || !make_map(&mv2, v, rows, g.d, 64, 64, 2) ||
@@ -640,7 +647,10 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
             ia.tm_qc = &mqc;
             ia.tm_kc = &mkc;
             ia.tm_vct = &mvc;
-            SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
+            if (attn_i8_eligible(ia))
+                SLA2_CUDA_TRY(launch_attn_i8(ia, &mphi, &mv, st, &g_launches));
+            else
+                SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
 #ifdef SLA2_V3  // experiment build: make variant NAME=v3 DEFS=-DSLA2_V3
         } else if (sparse_v3_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v3(sa, st, &g_launches));
@@ -766,6 +776,36 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
         // and the router need).
         ra.phiq_out = w.phiq;
         LinPlan plan;
+        if (g.quant) {
+            // QAT: the Q and V codes do not depend on mu; quantize them on a low-priority side
+            // stream beside the router (the K~ codes follow mu in run_linear_and_sparse)
+            cudaStream_t qs = aux_stream(3, -1);
+            cudaEvent_t ev0 = aux_event(13), ev_qv = aux_event(14);
+            SLA2_CUDA_TRY(cudaEventRecord(ev0, st));
+            SLA2_CUDA_TRY(cudaStreamWaitEvent(qs, ev0, 0));
+            QuantLaunch qa{};
+            qa.B = g.B;
+            qa.H = g.H;
+            qa.N = (int)g.N;
+            qa.d = (int)g.d;
+            qa.bq = (int)g.bq;
+            qa.bk = (int)g.bk;
+            qa.tm = (int)g.tm;
+            qa.tn = (int)g.tn;
+            qa.q = q;
+            qa.k = k;
+            qa.v = v;
+            qa.qc = w.qc;
+            qa.qs = w.qs;
+            qa.kc = w.kc;
+            qa.ks = w.ks;
+            qa.vct = w.vct;
+            qa.vs = w.vs;
+            qa.which = 1 | 4;
+            SLA2_CUDA_TRY(launch_quant_prep(qa, qs, &g_launches));
+            SLA2_CUDA_TRY(cudaEventRecord(ev_qv, qs));
+            plan.qv_codes = ev_qv;
+        }
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;
         plan.phiq_ready = w.phiq != nullptr;

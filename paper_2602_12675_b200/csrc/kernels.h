@@ -142,6 +142,8 @@ cudaError_t launch_sparse_v3(const SparseLaunch& a, cudaStream_t st, int* launch
 // also the dense mode (full_attention)
 bool sparse_fa_eligible(const SparseLaunch& a);
 cudaError_t launch_sparse_fa(const SparseLaunch& a, cudaStream_t st, int* launches);
+// the linear branch alone: O_l = phi(Q) Hc / (phi(Q) . Zc) per query block into a.ol (bf16)
+cudaError_t launch_linsel(const SparseLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_sparse_f32(const SparseLaunch& a, cudaStream_t st, int* launches);
 size_t sparse_f32_smem_bytes(int d, int bq, int bk);
 
@@ -160,6 +162,7 @@ struct QuantLaunch {
     float* ks;      // [BH][tn]
     int8_t* vct;    // [BH][N][d] V codes per key block (row-major, the PV MMA's MN-major B tile)
     float* vs;      // [BH][tn]
+    int which = 7;  // tensors to quantize: 1 = Q, 2 = K~, 4 = V
 };
 cudaError_t launch_quant_prep(const QuantLaunch& a, cudaStream_t st, int* launches);
 struct SparseI8Launch {
@@ -175,6 +178,11 @@ struct SparseI8Launch {
     const CUtensorMap* tm_vct;  // [BH*N][d] int8, box 128 x 64
 };
 cudaError_t launch_sparse_i8(const SparseI8Launch& a, cudaStream_t st, int* launches);
+// two-query-block INT8 attention (attn_i8.cu) after the bf16 linear-branch kernel; tm_phik3 /
+// tm_v3 are the 3-D [BH][N][d] maps the linear-branch kernel reads
+bool attn_i8_eligible(const SparseI8Launch& a);
+cudaError_t launch_attn_i8(const SparseI8Launch& a, const CUtensorMap* tm_phik3, const CUtensorMap* tm_v3,
+                           cudaStream_t st, int* launches);
 
 // ---- backward (backward.cu): sla2_backward, hard routing, fp32, d / bq / bk <= 64
 struct BackwardLaunch {

@@ -33,58 +33,94 @@ __device__ __forceinline__ int8_t quant_code(float x, float inv) {
     return (int8_t)(int)r;
 }
 
-// Codes + scale of one [rows x d] bf16 tile (rows = 64 or 128): block absmax, then codes.
-// kind: 0 = Q (block bq), 1 = K~ (block bk, K - mu), 2 = V (block bk).
-__global__ void __launch_bounds__(256) quant_prep_kernel(const __nv_bfloat16* __restrict__ q,
-                                                         const __nv_bfloat16* __restrict__ k,
-                                                         const __nv_bfloat16* __restrict__ v,
-                                                         const float* __restrict__ mu, int N, int d, int bq, int bk,
-                                                         int8_t* __restrict__ qc, float* __restrict__ qs,
-                                                         int8_t* __restrict__ kc, float* __restrict__ ks,
-                                                         int8_t* __restrict__ vc, float* __restrict__ vs) {
-    const int kind = blockIdx.z;
-    const int64_t bh = blockIdx.y;
-    const int blk = blockIdx.x;
-    const int rows = kind == 0 ? bq : bk;
-    const int nblk = N / rows;
-    if (blk >= nblk) return;
-    const __nv_bfloat16* src = (kind == 0 ? q : kind == 1 ? k : v) + (bh * N + (int64_t)blk * rows) * d;
-    int8_t* dst = (kind == 0 ? qc : kind == 1 ? kc : vc) + (bh * N + (int64_t)blk * rows) * d;
-    float* scale_out = (kind == 0 ? qs : kind == 1 ? ks : vs) + bh * nblk + blk;
-    const float* m = (kind == 1 && mu) ? mu + bh * d : nullptr;
+// Codes + scale of one [rows x 128] bf16 tile (rows = 64 or 128): block absmax, then codes.
+// kind: 0 = Q (block bq), 1 = K~ (block bk, K - mu), 2 = V (block bk). 16-byte loads, the tile
+// held in registers between the absmax and the codes (one read of the input).
+template <int ROWS>
+__device__ __forceinline__ void quant_tile(const __nv_bfloat16* __restrict__ src, const float* __restrict__ m,
+                                           int8_t* __restrict__ dst, float* __restrict__ scale_out) {
+    constexpr int IT = ROWS * 128 / 8 / 256;  // uint4 per thread
     __shared__ float red[8];
-    const int n = rows * d;
+    float x[IT][8];
     float amax = 0.0f;
-    for (int e = threadIdx.x; e < n; e += 256) {
-        float x = __bfloat162float(src[e]);
-        if (m) x = __fsub_rn(x, m[e % d]);
-        amax = fmaxf(amax, fabsf(x));
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        const int v = threadIdx.x + u * 256;  // uint4 index: row v / 16, columns (v % 16) * 8 ..
+        const uint4 w = reinterpret_cast<const uint4*>(src)[v];
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ww[e]));
+            x[u][2 * e] = f.x;
+            x[u][2 * e + 1] = f.y;
+        }
+        if (m) {
+            const int c0 = (v & 15) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[u][e] = __fsub_rn(x[u][e], m[c0 + e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) amax = fmaxf(amax, fabsf(x[u][e]));
     }
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
     __syncthreads();
     amax = red[0];
+#pragma unroll
     for (int w = 1; w < 8; ++w) amax = fmaxf(amax, red[w]);
-    if (amax == 0.0f) {
-        for (int e = threadIdx.x; e < n; e += 256) dst[e] = 0;
-        if (threadIdx.x == 0) *scale_out = 1.17549435e-38f;  // numeric_limits<float>::min()
-        return;
-    }
-    const float scale = __fdiv_rn(amax, 127.0f);
-    const float inv = __fdiv_rn(1.0f, scale);
-    for (int e = threadIdx.x; e < n; e += 256) {
-        float x = __bfloat162float(src[e]);
-        if (m) x = __fsub_rn(x, m[e % d]);
-        dst[e] = quant_code(x, inv);
+    const float scale = amax == 0.0f ? 1.17549435e-38f : __fdiv_rn(amax, 127.0f);  // all-zero: FLT_MIN
+    const float inv = amax == 0.0f ? 0.0f : __fdiv_rn(1.0f, scale);
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            lo |= (uint32_t)(uint8_t)quant_code(x[u][e], inv) << (8 * e);
+            hi |= (uint32_t)(uint8_t)quant_code(x[u][4 + e], inv) << (8 * e);
+        }
+        reinterpret_cast<uint2*>(dst)[threadIdx.x + u * 256] = make_uint2(lo, hi);
     }
     if (threadIdx.x == 0) *scale_out = scale;
 }
 
+__global__ void __launch_bounds__(256) quant_prep_kernel(const __nv_bfloat16* __restrict__ q,
+                                                         const __nv_bfloat16* __restrict__ k,
+                                                         const __nv_bfloat16* __restrict__ v,
+                                                         const float* __restrict__ mu, int N, int bq, int bk,
+                                                         int which, int8_t* __restrict__ qc, float* __restrict__ qs,
+                                                         int8_t* __restrict__ kc, float* __restrict__ ks,
+                                                         int8_t* __restrict__ vc, float* __restrict__ vs) {
+    constexpr int d = 128;
+    // blockIdx.x enumerates the head's tiles of the selected tensors in the order Q, K~, V
+    const int64_t bh = blockIdx.y;
+    int blk = blockIdx.x, kind = -1;
+    for (int kk = 0; kk < 3 && kind < 0; ++kk) {
+        if (!(which & (1 << kk))) continue;
+        const int n = N / (kk == 0 ? bq : bk);
+        if (blk < n)
+            kind = kk;
+        else
+            blk -= n;
+    }
+    const int rows = kind == 0 ? bq : bk, nblk = N / rows;
+    const __nv_bfloat16* src = (kind == 0 ? q : kind == 1 ? k : v) + (bh * N + (int64_t)blk * rows) * d;
+    int8_t* dst = (kind == 0 ? qc : kind == 1 ? kc : vc) + (bh * N + (int64_t)blk * rows) * d;
+    float* scale_out = (kind == 0 ? qs : kind == 1 ? ks : vs) + bh * nblk + blk;
+    const float* m = (kind == 1 && mu) ? mu + bh * d : nullptr;
+    if (rows == 128)
+        quant_tile<128>(src, m, dst, scale_out);
+    else
+        quant_tile<64>(src, m, dst, scale_out);
+}
+
 cudaError_t launch_quant_prep(const QuantLaunch& a, cudaStream_t st, int* launches) {
-    const int maxblk = a.N / (a.bq < a.bk ? a.bq : a.bk);
-    quant_prep_kernel<<<dim3(maxblk, (unsigned)(a.B * a.H), 3), 256, 0, st>>>(
+    if (a.d != 128 || (a.bq != 64 && a.bq != 128) || (a.bk != 64 && a.bk != 128)) return cudaErrorInvalidValue;
+    const int which = a.which ? a.which : 7;
+    const int per_head =
+        ((which & 1) ? a.N / a.bq : 0) + ((which & 2) ? a.N / a.bk : 0) + ((which & 4) ? a.N / a.bk : 0);
+    quant_prep_kernel<<<dim3(per_head, (unsigned)(a.B * a.H)), 256, 0, st>>>(
         (const __nv_bfloat16*)a.q, (const __nv_bfloat16*)a.k, (const __nv_bfloat16*)a.v, a.smooth ? a.mu : nullptr,
-        a.N, a.d, a.bq, a.bk, a.qc, a.qs, a.kc, a.ks, a.vct, a.vs);
+        a.N, a.bq, a.bk, which, a.qc, a.qs, a.kc, a.ks, a.vct, a.vs);
     ++*launches;
     return cudaGetLastError();
 }
@@ -206,43 +242,46 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sHc = smem + OFF_V;  // 32 KB epilogue alias of the V stages (free after the loop)
 
     if (warp == 0) {
-        if (lane == 0) {  // Q codes + Q bf16, K~ code ring
-            const uint64_t pol = policy_evict_last();
-            const int qrow = (int)(bh * p.N + (int64_t)i * BQ);
-            mbar_arrive_expect_tx(&bar_q, QC_BYTES + Q_BYTES);
-            tma_load_2d(sQc, &tmQc, 0, qrow, &bar_q);
-            tma_load_2d(sQ, &tmQ, 0, qrow, &bar_q);
-            tma_load_2d(sQ + 8192, &tmQ, 0, qrow + 64, &bar_q);
-            tma_load_2d(sQ + 16384, &tmQ, 64, qrow, &bar_q);
-            tma_load_2d(sQ + 24576, &tmQ, 64, qrow + 64, &bar_q);
-            for (int j = 0; j < nb; ++j) {
-                const int s = j % NSK;
+        // Q codes + Q bf16, K~ code ring; one box per lane (bulk-tensor copies issued by one
+        // thread complete one after another)
+        const uint64_t pol = policy_evict_last();
+        const int qrow = (int)(bh * p.N + (int64_t)i * BQ);
+        if (lane == 0) mbar_arrive_expect_tx(&bar_q, QC_BYTES + Q_BYTES);
+        __syncwarp();
+        if (lane == 0) tma_load_2d(sQc, &tmQc, 0, qrow, &bar_q);
+        if (lane >= 1 && lane < 5) {
+            const int u = lane - 1;
+            tma_load_2d(sQ + u * 8192, &tmQ, (u >> 1) * 64, qrow + (u & 1) * 64, &bar_q);
+        }
+        for (int j = 0; j < nb; ++j) {
+            const int s = j % NSK;
+            if (lane == 0) {
                 if (j >= NSK) mbar_wait(&bar_k_empty[s], ((j / NSK) - 1) & 1);
-                const int krow = (int)(bh * p.N + (int64_t)idx[j] * BK);
                 mbar_arrive_expect_tx(&bar_k_full[s], KC_BYTES);
+                const int krow = (int)(bh * p.N + (int64_t)idx[j] * BK);
                 tma_load_2d_hint(sKc(s), &tmKc, 0, krow, &bar_k_full[s], pol);
             }
         }
     } else if (warp == 2) {
-        if (lane == 0) {  // V codes, V bf16, phi(K) ring; Htot
-            const uint64_t pol = policy_evict_last();
-            for (int j = 0; j < nb; ++j) {
-                const int s = j % NSV;
+        // V codes, V bf16, phi(K) ring; Htot -- one box per lane
+        const uint64_t pol = policy_evict_last();
+        for (int j = 0; j < nb; ++j) {
+            const int s = j % NSV;
+            if (lane == 0) {
                 if (j >= NSV) mbar_wait(&bar_v_empty[s], ((j / NSV) - 1) & 1);
-                const int krow = (int)(bh * p.N + (int64_t)idx[j] * BK);
                 mbar_arrive_expect_tx(&bar_v_full[s], linear ? VST_BYTES : VC_BYTES);
-                tma_load_2d_hint(sVc(s), &tmVc, 0, krow, &bar_v_full[s], pol);
-                if (linear) {
-                    tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol);
-                    tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol);
-                    tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol);
-                    tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol);
-                }
-                if (j == 0 && linear) {
-                    mbar_arrive_expect_tx(&bar_ht, HT_BYTES);
-                    tma_load_2d_hint(sHt, &tmHt, 0, (int)(bh * D), &bar_ht, pol);
-                    tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol);
-                }
+                if (j == 0 && linear) mbar_arrive_expect_tx(&bar_ht, HT_BYTES);
+            }
+            __syncwarp();
+            const int krow = (int)(bh * p.N + (int64_t)idx[j] * BK);
+            if (lane == 0) tma_load_2d_hint(sVc(s), &tmVc, 0, krow, &bar_v_full[s], pol);
+            if (linear) {
+                if (lane == 1) tma_load_2d_hint(sV(s), &tmV, 0, krow, &bar_v_full[s], pol);
+                if (lane == 2) tma_load_2d_hint(sV(s) + 8192, &tmV, 64, krow, &bar_v_full[s], pol);
+                if (lane == 3) tma_load_2d_hint(sPh(s), &tmPhi, 0, krow, &bar_v_full[s], pol);
+                if (lane == 4) tma_load_2d_hint(sPh(s) + 8192, &tmPhi, 64, krow, &bar_v_full[s], pol);
+                if (j == 0 && lane == 5) tma_load_2d_hint(sHt, &tmHt, 0, (int)(bh * D), &bar_ht, pol);
+                if (j == 0 && lane == 6) tma_load_2d_hint(sHt + 16384, &tmHt, 64, (int)(bh * D), &bar_ht, pol);
             }
         }
     } else if (warp == 1) {

@@ -779,30 +779,36 @@ bool sparse_fa_eligible(const SparseLaunch& a) {
            (a.dense || (a.phiq != nullptr && a.tm_phiq != nullptr && a.ol != nullptr));
 }
 
+cudaError_t launch_linsel(const SparseLaunch& a, cudaStream_t st, int* launches) {
+    LinSelParams lp;
+    lp.kv_idx = a.kv_idx;
+    lp.kv_cnt = a.kv_cnt;
+    lp.kstride = a.kstride;
+    lp.kappa = a.kappa;
+    lp.ztot = a.ztot;
+    lp.zblk = a.zblk;
+    lp.htot = a.htot;
+    lp.ol = (__nv_bfloat16*)a.ol;
+    lp.N = a.N;
+    lp.tm = a.tm;
+    lp.tn = a.tn;
+    lp.ntiles = (int)(a.B * a.H) * a.tm;
+    cudaError_t e = ensure_smem_attr((const void*)sla2_linsel_kernel, (int)fa::LS_SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    sla2_linsel_kernel<<<lp.ntiles < sms ? lp.ntiles : sms, 256, fa::LS_SMEM, st>>>(*a.tm_phiq, *a.tm_phik, *a.tm_v,
+                                                                                    lp);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sparse_fa(const SparseLaunch& a, cudaStream_t st, int* launches) {
     const int ntiles = (int)(a.B * a.H) * a.tm;
     if (!a.dense) {
-        LinSelParams lp;
-        lp.kv_idx = a.kv_idx;
-        lp.kv_cnt = a.kv_cnt;
-        lp.kstride = a.kstride;
-        lp.kappa = a.kappa;
-        lp.ztot = a.ztot;
-        lp.zblk = a.zblk;
-        lp.htot = a.htot;
-        lp.ol = (__nv_bfloat16*)a.ol;
-        lp.N = a.N;
-        lp.tm = a.tm;
-        lp.tn = a.tn;
-        lp.ntiles = ntiles;
-        cudaError_t e = ensure_smem_attr((const void*)sla2_linsel_kernel, (int)fa::LS_SMEM);
+        const cudaError_t e = launch_linsel(a, st, launches);
         if (e != cudaSuccess) return e;
-        int dev0 = 0, sms0 = 148;
-        cudaGetDevice(&dev0);
-        cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
-        sla2_linsel_kernel<<<ntiles < sms0 ? ntiles : sms0, 256, fa::LS_SMEM, st>>>(*a.tm_phiq, *a.tm_phik, *a.tm_v, lp);
-        ++*launches;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     AttnParams p;
     p.kv_idx = a.dense ? nullptr : a.kv_idx;
