@@ -460,11 +460,13 @@ def main():
     except Exception:
         pass
     if c["quant"]:
-        # QK^T and PV run on tcgen05 kind::i8 (K = 32 per instruction at the kind::f16 issue
-        # rate, tools/mb_umma.cu): the denominator is twice the measured bf16 burst
-        kern, peak, peak_src = "sla2_sparse_i8_kernel", 2 * pk_["bf16"], pk_["src"] + " bf16 burst x 2 (kind::i8)"
+        # the QAT stage: K~ codes (quant_prep_kernel), the bf16 linear branch (sla2_linsel_kernel)
+        # and the INT8 softmax branch (sla2_attn_i8_kernel: QK^T and PV on tcgen05 kind::i8, K = 32
+        # per instruction at the kind::f16 issue rate, tools/mb_umma.cu -> twice the bf16 peak)
+        kern = "quant_prep_kernel (K~ codes) + sla2_linsel_kernel + sla2_attn_i8_kernel"
+        peak, peak_src = 2 * pk_["bf16"], pk_["src"] + " bf16 burst x 2 (kind::i8)"
     elif c["bf16"]:
-        kern, peak, peak_src = "sla2_sparse_bf16_kernel", pk_["bf16"], pk_["src"] + " burst bf16 (MEASURED_PEAKS.json)"
+        kern, peak, peak_src = "sla2_sparse_v2_kernel", pk_["bf16"], pk_["src"] + " burst bf16 (MEASURED_PEAKS.json)"
     else:
         kern, peak, peak_src = "sla2_sparse_f32_kernel", pk_["bf16"], pk_["src"] + " burst bf16 (MEASURED_PEAKS.json)"
     roofline = {"bound": "tensor", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -519,7 +519,9 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
     if (plan.kprep) {
         cudaEvent_t ev_k = aux_event(10);
         // fork at mu: phi(K~), z_j and Htot on the linear stream, beside the router's pooled
-        // keys (launch_kpool, below) and back half on st
+        // keys (launch_kpool, below) and back half on st. Forking after the pooled keys instead
+        // was measured slower (the router's back half loses more to the concurrent precompute
+        // than the pooled keys gain: 0.622 vs 0.619 ms at cfg2)
         la.phik_ready = !(la.tm_k && la.mu);  // the fused kernel computes phi(K~) itself
         SLA2_CUDA_TRY(cudaEventRecord(ev_k, st));
         dep = ev_k;
