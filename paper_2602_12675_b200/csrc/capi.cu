@@ -274,7 +274,11 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.htot = c.take<float>(g.BH * g.d * g.d);
     t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
     t.phiq = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
+#ifdef SLA2_FA_SPARSE
     t.ol = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
+#else
+    t.ol = (g.bf16 && g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;  // QAT: linear-branch O_l
+#endif
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
