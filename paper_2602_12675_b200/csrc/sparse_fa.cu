@@ -381,6 +381,8 @@ struct AttnParams {
     int N, H, tm, tn, ntiles;
     int last_valid;  // keys in the last (possibly partial) key block
     int dense;
+    int pair_kv;  // dense mode, tm even: the lanes take query blocks 2u and 2u + 1 of one head and
+                  // share one K / V ring (same key blocks, half the L2 traffic, twice the depth)
     float scale_log2;
 #ifdef SLA2_TRACE
     unsigned long long* trace;  // [grid][2 lanes][32 steps][16 events] %globaltimer (analysis build)
@@ -422,7 +424,7 @@ __device__ __forceinline__ FaTile fa_tile(const AttnParams& p, int t) {
 __device__ __forceinline__ int fa_block(const FaTile& T, int j) { return T.idx ? T.idx[j] : j; }
 // lane X's k-th query block of this CTA (or -1)
 __device__ __forceinline__ int fa_lane_tile(const AttnParams& p, int x, int k) {
-    const int t = blockIdx.x + (2 * k + x) * (int)gridDim.x;
+    const int t = p.pair_kv ? 2 * (blockIdx.x + k * (int)gridDim.x) + x : blockIdx.x + (2 * k + x) * (int)gridDim.x;
     return t < p.ntiles ? t : -1;
 }
 
@@ -475,11 +477,11 @@ __global__ void __launch_bounds__(512, 1)
             mbar_init(&bar_l_free[x], 4);
             for (int s = 0; s < NK; ++s) {
                 mbar_init(&bar_k_full[x][s], 1);
-                mbar_init(&bar_k_empty[x][s], 1);
+                mbar_init(&bar_k_empty[x][s], p.pair_kv ? 2 : 1);  // shared ring: both issuers release
             }
             for (int s = 0; s < NV; ++s) {
                 mbar_init(&bar_v_full[x][s], 1);
-                mbar_init(&bar_v_empty[x][s], 1);
+                mbar_init(&bar_v_empty[x][s], p.pair_kv ? 2 : 1);
             }
         }
         fence_barrier_init();
@@ -505,8 +507,15 @@ __global__ void __launch_bounds__(512, 1)
             }
             const uint64_t pol = policy_evict_last();
             uint8_t* dq = smem + AT_OFF_Q + x * Q_BYTES;
-            uint8_t* dk = smem + AT_OFF_K + x * NK * TILE_BYTES;
-            uint8_t* dv = smem + AT_OFF_V + x * NV * TILE_BYTES;
+            // shared K / V ring (pair_kv): lane A's producer fills both lanes' slots, lane B's loads Q only
+            const bool kv = !p.pair_kv || x == 0;
+            const int nk = p.pair_kv ? 2 * NK : NK, nv = p.pair_kv ? 2 * NV : NV;
+            uint8_t* dk = smem + AT_OFF_K + (p.pair_kv ? 0 : x * NK * TILE_BYTES);
+            uint8_t* dv = smem + AT_OFF_V + (p.pair_kv ? 0 : x * NV * TILE_BYTES);
+            uint64_t* kfull = p.pair_kv ? &bar_k_full[0][0] : bar_k_full[x];
+            uint64_t* kempty = p.pair_kv ? &bar_k_empty[0][0] : bar_k_empty[x];
+            uint64_t* vfull = p.pair_kv ? &bar_v_full[0][0] : bar_v_full[x];
+            uint64_t* vempty = p.pair_kv ? &bar_v_empty[0][0] : bar_v_empty[x];
             int g = 0;
             for (int k = 0;; ++k) {
                 const int t = fa_lane_tile(p, x, k);
@@ -519,22 +528,21 @@ __global__ void __launch_bounds__(512, 1)
                 __syncwarp();
                 if (lane < 4)
                     tma_load_3d(dq + lane * 8192, &tmQ, (lane >> 1) * 64, T.i * BQ + (lane & 1) * 64, T.bh, &bar_q_full[x]);
-                for (int j = 0; j < T.nb; ++j, ++g) {
+                for (int j = 0; j < T.nb && kv; ++j, ++g) {
                     const int krow = fa_block(T, j) * BK;
-                    const int sk = g % NK, sv = g % NV;
+                    const int sk = g % nk, sv = g % nv;
                     if (lane == 0) {
-                        if (g >= NK) FA_WAIT(&bar_k_empty[x][sk], (uint32_t)(((g / NK) - 1) & 1));
-                        mbar_arrive_expect_tx(&bar_k_full[x][sk], TILE_BYTES);
-                        if (g >= NV) FA_WAIT(&bar_v_empty[x][sv], (uint32_t)(((g / NV) - 1) & 1));
-                        mbar_arrive_expect_tx(&bar_v_full[x][sv], TILE_BYTES);
+                        if (g >= nk) FA_WAIT(&kempty[sk], (uint32_t)(((g / nk) - 1) & 1));
+                        mbar_arrive_expect_tx(&kfull[sk], TILE_BYTES);
+                        if (g >= nv) FA_WAIT(&vempty[sv], (uint32_t)(((g / nv) - 1) & 1));
+                        mbar_arrive_expect_tx(&vfull[sv], TILE_BYTES);
                     }
                     __syncwarp();
                     if (lane < 2)
-                        tma_load_3d_hint(dk + sk * TILE_BYTES + lane * 8192, &tmK, lane * 64, krow, T.bh,
-                                         &bar_k_full[x][sk], pol);
+                        tma_load_3d_hint(dk + sk * TILE_BYTES + lane * 8192, &tmK, lane * 64, krow, T.bh, &kfull[sk], pol);
                     else if (lane < 4)
                         tma_load_3d_hint(dv + sv * TILE_BYTES + (lane - 2) * 8192, &tmV, (lane - 2) * 64, krow, T.bh,
-                                         &bar_v_full[x][sv], pol);
+                                         &vfull[sv], pol);
                 }
             }
         } else if (warp == 1 || warp == 2) {
@@ -548,16 +556,21 @@ __global__ void __launch_bounds__(512, 1)
             const uint32_t tl = warp_uniform(tmem) + (uint32_t)x * 256;  // lane x: S0 | S1 | O
             const uint32_t sb = warp_uniform(sbase);
             const uint64_t dQ = sdesc_sw128(sb + AT_OFF_Q + x * Q_BYTES, 16, 1024);
-            const uint64_t dK0 = sdesc_sw128(sb + AT_OFF_K + x * NK * TILE_BYTES, 16, 1024);
-            const uint64_t dV0 = sdesc_sw128(sb + AT_OFF_V + x * NV * TILE_BYTES, 8192, 1024);
+            const int nk = p.pair_kv ? 2 * NK : NK, nv = p.pair_kv ? 2 * NV : NV;
+            const uint64_t dK0 = sdesc_sw128(sb + AT_OFF_K + (p.pair_kv ? 0 : x * NK * TILE_BYTES), 16, 1024);
+            const uint64_t dV0 = sdesc_sw128(sb + AT_OFF_V + (p.pair_kv ? 0 : x * NV * TILE_BYTES), 8192, 1024);
+            uint64_t* kfull = p.pair_kv ? &bar_k_full[0][0] : bar_k_full[x];
+            uint64_t* kempty = p.pair_kv ? &bar_k_empty[0][0] : bar_k_empty[x];
+            uint64_t* vfull = p.pair_kv ? &bar_v_full[0][0] : bar_v_full[x];
+            uint64_t* vempty = p.pair_kv ? &bar_v_empty[0][0] : bar_v_empty[x];
             FaCursor cq, cp;
             fa_cur_init(cq, p, x);
             fa_cur_init(cp, p, x);
             int gq = 0, gp = 0;  // Q K^T / P V issued
             auto issue_qk = [&]() {
-                const int g = gq, sk = g % NK;
+                const int g = gq, sk = g % nk;
                 if (cq.j == 0) FA_WAIT(&bar_q_full[x], (uint32_t)(cq.k & 1));
-                FA_WAIT(&bar_k_full[x][sk], (uint32_t)((g / NK) & 1));
+                FA_WAIT(&kfull[sk], (uint32_t)((g / nk) & 1));
                 tc_fence_after();
                 const uint64_t dK = dK0 + (uint64_t)((sk * TILE_BYTES) >> 4);
                 const uint32_t tS = tl + (uint32_t)(g & 1) * 64;
@@ -567,17 +580,17 @@ __global__ void __launch_bounds__(512, 1)
                                    dK + (((ks >> 2) * 8192 + (ks & 3) * 32) >> 4), ID_QK, ks > 0);
                 umma_commit_w(&bar_s_full[x][g & 1]);
                 if (lane == 0) FA_TR(x, g, 0);
-                umma_commit_w(&bar_k_empty[x][sk]);
+                umma_commit_w(&kempty[sk]);
                 if (cq.j == cq.T.nb - 1) umma_commit_w(&bar_q_free[x]);
                 ++gq;
                 fa_cur_next(cq, p, x);
             };
             auto issue_pv = [&]() {
-                const int g = gp, sv = g % NV;
+                const int g = gp, sv = g % nv;
                 FA_WAIT(&bar_p_full[x][g & 1], (uint32_t)((g >> 1) & 1));
                 if (lane == 0) FA_TR(x, g, 7);
                 if (cp.j == 0 && cp.k >= 1) FA_WAIT(&bar_o_free[x], (uint32_t)((cp.k - 1) & 1));
-                FA_WAIT(&bar_v_full[x][sv], (uint32_t)((g / NV) & 1));
+                FA_WAIT(&vfull[sv], (uint32_t)((g / nv) & 1));
                 tc_fence_after();
                 const uint64_t dV = dV0 + (uint64_t)((sv * TILE_BYTES) >> 4);
                 const uint32_t tP = tl + (uint32_t)(g & 1) * 64;
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(512, 1)
                     umma_bf16_ts_w(tl + 128, tP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (cp.j > 0 || ks > 0));
                 umma_commit_w(&bar_pv_done[x]);
                 if (lane == 0) FA_TR(x, g, 1);
-                umma_commit_w(&bar_v_empty[x][sv]);
+                umma_commit_w(&vempty[sv]);
                 if (cp.j == cp.T.nb - 1) umma_commit_w(&bar_o_ready[x]);
                 ++gp;
                 fa_cur_next(cp, p, x);
@@ -825,6 +838,7 @@ cudaError_t launch_sparse_fa(const SparseLaunch& a, cudaStream_t st, int* launch
     p.ntiles = ntiles;
     p.last_valid = a.N - (a.tn - 1) * fa::BK;
     p.dense = a.dense;
+    p.pair_kv = a.dense && (a.tm % 2 == 0);
     p.scale_log2 = a.inv_sqrt_d * 1.4426950408889634f;
 #ifdef SLA2_TRACE
     extern unsigned long long* g_trace_buf;
