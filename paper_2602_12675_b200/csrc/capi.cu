@@ -665,6 +665,10 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         } else if (sparse_fa_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_fa(sa, st, &g_launches));
 #endif
+#ifdef SLA2_V4  // experiment build until measured: make variant NAME=v4 DEFS=-DSLA2_V4
+        } else if (sparse_v4_eligible(sa)) {
+            SLA2_CUDA_TRY(launch_sparse_v4(sa, st, &g_launches));
+#endif
         } else if (sparse_v2_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
         } else {

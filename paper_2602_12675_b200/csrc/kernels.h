@@ -137,6 +137,9 @@ bool sparse_v2_eligible(const SparseLaunch& a);
 cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launches);
 // persistent variant with 8 softmax warps and double-buffered S (sparse_v3.cu)
 bool sparse_v3_eligible(const SparseLaunch& a);
+// persistent variant with 64-key steps, two S buffers and two O accumulators (sparse_v4.cu)
+bool sparse_v4_eligible(const SparseLaunch& a);
+cudaError_t launch_sparse_v4(const SparseLaunch& a, cudaStream_t st, int* launches);
 cudaError_t launch_sparse_v3(const SparseLaunch& a, cudaStream_t st, int* launches);
 // split forward (sparse_fa.cu): linear-branch kernel (O_l) + two-query-block attention kernel;
 // also the dense mode (full_attention)
