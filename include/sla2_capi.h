@@ -185,7 +185,8 @@ sla2_status sla2_dense_fwd(const sla2_fwd_params* p, const void* q, const void* 
  * fp32 q, k, v, d_out [B,H,N,d]; the routing mask [B,H,tm,tn] (u8, every row keeps a block);
  * rho [H,tm]; the forward's saved o_s, o_l [B,H,N,d] and big_l [B,H,N] (sla2_forward with
  * `saved`). Writes dq, dk, dv [B,H,N,d] and drho [B,H,tm] (per (b,h); sum over b for the
- * shared per-head logits). params: dtype SLA2_F32, d <= 64, bq <= 64, bk <= 64, N divisible,
+ * shared per-head logits). params: dtype SLA2_F32, d <= 128, bk <= 64, bq <= 64 or a multiple
+ * of 64 (<= 128 when d > 64: the Wan2.1 block shape d = 128, bq = 128, bk = 64), N divisible,
  * tm <= 1024; smooth as in the forward. SoftMask routing (stage 1) is not on this path.
  * The workspace is sla2_backward_workspace_size(p) bytes.
  */

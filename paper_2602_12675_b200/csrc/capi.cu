@@ -1064,8 +1064,10 @@ static sla2_status check_backward(const sla2_fwd_params* p) {
         return fail(SLA2_CONTRACT_ERROR, "sla2_backward: fp32 tensors (the backward is full precision, SPEC.md:358)");
     if (p->N % p->bq != 0 || p->N % p->bk != 0)
         return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");  // attention.hpp:39-41
-    if (p->d > 64 || p->bq > 64 || p->bk > 64 || p->N / p->bq > 1024)
-        return fail(SLA2_CONTRACT_ERROR, "sla2_backward: d, bq, bk <= 64 and tm <= 1024 on this path");
+    if (p->d > 128 || p->bk > 64 || (p->bq > 64 && (p->bq % 64 != 0 || (p->d > 64 && p->bq > 128))) ||
+        p->N / p->bq > 1024)
+        return fail(SLA2_CONTRACT_ERROR,
+                    "sla2_backward: d <= 128, bk <= 64, bq <= 64 or a multiple of 64 (<= 128 when d > 64), tm <= 1024");
     return SLA2_OK;
 }
 

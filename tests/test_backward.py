@@ -42,7 +42,11 @@ def test_reference_backward_binding_cpu():
 @pytest.mark.parametrize("N,H,d,bq,bk,kp,smooth,seed", [(1024, 2, 64, 64, 64, 25.0, True, 1),
                                                          (512, 1, 64, 32, 64, 10.0, True, 2),
                                                          (512, 1, 32, 64, 32, 30.0, False, 3),
-                                                         (256, 1, 64, 64, 64, 100.0, True, 4)])
+                                                         (256, 1, 64, 64, 64, 100.0, True, 4),
+                                                         # the Wan2.1 block shape (d = 128, bq = 128, bk = 64)
+                                                         (1024, 1, 128, 128, 64, 10.0, True, 5),
+                                                         (512, 2, 128, 128, 64, 25.0, False, 6),
+                                                         (512, 1, 96, 64, 32, 20.0, True, 7)])
 def test_backward_vs_reference(cuda, N, H, d, bq, bk, kp, smooth, seed):
     import torch
     from sla2_testlib import make_inputs, to_dev
@@ -68,11 +72,16 @@ def test_backward_vs_reference(cuda, N, H, d, bq, bk, kp, smooth, seed):
 @pytest.mark.gpu
 def test_backward_contract(cuda):
     import torch
-    x = torch.zeros((1, 1, 256, 128), device=cuda)
-    m = torch.ones((1, 1, 4, 4), dtype=torch.uint8, device=cuda)
-    with pytest.raises(sla2.ContractError):  # d = 128 > 64 on this path
-        sla2.sla2_backward(x, x, x, x, torch.zeros((1, 4), device=cuda), m,
+    x = torch.zeros((1, 1, 512, 256), device=cuda)
+    m = torch.ones((1, 1, 8, 8), dtype=torch.uint8, device=cuda)
+    with pytest.raises(sla2.ContractError):  # d = 256 > 128 on this path
+        sla2.sla2_backward(x, x, x, x, torch.zeros((1, 8), device=cuda), m,
                            {"o_s": x, "o_l": x, "big_l": x[..., 0].contiguous()}, bq=64, bk=64)
+    x = torch.zeros((1, 1, 512, 128), device=cuda)
+    m = torch.ones((1, 1, 2, 4), dtype=torch.uint8, device=cuda)
+    with pytest.raises(sla2.ContractError):  # bq = 256 > 128 with d > 64
+        sla2.sla2_backward(x, x, x, x, torch.zeros((1, 2), device=cuda), m,
+                           {"o_s": x, "o_l": x, "big_l": x[..., 0].contiguous()}, bq=256, bk=128)
 
 
 def _bwd_goldens():

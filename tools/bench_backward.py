@@ -16,7 +16,9 @@ import paper_2602_12675_b200 as sla2  # noqa: E402
 
 
 def main():
-    B, H, N, d, bq, bk, kp = 1, 2, int(os.environ.get("N", "4096")), 64, 64, 64, 10.0
+    B, H, N = 1, 2, int(os.environ.get("N", "4096"))
+    d, bq, bk = int(os.environ.get("D", "64")), int(os.environ.get("BQ", "64")), int(os.environ.get("BK", "64"))
+    kp = float(os.environ.get("KP", "10.0"))
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(0)
     q, k, v, dout = (torch.randn((B, H, N, d), generator=g, device=dev) for _ in range(4))
