@@ -303,7 +303,7 @@ inline std::pair<Matrix<T>, SLA2ForwardSaved<T>> forward_impl(const AttentionInp
     return {std::move(out), std::move(saved)};
 }
 
-// The device backward (sla2_backward C ABI: hard routing, fp32, d, bq, bk <= 64) on request; the
+// The device backward (sla2_backward C ABI: hard routing, fp32, d <= 128, bk <= 64, bq <= 64 or 128) on request; the
 // reference's own sla2_backward stays in place for everything else.
 template <class T>
 inline SLA2Gradients<T> backward_hard(const SLA2ForwardSaved<T>& saved, const AttentionInputs<T>& inputs,

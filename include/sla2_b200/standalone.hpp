@@ -488,7 +488,7 @@ struct SLA2Gradients {
 };
 
 // sla2_backward on the hard-routing path (the stage-2 / QAT fine-tuning backward): full
-// precision on the device from the forward's saved O_s, O_l, L and the mask. d, bq, bk <= 64.
+// precision on the device from the forward's saved O_s, O_l, L and the mask. d <= 128, bk <= 64, bq <= 64 or 128.
 inline SLA2Gradients<float> sla2_backward(const SLA2ForwardSaved<float>& saved, const AttentionInputs<float>& inputs,
                                           const MixRatio<float>& alpha, const Matrix<float>& d_out) {
     inputs.validate();

@@ -7,7 +7,7 @@ dq, dk, dv and drho; the router projections are constants of the node (hard top-
 gradient into them by construction, tape.hpp:260-262). `SLA2Attention` is the per-head layer
 of model.hpp:265-268 (router projections and mixing logits per head).
 
-The device backward is the fp32 path (d, bq, bk <= 64): this node takes fp32 tensors."""
+The device backward is the fp32 path (d <= 128, bk <= 64, bq <= 64 or 128): this node takes fp32 tensors."""
 from __future__ import annotations
 
 import torch
