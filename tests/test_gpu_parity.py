@@ -295,3 +295,20 @@ def test_gpu_vs_reference_golden(cuda, path):
         assert rel_err(got, g["out"])[0] <= BF16_TOL
     else:
         assert np.abs(got - g["out"]).max() <= F32_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,N", [(1, 2, 2048),   # tm even: the two lanes share one K / V ring
+                                   (1, 3, 1920),   # tm odd: independent lanes
+                                   (2, 1, 1000),   # ragged N (partial last query and key blocks)
+                                   (1, 1, 130),    # fewer query blocks than lanes on one SM
+                                   (1, 5, 640)])   # more CTAs' worth of lanes than query blocks per head
+def test_dense_attention_kernel_vs_sdpa(cuda, B, H, N):
+    """full_attention (attention.hpp:71-75) on the two-query-block tcgen05 kernel (sparse_fa.cu,
+    dense mode) against fp32 SDPA on the same bf16 inputs: within 1e-2 normwise."""
+    import torch
+    g = torch.Generator(device=cuda).manual_seed(N + H)
+    q, k, v = (torch.randn((B, H, N, 128), generator=g, device=cuda).to(torch.bfloat16) for _ in range(3))
+    o = sla2.full_attention(q, k, v).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
+    assert ((o - ref).abs().max() / ref.abs().max()).item() <= 1e-2
