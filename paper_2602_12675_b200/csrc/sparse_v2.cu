@@ -508,22 +508,24 @@ __global__ void __launch_bounds__(384, 1)
                     tc_fence_after();
                 }
                 const uint32_t pbase = tmem + lane_base + TM_P + b * 64;
-                float rs0 = 0.0f, rs1 = 0.0f;
+                const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m2, -m2);
+                float2 rs = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int blk = 0; blk < 2; ++blk) {
                     if (blk == 1 && !two) break;
                     uint32_t w[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const float p0 = v2_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e]), p.scale_log2, -m2));
-                        const float p1 = v2_exp2(fmaf(__uint_as_float(sr[blk * 64 + 2 * e + 1]), p.scale_log2, -m2));
-                        rs0 += p0;
-                        rs1 += p1;
-                        w[e] = pack_bf16(p0, p1);
+                    for (int e = 0; e < 32; ++e) {  // packed FFMA2 / FADD2 (half the issue of scalar)
+                        const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[blk * 64 + 2 * e]),
+                                                                 __uint_as_float(sr[blk * 64 + 2 * e + 1])),
+                                                     sc2, nm2);
+                        const float2 pe = make_float2(v2_exp2(x2.x), v2_exp2(x2.y));
+                        rs = __fadd2_rn(rs, pe);
+                        w[e] = pack_bf16(pe.x, pe.y);
                     }
                     tmem_st32(pbase + blk * 32, w);
                 }
-                l += rs0 + rs1;
+                l += rs.x + rs.y;
                 if (n == npair - 1) sL[k & 1][r] = l;  // before the last P: the epilogue's 1 / l
                 tmem_st_wait();
                 tc_fence_before();
