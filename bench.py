@@ -75,7 +75,18 @@ def peaks():
 
 
 def eff_flops(c):
-    return 4.0 * c["N"] ** 2 * c["d"] * c["B"] * c["H"]
+    # the paper's effective FLOPs, 4 N^2 d per head = flops_full (accounting.hpp:39-45)
+    from paper_2602_12675_b200.accounting import GeometryConfig, flops_full
+    return flops_full(GeometryConfig(c["N"], c["d"], c["B"] * c["H"], 1, 1))
+
+
+def flops_model(c, kappa, tn, ms):
+    """The reference's analytic SLA2 cost at the kept fraction (flops_sla2, accounting.hpp:47-77)."""
+    from paper_2602_12675_b200.accounting import GeometryConfig, flops_sla2
+    r = flops_sla2(GeometryConfig(c["N"], c["d"], c["B"] * c["H"], 1, 1), 1.0 - kappa / tn, c["bq"], c["bk"])
+    return {"source": "flops_sla2 (accounting.hpp:47-77) at sparsity 1 - kappa / tn", "full": r.full,
+            "sparse_branch": r.sparse_branch, "linear_branch": r.linear_branch, "router": r.router,
+            "total": r.total, "savings": r.savings, "tflops_on_model_total": r.total / (ms * 1e-3) / 1e12}
 
 
 def geometry(c):
@@ -542,7 +553,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
             "stages_ms": {"router": st_med[0], "linear_prep": st_med[1], "sparse_kernel": sparse_ms,
                           "total": st_med[3]},
-            "timeline_ms": timeline,
+            "timeline_ms": timeline, "flops_model": flops_model(c, kappa, tn, ms_per_step),
             "wall_s_timed_region": wall, **extra}
     print(json.dumps(line), flush=True)
     if world > 1:
