@@ -38,7 +38,7 @@ namespace sla2dev {
 
 namespace v2 {
 constexpr int BQ = 128, BK = 64, D = 128;
-constexpr int NKP = 2, NSV = 3;                // K pair ring, V / phi(K~) ring (one slot per tile holds Hc)
+constexpr int NKP = 2, NSV = 3;                // K pair ring, V / phi(K~) ring
 constexpr uint32_t Q_BYTES = BQ * D * 2;       // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;    // 16 KB
 constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // a K pair
@@ -164,15 +164,17 @@ __device__ __forceinline__ void v2_issue_qk(uint64_t* s_free, uint64_t* k_full, 
     umma_commit_w(&k_empty[s]);
 }
 // O += (c phi(Q)) Hc of tile kk once the epilogue has built both operands: A = c phi(Q) rows in
-// the first 64 Hsel columns of TMEM (TS), B = Hc (MN-major) in the tile's Hc slot. The tile's
-// Hsel was read before, and the next tile's phi(K~)^T V MMAs follow this one in the tensor pipe.
-__device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_done, int kk, bool linear, int hc,
+// the first 64 Hsel columns of TMEM (TS), B = Hc (MN-major) over the tile's own Q buffer (free
+// after its last Q K^T; the next Q it takes waits for this MMA, lin_done). Keeping Hc out of the
+// V / phi(K~) ring lets the next tile's first key blocks load without waiting for this MMA. The
+// tile's Hsel was read before, and the next tile's phi(K~)^T V MMAs follow this one in the pipe.
+__device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_done, int kk, bool linear,
                                            uint32_t sbase, uint32_t tm) {
     using namespace v2;
     V2_WAIT(lin_ready, (uint32_t)(kk & 1));
     tc_fence_after();
     if (linear) {
-        const uint64_t dB = sdesc_sw128(sbase + OFF_V + hc * VS_BYTES, 16384, 1024);
+        const uint64_t dB = sdesc_sw128(sbase + OFF_Q + (kk & 1) * Q_BYTES, 16384, 1024);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
             umma_bf16_ts_w(tm + TM_O, tm + TM_H + ks * 8, dB + ((ks * 2048) >> 4), idesc_bf16(128, 128, false, true), 1);
@@ -273,11 +275,12 @@ __global__ void __launch_bounds__(384, 1)
                         tma_load_3d_hint(sKp(s) + c * 16384 + b * 8192, &tmK, c * 64, krow, (int)T.bh, &bar_k_full[s], pol);
                     }
                 }
-                // Q of the next tile into the other buffer, free once tile k-1's last Q K^T read it
+                // Q of the next tile into the other buffer, which held tile k-1's Q and then its Hc: free
+                // once tile k-1's linear-branch MMA has read it
                 if (t + G < nt) {
                     const V2Tile T1 = v2_tile(p, t + G);
                     const int k1 = k + 1;
-                    if (lane == 0 && k1 >= 2) V2_WAIT(&bar_qk_done[k1 & 1], (uint32_t)(((k1 >> 1) - 1) & 1));
+                    if (lane == 0 && k1 >= 2) V2_WAIT(&bar_lin_done, (uint32_t)((k1 - 2) & 1));
                     load_q(&bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
                 }
             }
@@ -291,17 +294,14 @@ __global__ void __launch_bounds__(384, 1)
             int64_t gv = 0;
             for (int t = blockIdx.x; t < nt; t += G) {
                 const V2Tile T = v2_tile(p, t);
-                for (int j = 0; j <= T.nb; ++j, ++gv) {
+                for (int j = 0; j < T.nb; ++j, ++gv) {
                     const int s = (int)(gv % NSV);
                     if (lane == 0) {
                         if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
-                        if (j == T.nb)  // the Hc slot: allocated, not loaded
-                            mbar_arrive(&bar_v_full[s]);
-                        else
-                            mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
+                        mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
                     }
                     __syncwarp();
-                    if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
+                    if (lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
                         const int krow = T.idx[j] * BK, hz = (int)T.bh, c = lane & 1;
                         tma_load_3d_hint(sV(s) + (lane >> 1) * TILE_BYTES + c * 8192, lane < 2 ? &tmV : &tmPhi, c * 64, krow,
                                          hz, &bar_v_full[s], pol);
@@ -322,7 +322,6 @@ __global__ void __launch_bounds__(384, 1)
             int g = 0, gv = 0;  // global pair / V-slot counters (< 2^31 per CTA)
             int k = 0;
             bool prev_linear = false;
-            int prev_hc = 0;
             for (int t = blockIdx.x; t < nt; t += G, ++k) {
                 const V2Tile T = v2_tile(p, t);
                 const int nbu = (int)warp_uniform((uint32_t)T.nb);
@@ -341,7 +340,7 @@ __global__ void __launch_bounds__(384, 1)
                         if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
                     }
                     if (n == 0 && k > 0)  // tile k-1's linear term, before PV(0)
-                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
+                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, sbase, tm);
                     V2_WAIT(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
                     tc_fence_after();
                     if (n == 0 && k > 0) {
@@ -379,11 +378,9 @@ __global__ void __launch_bounds__(384, 1)
                 if (lane == 0) V2_TR(k, 28);
                 g += npu;
                 gv += nbu;
-                prev_hc = gv % NSV;  // the tile's Hc slot
-                gv += 1;
                 prev_linear = lin;
             }
-            if (k > 0) v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
+            if (k > 0) v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, sbase, tm);
         } else if (warp == 3) {
             // ============ Zc = Ztot - sum_sel z_j per tile (the linear denominators) ============
             int k = 0;
@@ -540,14 +537,10 @@ __global__ void __launch_bounds__(384, 1)
         // ============ epilogue of tile k (thread = row r), one tile behind the softmax ============
         const int r = threadIdx.x - 256;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        int gv = 0;
         int k = 0;
         for (int t = blockIdx.x; t < nt; t += G, ++k) {
             const V2Tile T = v2_tile(p, t);
             const int pb = k & 1;
-            const int vhc = gv + T.nb;  // the tile's Hc slot
-            const int hcs = vhc % NSV;
-            gv = vhc + 1;
             const int64_t grow = T.bh * (int64_t)p.N + (int64_t)T.i * BQ + r;
             const bool row_live = T.i * BQ + r < p.N;  // ragged N: the last block's rows past N
             float alpha = 1.0f, l = 1.0f;
@@ -600,8 +593,7 @@ __global__ void __launch_bounds__(384, 1)
             if (r == 0) V2_TR(k, 17);
             if (T.linear) {
                 // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
-                V2_WAIT(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
-                const uint32_t hb = smem_u32(sV(hcs));
+                const uint32_t hb = smem_u32(sQ(pb));  // the tile's Q buffer: its Q K^T are done (tile_done)
 #pragma unroll
                 for (int c0 = 0; c0 < 128; c0 += 32) {
                     uint32_t hs[32];
@@ -658,10 +650,7 @@ __global__ void __launch_bounds__(384, 1)
                                        pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
                 }
             }
-            if (r == 0) {
-                V2_TR(k, 22);
-                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring (the lin MMA is done)
-            }
+            if (r == 0) V2_TR(k, 22);
         }
     }
     tc_fence_before();
