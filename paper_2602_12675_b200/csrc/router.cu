@@ -482,10 +482,13 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const float x = u == 0 ? xv[a].x : u == 1 ? xv[a].y : u == 2 ? xv[a].z : xv[a].w;
-                acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(x, pv[u].x));
-                acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(x, pv[u].y));
-                acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(x, pv[u].z));
-                acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(x, pv[u].w));
+                const float2 x2 = make_float2(x, x);  // packed FMUL2 products, scalar FADD sums
+                const float2 p01 = __fmul2_rn(x2, make_float2(pv[u].x, pv[u].y));
+                const float2 p23 = __fmul2_rn(x2, make_float2(pv[u].z, pv[u].w));
+                acc[a][0] = __fadd_rn(acc[a][0], p01.x);
+                acc[a][1] = __fadd_rn(acc[a][1], p01.y);
+                acc[a][2] = __fadd_rn(acc[a][2], p23.x);
+                acc[a][3] = __fadd_rn(acc[a][3], p23.y);
             }
         }
     }
@@ -851,14 +854,18 @@ __device__ void warp_topk_row(const float* __restrict__ vals, int tn, int kappa,
 //            inv = 1 / sum, pc = e * inv (matrix.hpp:144-152), then top-kappa.
 // Dynamic smem: 8*tn floats + 8*(npow2*8 + tn) bytes + 8*d floats.
 constexpr int RROWS = 8;
+__host__ __device__ __forceinline__ int rr_ldv(int tn) { return ((tn + 3) & ~3) + 4; }
 template <int TK>  // 0: bitonic top-k; otherwise register top-k with TK keys per lane
 __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __restrict__ qp, const float* __restrict__ kp,
                                                           int kp_t, float inv_sqrt_d, int tm, int tn, int d, int kappa, int npow2,
                                                           float* __restrict__ pc_out, uint8_t* __restrict__ mask_out,
                                                           int32_t* __restrict__ idx_out) {
     extern __shared__ __align__(16) uint8_t smem[];
-    float* vals = reinterpret_cast<float*>(smem);       // [8][tn]
-    float* sq = vals + RROWS * tn;                       // [8][d]
+    // [8][ldv]: rows padded by 4 floats so the 8 rows' float4 at the same column fall in
+    // distinct banks (the serial row sums below read them across lanes)
+    const int ldv = rr_ldv(tn);
+    float* vals = reinterpret_cast<float*>(smem);
+    float* sq = vals + RROWS * ldv;                      // [8][d]
     uint8_t* keyb = reinterpret_cast<uint8_t*>(sq + RROWS * d);
     // per-row top-k scratch: 64-bit sort keys for the bitonic path, selection flags otherwise
     const size_t key_stride = TK > 0 ? (((size_t)tn + 15) & ~size_t(15)) + 512 : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
@@ -904,10 +911,16 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
                     const float qa[4] = {qv[a].x, qv[a].y, qv[a].z, qv[a].w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        acc[a][0] = __fadd_rn(acc[a][0], __fmul_rn(qa[u], kv[u].x));
-                        acc[a][1] = __fadd_rn(acc[a][1], __fmul_rn(qa[u], kv[u].y));
-                        acc[a][2] = __fadd_rn(acc[a][2], __fmul_rn(qa[u], kv[u].z));
-                        acc[a][3] = __fadd_rn(acc[a][3], __fmul_rn(qa[u], kv[u].w));
+                        // products as packed FMUL2 (two IEEE-rounded lanes), sums as scalar FADD
+                        // (a packed FADD2 fed by an FMUL2 is contracted to FFMA2 by ptxas, even
+                        // from explicit .rn PTX: not the reference's two roundings)
+                        const float2 q2 = make_float2(qa[u], qa[u]);
+                        const float2 p01 = __fmul2_rn(q2, make_float2(kv[u].x, kv[u].y));
+                        const float2 p23 = __fmul2_rn(q2, make_float2(kv[u].z, kv[u].w));
+                        acc[a][0] = __fadd_rn(acc[a][0], p01.x);
+                        acc[a][1] = __fadd_rn(acc[a][1], p01.y);
+                        acc[a][2] = __fadd_rn(acc[a][2], p23.x);
+                        acc[a][3] = __fadd_rn(acc[a][3], p23.y);
                     }
                 }
             }
@@ -915,7 +928,7 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b)
-                    if (jg * 4 + b < tn) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
+                    if (jg * 4 + b < tn) vals[(rg * 4 + a) * ldv + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
         }
     } else if ((tn & 3) == 0 && (d & 3) == 0) {
         // register tile: 4 rows x 4 columns per thread, 16 independent serial chains; each
@@ -947,7 +960,7 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) vals[(rg * 4 + a) * tn + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
+                for (int b = 0; b < 4; ++b) vals[(rg * 4 + a) * ldv + jg * 4 + b] = __fmul_rn(acc[a][b], inv_sqrt_d);
         }
     } else
     for (int j = tid; j < tn; j += 256) {
@@ -980,32 +993,38 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
             }
         }
 #pragma unroll
-        for (int r = 0; r < RROWS; ++r) vals[r * tn + j] = __fmul_rn(acc[r], inv_sqrt_d);
+        for (int r = 0; r < RROWS; ++r) vals[r * ldv + j] = __fmul_rn(acc[r], inv_sqrt_d);
+    }
+    __syncthreads();
+    const int i = i0 + warp;
+    float* v = vals + warp * ldv;
+    if (warp < nrows) {
+        float m = -INFINITY;
+        for (int j = lane; j < tn; j += 32) m = fmaxf(m, v[j]);
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        for (int j = lane; j < tn; j += 32) v[j] = expf_glibc(__fsub_rn(v[j], m));
+    }
+    __syncthreads();
+    // serial sums, j ascending (matrix.hpp:148-149): lane r of warp 0 walks row r, so one warp
+    // instruction advances all the CTA's rows (the chains' latency is the same as one per warp)
+    float* rinv = sq;  // the query rows are no longer needed
+    if (warp == 0 && lane < nrows) {
+        const float* vr = vals + lane * ldv;
+        float sum = 0.0f;
+        int j = 0;
+        for (; j + 4 <= tn; j += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(vr + j);
+            sum = __fadd_rn(sum, t.x);
+            sum = __fadd_rn(sum, t.y);
+            sum = __fadd_rn(sum, t.z);
+            sum = __fadd_rn(sum, t.w);
+        }
+        for (; j < tn; ++j) sum = __fadd_rn(sum, vr[j]);
+        rinv[lane] = __fdiv_rn(1.0f, sum);
     }
     __syncthreads();
     if (warp >= nrows) return;
-    const int i = i0 + warp;
-    float* v = vals + warp * tn;
-    float m = -INFINITY;
-    for (int j = lane; j < tn; j += 32) m = fmaxf(m, v[j]);
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    for (int j = lane; j < tn; j += 32) v[j] = expf_glibc(__fsub_rn(v[j], m));
-    __syncwarp();
-    float inv = 0.0f;
-    if (lane == 0) {  // serial sum, j ascending (matrix.hpp:148-149)
-        float sum = 0.0f;
-        int j = 0;
-        for (; j + 8 <= tn; j += 8) {
-            float t[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = v[j + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) sum = __fadd_rn(sum, t[u]);
-        }
-        for (; j < tn; ++j) sum = __fadd_rn(sum, v[j]);
-        inv = __fdiv_rn(1.0f, sum);
-    }
-    inv = __shfl_sync(0xffffffffu, inv, 0);
+    float inv = rinv[warp];
     for (int j = lane; j < tn; j += 32) {
         const float p = __fmul_rn(v[j], inv);
         v[j] = p;
@@ -1026,10 +1045,11 @@ __global__ void __launch_bounds__(256, 3) router_rows_kernel(const float* __rest
 }
 
 size_t router_rows_smem(int tn, int d, bool radix) {
+    const size_t ldv = (size_t)rr_ldv(tn);
     int npow2 = 1;
     while (npow2 < tn) npow2 <<= 1;
     const size_t key_stride = radix ? (((size_t)tn + 15) & ~size_t(15)) + 512 : (((size_t)npow2 * 8 + tn + 15) & ~size_t(15));
-    return (size_t)RROWS * tn * 4 + (size_t)RROWS * d * 4 + RROWS * key_stride + 16;
+    return (size_t)RROWS * ldv * 4 + (size_t)RROWS * d * 4 + RROWS * key_stride + 16;
 }
 
 // hard_topk alone on a caller-given score matrix (sla2_hard_topk).

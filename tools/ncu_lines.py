@@ -35,7 +35,7 @@ cur = None
 infun = False
 for line in g.splitlines():
     if re.match(r"\s*\.text\.", line) or line.startswith(".text"):
-        infun = kern in line
+        infun = os.environ.get("KDIS", kern) in line
     ms = re.findall(r"(\w+\.cuh?)\", line (\d+)", line)
     if ms and "//##" in line:  # outermost caller of inlined code
         cur = ms[-1][0] + ":" + ms[-1][1]
