@@ -9,8 +9,9 @@
 //  * three warpgroups: WG0 = TMA producers (Q / K pairs / phi(Q); V / phi(K~) ring), the MMA
 //    issuer and the Zc warp; WG1 = softmax (thread per query row) of tile k; WG2 = epilogue
 //    (thread per row) of tile k-1, concurrently; setmaxnreg moves registers to WG1/WG2;
-//  * two Q buffers: Q of tile k+1 arrives while tile k runs; the buffer then takes phi(Q) and
-//    finally the bf16 output block for the TMA store;
+//  * one Q buffer: Q of tile k+1 loads as soon as tile k's last Q K^T has read it (it arrives
+//    while tile k's last pairs and epilogue run); phi(Q) goes to TMEM, the output straight to
+//    global, and the epilogue's Hc (Htot - Hsel, bf16) takes one V / phi(K~) ring slot per tile;
 //  * the linear branch lands in the sparse accumulator: with c_r = (1 - a) l_r / (a den_r),
 //        out = a / l (O + (c phi(Q)) (Htot - Hsel))
 //    so the epilogue scales the phi(Q) rows by c, one MMA accumulates (c phi(Q)) Hc into O, and
@@ -38,13 +39,16 @@ namespace sla2dev {
 
 namespace v2 {
 constexpr int BQ = 128, BK = 64, D = 128;
-constexpr int NKP = 2, NSV = 3;                // K pair ring, V / phi(K~) ring
+// one Q buffer (the next tile's Q loads once this tile's last Q K^T is done), a ring of two K pairs
+// and four V / phi(K~) slots (one per tile holds the epilogue's Hc). A second Q buffer instead of
+// the 4th slot measured slower: the kernel waits on gather latency, so ring depth pays more
+constexpr int NKP = 2, NSV = 4;
 constexpr uint32_t Q_BYTES = BQ * D * 2;       // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;    // 16 KB
 constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // a K pair
 constexpr uint32_t VS_BYTES = 2 * TILE_BYTES;  // V + phi(K~), or Hc (bf16 128 x 128)
-constexpr uint32_t OFF_Q = 0;                  // 2 Q buffers
-constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr uint32_t OFF_Q = 0;                  // the Q buffer
+constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
 constexpr uint32_t OFF_V = OFF_K + NKP * KP_BYTES;
 constexpr uint32_t SMEM_BYTES = OFF_V + NSV * VS_BYTES;  // 224 KB
 constexpr uint32_t SMEM_ALLOC = SMEM_BYTES;  // + 3 KB static = the 227 KB limit: no alignment slack
@@ -143,7 +147,7 @@ __device__ __forceinline__ V2Tile v2_tile(const SparseV2Params& p, int t) {
 // by-value state: the counters stay in registers (lambdas capturing them by reference put them
 // on the stack).
 __device__ __forceinline__ void v2_issue_qk(uint64_t* s_free, uint64_t* k_full, uint64_t* k_empty, uint64_t* s_full,
-                                            int gg, uint32_t sbase, uint32_t tm, int pb, int nbu, int n) {
+                                            int gg, uint32_t sbase, uint32_t tm, int nbu, int n) {
     using namespace v2;
     if (gg > 0) {
         V2_WAIT(s_free, (uint32_t)((gg - 1) & 1));  // S of pair gg-1 is in the softmax's registers
@@ -153,7 +157,7 @@ __device__ __forceinline__ void v2_issue_qk(uint64_t* s_free, uint64_t* k_full, 
     V2_WAIT(&k_full[s], (uint32_t)((gg / NKP) & 1));
     tc_fence_after();
     const uint32_t idq = (2 * n + 1 < nbu) ? idesc_bf16(128, 128, false, false) : idesc_bf16(128, 64, false, false);
-    const uint64_t dQ = sdesc_sw128(sbase + OFF_Q + pb * Q_BYTES, 16, 1024);
+    const uint64_t dQ = sdesc_sw128(sbase + OFF_Q, 16, 1024);
     const uint64_t dK = sdesc_sw128(sbase + OFF_K + s * KP_BYTES, 16, 1024);
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
@@ -164,17 +168,15 @@ __device__ __forceinline__ void v2_issue_qk(uint64_t* s_free, uint64_t* k_full, 
     umma_commit_w(&k_empty[s]);
 }
 // O += (c phi(Q)) Hc of tile kk once the epilogue has built both operands: A = c phi(Q) rows in
-// the first 64 Hsel columns of TMEM (TS), B = Hc (MN-major) over the tile's own Q buffer (free
-// after its last Q K^T; the next Q it takes waits for this MMA, lin_done). Keeping Hc out of the
-// V / phi(K~) ring lets the next tile's first key blocks load without waiting for this MMA. The
-// tile's Hsel was read before, and the next tile's phi(K~)^T V MMAs follow this one in the pipe.
-__device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_done, int kk, bool linear,
+// the first 64 Hsel columns of TMEM (TS), B = Hc (MN-major) in the tile's Hc slot. The tile's
+// Hsel was read before, and the next tile's phi(K~)^T V MMAs follow this one in the tensor pipe.
+__device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_done, int kk, bool linear, int hc,
                                            uint32_t sbase, uint32_t tm) {
     using namespace v2;
     V2_WAIT(lin_ready, (uint32_t)(kk & 1));
     tc_fence_after();
     if (linear) {
-        const uint64_t dB = sdesc_sw128(sbase + OFF_Q + (kk & 1) * Q_BYTES, 16384, 1024);
+        const uint64_t dB = sdesc_sw128(sbase + OFF_V + hc * VS_BYTES, 16384, 1024);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
             umma_bf16_ts_w(tm + TM_O, tm + TM_H + ks * 8, dB + ((ks * 2048) >> 4), idesc_bf16(128, 128, false, true), 1);
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(384, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nt = p.ntiles, G = gridDim.x;
-    auto sQ = [&](int b) { return smem + OFF_Q + b * Q_BYTES; };
+    auto sQ = [&](int) { return smem + OFF_Q; };
     auto sKp = [&](int s) { return smem + OFF_K + s * KP_BYTES; };
     auto sV = [&](int s) { return smem + OFF_V + s * VS_BYTES; };
 
@@ -275,12 +277,11 @@ __global__ void __launch_bounds__(384, 1)
                         tma_load_3d_hint(sKp(s) + c * 16384 + b * 8192, &tmK, c * 64, krow, (int)T.bh, &bar_k_full[s], pol);
                     }
                 }
-                // Q of the next tile into the other buffer, which held tile k-1's Q and then its Hc: free
-                // once tile k-1's linear-branch MMA has read it
+                // Q of the next tile, once tile k's last Q K^T has read the buffer
                 if (t + G < nt) {
                     const V2Tile T1 = v2_tile(p, t + G);
                     const int k1 = k + 1;
-                    if (lane == 0 && k1 >= 2) V2_WAIT(&bar_lin_done, (uint32_t)((k1 - 2) & 1));
+                    if (lane == 0) V2_WAIT(&bar_qk_done[k & 1], (uint32_t)((k >> 1) & 1));  // tile k's last Q K^T
                     load_q(&bar_q_full[k1 & 1], sQ(k1 & 1), T1.i * BQ, (int)T1.bh);
                 }
             }
@@ -294,14 +295,17 @@ __global__ void __launch_bounds__(384, 1)
             int64_t gv = 0;
             for (int t = blockIdx.x; t < nt; t += G) {
                 const V2Tile T = v2_tile(p, t);
-                for (int j = 0; j < T.nb; ++j, ++gv) {
+                for (int j = 0; j <= T.nb; ++j, ++gv) {
                     const int s = (int)(gv % NSV);
                     if (lane == 0) {
                         if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
-                        mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
+                        if (j == T.nb)  // the Hc slot: allocated, not loaded
+                            mbar_arrive(&bar_v_full[s]);
+                        else
+                            mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
                     }
                     __syncwarp();
-                    if (lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
+                    if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
                         const int krow = T.idx[j] * BK, hz = (int)T.bh, c = lane & 1;
                         tma_load_3d_hint(sV(s) + (lane >> 1) * TILE_BYTES + c * 8192, lane < 2 ? &tmV : &tmPhi, c * 64, krow,
                                          hz, &bar_v_full[s], pol);
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(384, 1)
             int g = 0, gv = 0;  // global pair / V-slot counters (< 2^31 per CTA)
             int k = 0;
             bool prev_linear = false;
+            int prev_hc = 0;
             for (int t = blockIdx.x; t < nt; t += G, ++k) {
                 const V2Tile T = v2_tile(p, t);
                 const int nbu = (int)warp_uniform((uint32_t)T.nb);
@@ -331,16 +336,16 @@ __global__ void __launch_bounds__(384, 1)
                 V2_WAIT(&bar_q_full[pb], (uint32_t)((k >> 1) & 1));
                 tc_fence_after();
                 if (lane == 0) V2_TR(k, 0);
-                v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, g, sbase, tm, pb, nbu, 0);
+                v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, g, sbase, tm, nbu, 0);
                 if (npu == 1) umma_commit_w(&bar_qk_done[pb]);
                 for (int n = 0; n < npu; ++n) {
                     const int gg = g + n;
                     if (n + 1 < npu) {
-                        v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, gg + 1, sbase, tm, pb, nbu, n + 1);
+                        v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, gg + 1, sbase, tm, nbu, n + 1);
                         if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
                     }
                     if (n == 0 && k > 0)  // tile k-1's linear term, before PV(0)
-                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, sbase, tm);
+                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
                     V2_WAIT(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
                     tc_fence_after();
                     if (n == 0 && k > 0) {
@@ -378,9 +383,11 @@ __global__ void __launch_bounds__(384, 1)
                 if (lane == 0) V2_TR(k, 28);
                 g += npu;
                 gv += nbu;
+                prev_hc = gv % NSV;  // the tile's Hc slot
+                gv += 1;
                 prev_linear = lin;
             }
-            if (k > 0) v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, sbase, tm);
+            if (k > 0) v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
         } else if (warp == 3) {
             // ============ Zc = Ztot - sum_sel z_j per tile (the linear denominators) ============
             int k = 0;
@@ -537,10 +544,14 @@ __global__ void __launch_bounds__(384, 1)
         // ============ epilogue of tile k (thread = row r), one tile behind the softmax ============
         const int r = threadIdx.x - 256;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        int gv = 0;
         int k = 0;
         for (int t = blockIdx.x; t < nt; t += G, ++k) {
             const V2Tile T = v2_tile(p, t);
             const int pb = k & 1;
+            const int vhc = gv + T.nb;  // the tile's Hc slot
+            const int hcs = vhc % NSV;
+            gv = vhc + 1;
             const int64_t grow = T.bh * (int64_t)p.N + (int64_t)T.i * BQ + r;
             const bool row_live = T.i * BQ + r < p.N;  // ragged N: the last block's rows past N
             float alpha = 1.0f, l = 1.0f;
@@ -593,7 +604,8 @@ __global__ void __launch_bounds__(384, 1)
             if (r == 0) V2_TR(k, 17);
             if (T.linear) {
                 // Hc = Htot - Hsel, row f = r, as the MN-major B tile [c_atom 2][f 128][64 c] (bf16)
-                const uint32_t hb = smem_u32(sQ(pb));  // the tile's Q buffer: its Q K^T are done (tile_done)
+                V2_WAIT(&bar_v_full[hcs], (uint32_t)((vhc / NSV) & 1));  // the Hc slot is ours
+                const uint32_t hb = smem_u32(sV(hcs));
 #pragma unroll
                 for (int c0 = 0; c0 < 128; c0 += 32) {
                     uint32_t hs[32];
@@ -650,7 +662,10 @@ __global__ void __launch_bounds__(384, 1)
                                        pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
                 }
             }
-            if (r == 0) V2_TR(k, 22);
+            if (r == 0) {
+                V2_TR(k, 22);
+                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring (the lin MMA is done)
+            }
         }
     }
     tc_fence_before();
