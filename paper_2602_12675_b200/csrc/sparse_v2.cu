@@ -340,12 +340,14 @@ __global__ void __launch_bounds__(384, 1)
                 if (npu == 1) umma_commit_w(&bar_qk_done[pb]);
                 for (int n = 0; n < npu; ++n) {
                     const int gg = g + n;
+                    // tile k-1's linear term ahead of QK(1) in the tensor pipe: O (and the Hc slot) free
+                    // sooner for PV(0); S(1) is not needed before P(0) anyway (measured 0.582 -> 0.566 ms)
+                    if (n == 0 && k > 0)
+                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
                     if (n + 1 < npu) {
                         v2_issue_qk(bar_s_free_p, bar_k_full, bar_k_empty, &bar_s_full, gg + 1, sbase, tm, nbu, n + 1);
                         if (n + 2 == npu) umma_commit_w(&bar_qk_done[pb]);  // the tile's last Q K^T
                     }
-                    if (n == 0 && k > 0)  // tile k-1's linear term, before PV(0)
-                        v2_lin_mma(&bar_lin_ready, &bar_lin_done, k - 1, prev_linear, prev_hc, sbase, tm);
                     V2_WAIT(&bar_p_full[gg & 1], (uint32_t)((gg >> 1) & 1));
                     tc_fence_after();
                     if (n == 0 && k > 0) {
@@ -637,7 +639,10 @@ __global__ void __launch_bounds__(384, 1)
             V2_WAIT(&bar_lin_done, (uint32_t)(k & 1));
             __syncwarp();
             tc_fence_after();
-            if (r == 0) V2_TR(k, 20);
+            if (r == 0) {
+                V2_TR(k, 20);
+                mbar_arrive(&bar_v_empty[hcs]);  // the lin MMA has read Hc: the slot returns to the V ring
+            }
             // out = alpha / l * O straight to global (row r: 256 contiguous bytes)
             const float sc = alpha / l;
             uint4* orow = reinterpret_cast<uint4*>(p.out + grow * D);
@@ -662,10 +667,7 @@ __global__ void __launch_bounds__(384, 1)
                                        pack_bf16(__uint_as_float(o[ch * 8 + 6]) * sc, __uint_as_float(o[ch * 8 + 7]) * sc));
                 }
             }
-            if (r == 0) {
-                V2_TR(k, 22);
-                mbar_arrive(&bar_v_empty[hcs]);  // the Hc slot returns to the V ring (the lin MMA is done)
-            }
+            if (r == 0) V2_TR(k, 22);
         }
     }
     tc_fence_before();
