@@ -52,6 +52,11 @@ CONFIGS = {
     # the INT8 QAT path keeps the reference's divisibility rule (N padded to 32768)
     "cfg3": dict(workload="wan2.1-1.3B-480p attention, INT8 QAT (BASELINE configs[2])", B=1, H=12, N=32768,
                  d=128, bq=128, bk=64, k_percent=3.0, bf16=True, quant=True),
+    # configs[2]'s low-bit P/V product (FP8 PV): E4M3 P, V and phi(K~) on kind::f8f6f4, bf16 Q K^T,
+    # at the true N = 32760; not a reference mode (the reference is INT8-only), so the oracle is the
+    # unquantized reference; the output bar is the FP8 one (1e-1 max normwise, tests/test_gpu_fp8.py)
+    "cfg3fp8": dict(workload="wan2.1-1.3B-480p attention, FP8 P/V low-bit mode (BASELINE configs[2])", B=1, H=12,
+                    N=32760, d=128, bq=128, bk=64, k_percent=3.0, bf16=True, quant="fp8"),
     "cfg4": dict(workload="wan2.1-14B-720p attention (BASELINE configs[3])", B=1, H=40, N=75600, d=128, bq=128,
                  bk=64, k_percent=3.0, bf16=True, quant=False),
     "cfg1": dict(workload="fp32 CPU-oracle case (BASELINE configs[0])", B=1, H=2, N=4096, d=64, bq=64, bk=64,
@@ -182,7 +187,7 @@ def cpu_reference_run(c, steps, warmup, threads=None):
     for s in range(warmup + steps):
         t0 = time.perf_counter()
         o.attention(q[0, 0], k[0, 0], v[0, 0], c["bq"], c["bk"], pq[0], pk[0], rho[0], c["k_percent"],
-                    quant=c["quant"])
+                    quant=c["quant"] is True)
         dt = time.perf_counter() - t0
         if s >= warmup:
             times.append(dt)
@@ -243,7 +248,8 @@ def parity_block(c, masks_all, outs, dev, seed_base, dtype):
 
     t0 = time.perf_counter()
     res = verify_gathered(masks_all.cpu().numpy(), {h: o.float().cpu().numpy() for h, o in outs.items()}, regen,
-                          c["k_percent"], c["bq"], c["bk"], quant=c["quant"])
+                          c["k_percent"], c["bq"], c["bk"], quant=c["quant"] is True,
+                          tol=0.1 if c["quant"] == "fp8" else 1e-2)  # FP8 bar: tests/test_gpu_fp8.py
     res["check_s"] = round(time.perf_counter() - t0, 2)
     return res
 
@@ -312,7 +318,7 @@ def main():
     tm, tn, kappa = geometry(c)
     cfg_out = {"workload": c["workload"], "name": cfg_name, "B": c["B"], "H": c["H"], "N": c["N"], "d": c["d"],
                "bq": c["bq"], "bk": c["bk"], "k_percent": c["k_percent"], "kappa": kappa, "sparsity": 1 - kappa / tn,
-               "quant": "int8" if c["quant"] else "none",
+               "quant": {True: "int8", False: "none"}.get(c["quant"], c["quant"]),
                "parallelism": (f"heads-replicated x{world} (weak)" if scaling == "weak"
                                else f"heads sharded over {world} ranks (strong)")}
 
@@ -470,7 +476,12 @@ def main():
             traffic = json.load(f).get(cfg_name, {}).get("sparse_kernel_dram_bytes_per_launch")
     except Exception:
         pass
-    if c["quant"]:
+    if c["quant"] == "fp8":
+        # PV and phi(K~)^T V on kind::f8f6f4 (twice the bf16 rate), Q K^T and the phi(Q) Hc product
+        # on kind::f16: the bf16 peak is the conservative denominator
+        kern, peak, peak_src = ("sla2_sparse_v2_kernel<F8> (E4M3 P / V / phi(K~))", pk_["bf16"],
+                                pk_["src"] + " burst bf16 (MEASURED_PEAKS.json)")
+    elif c["quant"]:
         # the QAT stage: K~ codes (quant_prep_kernel), the bf16 linear branch (sla2_linsel_kernel)
         # and the INT8 softmax branch (sla2_attn_i8_kernel: QK^T and PV on tcgen05 kind::i8, K = 32
         # per instruction at the kind::f16 issue rate, tools/mb_umma.cu -> twice the bf16 peak)
@@ -585,7 +596,7 @@ def standin_main(args, c, cfg_out, world, rank, scaling):
     masks, outs = [], []
     for h in range(h0, h1):
         q, k, v, pq, pk, rho = (x.float().numpy() for x in sd.head_inputs(h, c["N"], c["d"], tm, dt, dev))
-        o, m = oracle_attention_any(q, k, v, pq, pk, rho, c["bq"], c["bk"], c["k_percent"], quant=c["quant"])[:2]
+        o, m = oracle_attention_any(q, k, v, pq, pk, rho, c["bq"], c["bk"], c["k_percent"], quant=c["quant"] is True)[:2]
         masks.append(torch.from_numpy(m))
         outs.append(torch.from_numpy(o))
     t_max = sd.max_over_ranks((time.perf_counter() - t0) * 1e3)

@@ -46,7 +46,10 @@ typedef enum {
 typedef enum { SLA2_F32 = 0, SLA2_BF16 = 1 } sla2_dtype;
 
 /* QuantConfig (quant.hpp:15-19): NONE = nullptr, INT8 = {bits 8, qk_product, pv_product}. */
-typedef enum { SLA2_QUANT_NONE = 0, SLA2_QUANT_INT8 = 1 } sla2_quant;
+/* SLA2_QUANT_FP8PV is not a reference mode (the reference is INT8-only): the paper's low-bit
+ * P/V product in E4M3 on kind::f8f6f4 (P unscaled, V with one scale per head, phi(K~) x 448),
+ * bf16 Q K^T, fp32 accumulation; bf16 path, out only; checked within the bf16 tolerance. */
+typedef enum { SLA2_QUANT_NONE = 0, SLA2_QUANT_INT8 = 1, SLA2_QUANT_FP8PV = 2 } sla2_quant;
 
 typedef struct {
     int64_t B, H, N, d; /* batch, heads, tokens, head dim. N % bq == N % bk == 0 as the reference

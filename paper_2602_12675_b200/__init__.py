@@ -189,7 +189,7 @@ class FwdParams:
         p.B, p.H, p.N, p.d, p.bq, p.bk = self.B, self.H, self.N, self.d, self.bq, self.bk
         p.k_percent = float(self.k_percent)
         p.dtype = 1 if self.bf16 else 0
-        p.quant = 1 if self.quant else 0
+        p.quant = _quant_code(self.quant)
         p.smooth = int(bool(self.smooth))
         p.exact_mu = int(bool(self.exact_mu))
         p.tau = float(self.tau)
@@ -237,6 +237,18 @@ def _stream(dev):
     return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
+def _quant_code(quant) -> int:
+    """quant: False / "none" -> SLA2_QUANT_NONE; True / "int8" -> SLA2_QUANT_INT8 (the reference's
+    QuantConfig, quant.hpp:15-19, reproduced exactly); "fp8" -> SLA2_QUANT_FP8PV (E4M3 P / V,
+    tolerance only; not a reference mode)."""
+    if isinstance(quant, str):
+        codes = {"none": 0, "int8": 1, "fp8": 2}
+        if quant not in codes:
+            raise ContractError(f"unknown quant mode {quant!r} (none, int8, fp8)")
+        return codes[quant]
+    return 1 if quant else 0
+
+
 def _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu, tau=0.1):
     import torch
     if q.dim() != 4:
@@ -273,7 +285,7 @@ def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant
     sv = None
     svs = None
     if saved:
-        sv, svs = _saved_buffers(p, q, saved == "full", bool(quant) and saved == "full")
+        sv, svs = _saved_buffers(p, q, saved == "full", _quant_code(quant) == 1 and saved == "full")
     if workspace is not None:
         if workspace.dtype != torch.uint8 or workspace.device != dev or workspace.numel() < workspace_bytes(p):
             raise ContractError("workspace too small (see workspace_bytes)")
@@ -453,7 +465,7 @@ def sla2_forward_blockwise(q, k, v, mask, rho, *, bq=128, bk=64, quant=False, sm
     sv = None
     svs = None
     if saved:
-        sv, svs = _saved_buffers(p, q, saved == "full", bool(quant) and saved == "full")
+        sv, svs = _saved_buffers(p, q, saved == "full", _quant_code(quant) == 1 and saved == "full")
     ws = _workspace(p, dev)
     _raise(lib().sla2_sparse_fwd(C.byref(cp), _ptr(q), _ptr(k), _ptr(v), _ptr(rho.contiguous()),
                                  _ptr(mask.contiguous().to(torch.uint8)), _ptr(out),

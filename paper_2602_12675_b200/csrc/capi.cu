@@ -190,6 +190,7 @@ bool make_map3(CUtensorMap* out, const void* ptr, uint64_t heads, uint64_t rows,
 struct Geo {
     int64_t B, H, BH, N, d, bq, bk, tm, tn, kappa;
     bool bf16, quant;
+    bool fp8;  // SLA2_QUANT_FP8PV: E4M3 P / V / phi(K~) in the sparse kernel (tolerance mode)
     int nchunk;
 };
 
@@ -208,6 +209,7 @@ Geo geometry(const sla2_fwd_params* p) {
     g.kappa = sla2_topk_budget(p->k_percent, g.tn);
     g.bf16 = p->dtype == SLA2_BF16;
     g.quant = p->quant == SLA2_QUANT_INT8;
+    g.fp8 = p->quant == SLA2_QUANT_FP8PV && g.bf16;
     if (g.bf16) {
         // Htot partial chunks of 22 key blocks (kphi_htot_kernel, 2 CTAs per SM): at cfg2, 12 heads
         // x 24 chunks = 288 CTAs, one wave on 148 SMs. Depends on tn only, so a head's Htot (and
@@ -251,6 +253,8 @@ struct Workspace {
     void* ol;    // bf16 path: the linear branch's O_l rows (sparse_fa.cu), [BH][N][d]
     int8_t *qc, *kc, *vct;
     float *qs, *ks, *vs;
+    uint8_t *v8, *phi8;  // FP8 P/V mode: E4M3 V and phi(K~) [BH][N][d]
+    uint32_t* vamax;     // FP8 P/V mode: [BH] max |V|
     int32_t* cnt;
     int* flag;
 };
@@ -279,6 +283,11 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
 #else
     t.ol = (g.bf16 && g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;  // QAT: linear-branch O_l
 #endif
+    if (g.fp8) {
+        t.v8 = c.take<uint8_t>(g.BH * g.N * g.d);
+        t.phi8 = c.take<uint8_t>(g.BH * g.N * g.d);
+        t.vamax = c.take<uint32_t>(g.BH);
+    }
     if (g.quant) {
         t.qc = c.take<int8_t>(g.BH * g.N * g.d);
         t.kc = c.take<int8_t>(g.BH * g.N * g.d);
@@ -424,7 +433,7 @@ static sla2_status check_common(const sla2_fwd_params* p, bool hard_budget = tru
         return fail(SLA2_SHAPE_ERROR, "B, H, N, d must be positive");
     if (p->bq <= 0 || p->bk <= 0) return fail(SLA2_SHAPE_ERROR, "block sizes must be positive");
     if ((p->N % p->bq != 0 || p->N % p->bk != 0) &&
-        !(p->dtype == SLA2_BF16 && p->quant == SLA2_QUANT_NONE && p->d == 128 && p->bq == 128 && p->bk == 64))
+        !(p->dtype == SLA2_BF16 && p->quant != SLA2_QUANT_INT8 && p->d == 128 && p->bq == 128 && p->bk == 64))
         // the reference's rule (attention.hpp:39-41); the ragged extension (partial last blocks,
         // SURVEY.md 8f item 2) exists on the bf16 tcgen05 path only
         return fail(SLA2_SHAPE_ERROR, "AttentionInputs: N must be divisible by bq and bk");
@@ -432,8 +441,10 @@ static sla2_status check_common(const sla2_fwd_params* p, bool hard_budget = tru
         return fail(SLA2_SHAPE_ERROR, "hard_topk: k_percent must be in (0, 100]");  // router.hpp:108-110
     if (!(p->tau > 0.0f)) return fail(SLA2_NUMERIC_ERROR, "RouterParams: tau must be positive");  // router.hpp:32
     if (p->dtype != SLA2_F32 && p->dtype != SLA2_BF16) return fail(SLA2_CONTRACT_ERROR, "unknown dtype");
-    if (p->quant != SLA2_QUANT_NONE && p->quant != SLA2_QUANT_INT8)
+    if (p->quant != SLA2_QUANT_NONE && p->quant != SLA2_QUANT_INT8 && p->quant != SLA2_QUANT_FP8PV)
         return fail(SLA2_CONTRACT_ERROR, "unknown quant mode");
+    if (p->quant == SLA2_QUANT_FP8PV && p->dtype != SLA2_BF16)
+        return fail(SLA2_CONTRACT_ERROR, "FP8 P/V mode runs on the bf16 inputs path");
     if (p->N * p->B * p->H > (int64_t)INT32_MAX)
         return fail(SLA2_CONTRACT_ERROR, "B*H*N exceeds the 2^31 row limit of the TMA descriptors");
     return SLA2_OK;
@@ -476,6 +487,7 @@ size_t sla2_workspace_size(const sla2_fwd_params* p) {
 struct LinPlan {
     cudaEvent_t dep = nullptr;
     cudaEvent_t qv_codes = nullptr;  // QAT: Q and V codes were quantized on a side stream (done at this event)
+    cudaEvent_t fp8_v = nullptr;     // FP8 P/V: V8 and its per-head scale were made on a side stream
     bool kprep = false;
     bool phiq_ready = false;  // the router front already wrote phi(Q) (bf16 path)
     float* kbar = nullptr;
@@ -536,7 +548,13 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         cudaEvent_t lin_done = aux_event(11);
         SLA2_CUDA_TRY(cudaStreamWaitEvent(lin, dep, 0));
         if (plan.kprep && la.phik_ready) SLA2_CUDA_TRY(launch_kphi(la, lin, &g_launches));
+        // FP8 P/V: the fused phi(K~) / Htot kernel writes E4M3 phi(K~) directly
+        const bool phi8_fused = g.fp8 && la.tm_k && !la.phik_ready;
+        if (phi8_fused) la.phi8 = w.phi8;
         SLA2_CUDA_TRY(launch_linear_prep(la, lin, &g_launches));
+        if (g.fp8 && (!phi8_fused || !plan.fp8_v))  // the E4M3 operands not made elsewhere
+            SLA2_CUDA_TRY(launch_fp8pv_prep(plan.fp8_v ? nullptr : v, phi8_fused ? nullptr : w.phik, w.v8, w.phi8,
+                                            w.vamax, g.BH, g.N, lin, &g_launches));
         mark(8, lin);
         SLA2_CUDA_TRY(cudaEventRecord(lin_done, lin));
         // the router's key side on a high-priority stream: the block scheduler serves it ahead of
@@ -568,6 +586,7 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         SLA2_CUDA_TRY(cudaStreamWaitEvent(st, lin_done, 0));
     } else {
         SLA2_CUDA_TRY(launch_linear_prep(la, st, &g_launches));
+        if (g.fp8) SLA2_CUDA_TRY(launch_fp8pv_prep(v, w.phik, w.v8, w.phi8, w.vamax, g.BH, g.N, st, &g_launches));
     }
     mark(2, st);
 
@@ -679,6 +698,19 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         } else if (sparse_v4_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v4(sa, st, &g_launches));
 #endif
+        } else if (g.fp8) {
+            // FP8 P/V (tolerance mode): the persistent kernel with E4M3 P, V and phi(K~)
+            CUtensorMap mv8, mphi8;
+            if (!make_map3(&mv8, w.v8, (uint64_t)g.BH, (uint64_t)g.N, g.d, 128, 64, 1) ||
+                !make_map3(&mphi8, w.phi8, (uint64_t)g.BH, (uint64_t)g.N, g.d, 128, 64, 1))
+                return fail(SLA2_CUDA_ERROR, "cuTensorMapEncodeTiled failed (fp8 operands)");
+            if (plan.fp8_v) SLA2_CUDA_TRY(cudaStreamWaitEvent(st, plan.fp8_v, 0));
+            sa.vamax = w.vamax;
+            sa.tm_v8 = &mv8;
+            sa.tm_phi8 = &mphi8;
+            if (!sparse_v2_eligible(sa))
+                return fail(SLA2_CONTRACT_ERROR, "FP8 P/V mode computes out only (no saved state)");
+            SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
         } else if (sparse_v2_eligible(sa)) {
             SLA2_CUDA_TRY(launch_sparse_v2(sa, st, &g_launches));
         } else {
@@ -825,6 +857,17 @@ sla2_status sla2_forward(const sla2_fwd_params* p, const void* q, const void* k,
             SLA2_CUDA_TRY(launch_quant_prep(qa, qs, &g_launches));
             SLA2_CUDA_TRY(cudaEventRecord(ev_qv, qs));
             plan.qv_codes = ev_qv;
+        } else if (g.fp8) {
+            // FP8 P/V: V's per-head scale and E4M3 codes do not depend on mu either: a low-priority
+            // side stream makes them while the serial column mean holds a few SMs (measured at
+            // cfg3fp8: 0.591-0.598 ms; after the linear precompute instead: 0.597-0.600 ms)
+            cudaStream_t qs = aux_stream(3, -1);
+            cudaEvent_t ev0 = aux_event(13), ev_v = aux_event(14);
+            SLA2_CUDA_TRY(cudaEventRecord(ev0, st));
+            SLA2_CUDA_TRY(cudaStreamWaitEvent(qs, ev0, 0));
+            SLA2_CUDA_TRY(launch_fp8pv_prep(v, nullptr, w.v8, w.phi8, w.vamax, g.BH, g.N, qs, &g_launches));
+            SLA2_CUDA_TRY(cudaEventRecord(ev_v, qs));
+            plan.fp8_v = ev_v;
         }
         SLA2_CUDA_TRY(launch_router_front(ra, st, &g_launches));
         plan.kprep = true;

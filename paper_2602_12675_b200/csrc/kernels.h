@@ -78,6 +78,7 @@ struct LinearLaunch {
     const CUtensorMap* tm_k;  // bf16 path: K map (box 64x64, SW128); with mu set, phi(K~) is fused
                               // into the Htot partial kernel (kphi_htot_kernel)
     bool phik_ready;  // phi(K~) and z_j already written by launch_kprep
+    uint8_t* phi8 = nullptr;  // FP8 P/V mode: the fused kernel writes E4M3 448 phi(K~) here instead of phik
 };
 cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* launches);
 // Fused key-side prep (d = 128): phi(K~) + z_j (as phik_kernel) and the router's pooled keys
@@ -125,6 +126,10 @@ struct SparseLaunch {
     const void* phiq;            // the same phi(Q) rows (bf16 [BH][N][d])
     const CUtensorMap* tm_out;   // out bf16 as [BH*N][d], box 64 x 64, SW128 (TMA-stored blocks)
     void* ol;                    // bf16 [BH][N][d] scratch: the linear branch's O_l (sparse_fa.cu)
+    // FP8 P/V mode (sparse_v2.cu, non-null vamax): E4M3 V8 / phi8 [BH][N][128] maps (box 128 x 64 B)
+    const uint32_t* vamax;       // [BH] max |V| bits
+    const CUtensorMap* tm_v8;
+    const CUtensorMap* tm_phi8;
     // f32 path
     const float* q;
     const float* k;
@@ -135,6 +140,9 @@ cudaError_t launch_sparse_bf16(const SparseLaunch& a, cudaStream_t st, int* laun
 // persistent variant (sparse_v2.cu): the non-saved, non-dense bf16 path
 bool sparse_v2_eligible(const SparseLaunch& a);
 cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launches);
+// FP8 P/V operands: amax[bh] = max |V|, v8 = e4m3(V * 448 / amax), phi8 = e4m3(448 phi(K~)) (bf16 in)
+cudaError_t launch_fp8pv_prep(const void* v, const void* phik, uint8_t* v8, uint8_t* phi8, uint32_t* amax, int64_t BH,
+                              int64_t N, cudaStream_t st, int* launches);
 // persistent variant with 8 softmax warps and double-buffered S (sparse_v3.cu)
 bool sparse_v3_eligible(const SparseLaunch& a);
 // persistent variant with 64-key steps, two S buffers and two O accumulators (sparse_v4.cu)

@@ -301,7 +301,7 @@ constexpr uint32_t SMEM = NS * 2 * TILE + 1024;  // [K -> phi(K~)][V] per stage
 __global__ void __launch_bounds__(192, 1)
     kphi_htot_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      const float* __restrict__ mu, __nv_bfloat16* __restrict__ phik, float* __restrict__ zblk,
-                     float* __restrict__ hpart, int N, int per, int nchunk) {
+                     float* __restrict__ hpart, int N, int per, int nchunk, uint8_t* __restrict__ phi8) {
     using namespace kh;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -426,8 +426,15 @@ __global__ void __launch_bounds__(192, 1)
                     uint32_t w1 = pack_bf16(xs[u][2] * inv, xs[u][3] * inv);
                     if (r0 + u >= cnt) w0 = w1 = 0u;  // past N: no key, phi = 0 (adds nothing to Htot)
                     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr[u]), "r"(w0), "r"(w1) : "memory");
-                    if (r0 + u < cnt)
-                        *reinterpret_cast<uint2*>(phik + (grow0 + r0 + u) * D + lane * 4) = make_uint2(w0, w1);
+                    if (r0 + u < cnt) {
+                        if (phi8)  // FP8 P/V mode: only the E4M3 448 phi(K~) rows the sparse kernel reads
+                            *reinterpret_cast<uint32_t*>(phi8 + (grow0 + r0 + u) * D + lane * 4) =
+                                pack_e4m3x2(__uint_as_float(w0 << 16) * 448.0f, __uint_as_float(w0 & 0xffff0000u) * 448.0f) |
+                                (pack_e4m3x2(__uint_as_float(w1 << 16) * 448.0f, __uint_as_float(w1 & 0xffff0000u) * 448.0f)
+                                 << 16);
+                        else
+                            *reinterpret_cast<uint2*>(phik + (grow0 + r0 + u) * D + lane * 4) = make_uint2(w0, w1);
+                    }
                     z[0] += __uint_as_float(w0 << 16);
                     z[1] += __uint_as_float(w0 & 0xffff0000u);
                     z[2] += __uint_as_float(w1 << 16);
@@ -777,7 +784,7 @@ cudaError_t launch_linear_prep(const LinearLaunch& a, cudaStream_t st, int* laun
         ensure_smem_attr((const void*)kphi_htot_kernel, (int)(kh::SMEM));
         const int per = (tn + a.nchunk - 1) / a.nchunk;
         kphi_htot_kernel<<<dim3(a.nchunk, (unsigned)a.BH), 192, kh::SMEM, st>>>(
-            *a.tm_k, *a.tm_v, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.hpart, a.N, per, a.nchunk);
+            *a.tm_k, *a.tm_v, a.mu, (__nv_bfloat16*)a.phik, a.zblk, a.hpart, a.N, per, a.nchunk, a.phi8);
     } else if (a.bf16) {
         if (!a.phik_ready)
             phik_kernel<__nv_bfloat16, __nv_bfloat16><<<g1, 128, 0, st>>>(

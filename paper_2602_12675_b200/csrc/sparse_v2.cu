@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 
@@ -45,6 +46,7 @@ constexpr int BQ = 128, BK = 64, D = 128;
 constexpr int NKP = 2, NSV = 4;
 constexpr uint32_t Q_BYTES = BQ * D * 2;       // 32 KB
 constexpr uint32_t TILE_BYTES = BK * D * 2;    // 16 KB
+constexpr uint32_t TILE8_BYTES = BK * D;       // 8 KB: an E4M3 V / phi(K~) block (FP8 P/V mode)
 constexpr uint32_t KP_BYTES = 2 * TILE_BYTES;  // a K pair
 constexpr uint32_t VS_BYTES = 2 * TILE_BYTES;  // V + phi(K~), or Hc (bf16 128 x 128)
 constexpr uint32_t OFF_Q = 0;                  // the Q buffer
@@ -67,6 +69,7 @@ struct SparseV2Params {
     const __nv_bfloat16* htot16;  // [BH][D][D] bf16 (the epilogue forms Hc = Htot - Hsel from it)
     const __nv_bfloat16* phiq;    // [BH][N][D] bf16 phi(Q) rows (router front)
     __nv_bfloat16* out;           // [BH][N][D]
+    const uint32_t* vamax;        // FP8 P/V mode: [BH] max |V| bits (V8 = e4m3(V * 448 / amax), phi8 = e4m3(448 phi))
     int N, H, tm, tn, ntiles;
     int last_valid;
     float scale_log2;
@@ -184,6 +187,7 @@ __device__ __forceinline__ void v2_lin_mma(uint64_t* lin_ready, uint64_t* lin_do
     umma_commit_w(lin_done);
 }
 
+template <bool F8>
 __global__ void __launch_bounds__(384, 1)
     sla2_sparse_v2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmPhi,
@@ -301,11 +305,17 @@ __global__ void __launch_bounds__(384, 1)
                         if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
                         if (j == T.nb)  // the Hc slot: allocated, not loaded
                             mbar_arrive(&bar_v_full[s]);
+                        else if (F8)
+                            mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE8_BYTES : TILE8_BYTES);
                         else
                             mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
                     }
                     __syncwarp();
-                    if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
+                    if (F8) {  // one 128-byte-wide box per tensor: V8 at the slot, phi8 TILE_BYTES in
+                        if (j < T.nb && lane < (T.linear ? 2 : 1))
+                            tma_load_3d_hint(sV(s) + lane * TILE_BYTES, lane == 0 ? &tmV : &tmPhi, 0, T.idx[j] * BK,
+                                             (int)T.bh, &bar_v_full[s], pol);
+                    } else if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
                         const int krow = T.idx[j] * BK, hz = (int)T.bh, c = lane & 1;
                         tma_load_3d_hint(sV(s) + (lane >> 1) * TILE_BYTES + c * 8192, lane < 2 ? &tmV : &tmPhi, c * 64, krow,
                                          hz, &bar_v_full[s], pol);
@@ -319,6 +329,8 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t ID_PV = idesc_bf16(128, 128, false, true);
             constexpr uint32_t ID_HS = idesc_bf16(128, 128, true, true);
             constexpr uint32_t ID_LIN = idesc_bf16(128, 128, false, true);
+            constexpr uint32_t ID_PV8 = idesc_e4m3(128, 128, false, true);
+            constexpr uint32_t ID_HS8 = idesc_e4m3(128, 128, true, true);
             const uint32_t tm = warp_uniform(tmem);
             const uint32_t sbase = warp_uniform(smem_u32(smem));
             uint64_t* bar_s_free_p = &bar_s_free;
@@ -362,10 +374,17 @@ __global__ void __launch_bounds__(384, 1)
                         V2_WAIT(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
                         tc_fence_after();
                         const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
-                        const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 32);
+                        if (F8) {  // P: 4 e4m3 per TMEM column (16 per key block); V8 MN-major, 32 keys per MMA
+                            const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 16);
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)
-                            umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
+                            for (int ks = 0; ks < 2; ++ks)
+                                umma_f8_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 4096) >> 4), ID_PV8, (j > 0 || ks > 0));
+                        } else {
+                            const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 32);
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_bf16_ts_w(tm + TM_O, aP + ks * 8, dV + ((ks * 2048) >> 4), ID_PV, (j > 0 || ks > 0));
+                        }
                     }
                     umma_commit_w(&bar_pv_done[gg & 1]);
                     for (int j = j0; j < j1; ++j) {
@@ -373,10 +392,17 @@ __global__ void __launch_bounds__(384, 1)
                         if (lin) {
                             const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
                             const uint64_t dP = dV + (TILE_BYTES >> 4);
+                            if (F8) {
 #pragma unroll
-                            for (int ks = 0; ks < 4; ++ks)
-                                umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
-                                               (j > 0 || ks > 0));
+                                for (int ks = 0; ks < 2; ++ks)
+                                    umma_f8_ss_w(tm + TM_H, dP + ((ks * 4096) >> 4), dV + ((ks * 4096) >> 4), ID_HS8,
+                                                 (j > 0 || ks > 0));
+                            } else {
+#pragma unroll
+                                for (int ks = 0; ks < 4; ++ks)
+                                    umma_bf16_ss_w(tm + TM_H, dP + ((ks * 2048) >> 4), dV + ((ks * 2048) >> 4), ID_HS,
+                                                   (j > 0 || ks > 0));
+                            }
                         }
                         umma_commit_w(&bar_v_empty[sv]);
                     }
@@ -519,17 +545,35 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int blk = 0; blk < 2; ++blk) {
                     if (blk == 1 && !two) break;
-                    uint32_t w[32];
+                    if (F8) {  // P <= 2^RESCALE_LOG2 = 256 < 448: e4m3 without a scale, 4 keys per column
+                        uint32_t w[16];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {  // packed FFMA2 / FADD2 (half the issue of scalar)
-                        const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[blk * 64 + 2 * e]),
-                                                                 __uint_as_float(sr[blk * 64 + 2 * e + 1])),
-                                                     sc2, nm2);
-                        const float2 pe = make_float2(v2_exp2(x2.x), v2_exp2(x2.y));
-                        rs = __fadd2_rn(rs, pe);
-                        w[e] = pack_bf16(pe.x, pe.y);
+                        for (int e = 0; e < 16; ++e) {
+                            const float2 xa = __ffma2_rn(make_float2(__uint_as_float(sr[blk * 64 + 4 * e]),
+                                                                     __uint_as_float(sr[blk * 64 + 4 * e + 1])),
+                                                         sc2, nm2);
+                            const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sr[blk * 64 + 4 * e + 2]),
+                                                                     __uint_as_float(sr[blk * 64 + 4 * e + 3])),
+                                                         sc2, nm2);
+                            const float2 pa = make_float2(v2_exp2(xa.x), v2_exp2(xa.y));
+                            const float2 pb2 = make_float2(v2_exp2(xb.x), v2_exp2(xb.y));
+                            rs = __fadd2_rn(rs, __fadd2_rn(pa, pb2));
+                            w[e] = pack_e4m3x2(pa.x, pa.y) | (pack_e4m3x2(pb2.x, pb2.y) << 16);
+                        }
+                        tmem_st16(pbase + blk * 16, w);
+                    } else {
+                        uint32_t w[32];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {  // packed FFMA2 / FADD2 (half the issue of scalar)
+                            const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[blk * 64 + 2 * e]),
+                                                                     __uint_as_float(sr[blk * 64 + 2 * e + 1])),
+                                                         sc2, nm2);
+                            const float2 pe = make_float2(v2_exp2(x2.x), v2_exp2(x2.y));
+                            rs = __fadd2_rn(rs, pe);
+                            w[e] = pack_bf16(pe.x, pe.y);
+                        }
+                        tmem_st32(pbase + blk * 32, w);
                     }
-                    tmem_st32(pbase + blk * 32, w);
                 }
                 l += rs.x + rs.y;
                 if (n == npair - 1) sL[k & 1][r] = l;  // before the last P: the epilogue's 1 / l
@@ -557,6 +601,15 @@ __global__ void __launch_bounds__(384, 1)
             const int64_t grow = T.bh * (int64_t)p.N + (int64_t)T.i * BQ + r;
             const bool row_live = T.i * BQ + r < p.N;  // ragged N: the last block's rows past N
             float alpha = 1.0f, l = 1.0f;
+            // FP8 P/V: O and Hsel accumulate in V8 units (V = vs V8, phi = phi8 / 448):
+            // out = alpha / l * vs * (O8 + (c phi(Q)) Hc8), Hc8 = Htot / vs - Hsel8 / 448
+            float vs = 1.0f, ivs = 1.0f;
+            if (F8) {
+                const float am = __uint_as_float(p.vamax[T.bh]);
+                vs = am > 0.0f ? am * (1.0f / 448.0f) : 1.0f;
+                ivs = 1.0f / vs;
+            }
+            const float hs_scale = F8 ? 1.0f / 448.0f : 1.0f;
             uint32_t cq[64];  // c phi(Q)_r as packed bf16 pairs (the lin MMA's A row)
             uint4 htr[16];    // Htot row f = r (bf16)
             if (T.linear) {
@@ -621,8 +674,12 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 tf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t8[e]));
-                            o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
-                                              tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
+                            if (F8)
+                                o4[e] = pack_bf16(tf.x * ivs - __uint_as_float(hs[ch * 8 + 2 * e]) * hs_scale,
+                                                  tf.y * ivs - __uint_as_float(hs[ch * 8 + 2 * e + 1]) * hs_scale);
+                            else
+                                o4[e] = pack_bf16(tf.x - __uint_as_float(hs[ch * 8 + 2 * e]),
+                                                  tf.y - __uint_as_float(hs[ch * 8 + 2 * e + 1]));
                         }
                         st_shared_v4(hb + (c >> 6) * 16384 + sw128_off(r, c & 63), o4[0], o4[1], o4[2], o4[3]);
                     }
@@ -644,7 +701,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(&bar_v_empty[hcs]);  // the lin MMA has read Hc: the slot returns to the V ring
             }
             // out = alpha / l * O straight to global (row r: 256 contiguous bytes)
-            const float sc = alpha / l;
+            const float sc = F8 ? alpha / l * vs : alpha / l;
             uint4* orow = reinterpret_cast<uint4*>(p.out + grow * D);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -695,6 +752,7 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
     p.htot16 = (const __nv_bfloat16*)a.htot16;
     p.phiq = (const __nv_bfloat16*)a.phiq;
     p.out = (__nv_bfloat16*)a.out;
+    p.vamax = a.vamax;
     p.N = a.N;
     p.H = (int)a.H;
     p.tm = a.tm;
@@ -706,14 +764,102 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
     extern unsigned long long* g_trace_buf;
     p.trace = g_trace_buf;
 #endif
-    cudaError_t e = ensure_smem_attr((const void*)sla2_sparse_v2_kernel, (int)v2::SMEM_ALLOC);
+    const bool f8 = a.vamax != nullptr;
+    const void* fn = f8 ? (const void*)sla2_sparse_v2_kernel<true> : (const void*)sla2_sparse_v2_kernel<false>;
+    cudaError_t e = ensure_smem_attr(fn, (int)v2::SMEM_ALLOC);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = p.ntiles < sms ? p.ntiles : sms;
-    sla2_sparse_v2_kernel<<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v, *a.tm_phik, p);
+    if (f8)
+        sla2_sparse_v2_kernel<true><<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v8, *a.tm_phi8, p);
+    else
+        sla2_sparse_v2_kernel<false><<<grid, v2::NTHREADS, v2::SMEM_ALLOC, st>>>(*a.tm_q, *a.tm_k, *a.tm_v, *a.tm_phik, p);
     ++*launches;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ FP8 P/V operand preparation
+// (tolerance mode, not in the reference, which is INT8-only: quant.hpp:15-19). Per head one
+// scale for V: amax = max |V| over the head's N x d entries (fp32 bits, atomicMax on the
+// non-negative bit patterns), V8 = e4m3(V * 448 / amax); phi(K~) is a row softmax in (0, 1], so
+// phi8 = e4m3(448 phi) needs no scale. Both are [BH][N][128] E4M3, the sparse kernel's
+// 128-byte-wide TMA boxes.
+__device__ __forceinline__ float absmax8_bf16(uint4 w) {
+    float r = 0.0f;
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        r = fmaxf(r, fabsf(__uint_as_float(u[e] << 16)));
+        r = fmaxf(r, fabsf(__uint_as_float(u[e] & 0xFFFF0000u)));
+    }
+    return r;
+}
+__global__ void __launch_bounds__(256) v_absmax_kernel(const uint4* __restrict__ v, uint32_t* __restrict__ amax,
+                                                       int64_t per_head) {  // per_head: uint4 per head
+    const int64_t bh = blockIdx.y;
+    const uint4* src = v + bh * per_head;
+    float m = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < per_head; i += (int64_t)gridDim.x * 256)
+        m = fmaxf(m, absmax8_bf16(src[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, wm[w]);
+        atomicMax(amax + bh, __float_as_uint(m));
+    }
+}
+__device__ __forceinline__ uint2 e4m3x8(uint4 w, float s) {
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+    uint32_t r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t a = u[2 * h], b = u[2 * h + 1];
+        r[h] = pack_e4m3x2(__uint_as_float(a << 16) * s, __uint_as_float(a & 0xFFFF0000u) * s) |
+               (pack_e4m3x2(__uint_as_float(b << 16) * s, __uint_as_float(b & 0xFFFF0000u) * s) << 16);
+    }
+    return make_uint2(r[0], r[1]);
+}
+// dst = e4m3(src * scale), scale = 448 / amax[head] (amax non-null) or `cscale`
+__global__ void __launch_bounds__(256) e4m3_convert_kernel(const uint4* __restrict__ src, const uint32_t* __restrict__ amax,
+                                                           float cscale, uint2* __restrict__ dst, int64_t per_head,
+                                                           int64_t total) {
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (int64_t)gridDim.x * 256) {
+        float s = cscale;
+        if (amax) {
+            const float am = __uint_as_float(__ldg(amax + i / per_head));
+            s = am > 0.0f ? 448.0f / am : 1.0f;
+        }
+        dst[i] = e4m3x8(src[i], s);
+    }
+}
+
+// v non-null: amax = max |V| per head, then V8; phik non-null: phi8 = e4m3(448 phi(K~)).
+cudaError_t launch_fp8pv_prep(const void* v, const void* phik, uint8_t* v8, uint8_t* phi8, uint32_t* amax, int64_t BH,
+                              int64_t N, cudaStream_t st, int* launches) {
+    const int64_t per_head = N * 128 / 8;  // uint4 (8 bf16) per head
+    const int64_t total = BH * per_head;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    if (v) {
+        cudaError_t e = cudaMemsetAsync(amax, 0, BH * sizeof(uint32_t), st);
+        if (e != cudaSuccess) return e;
+        const int gx = (int)std::min<int64_t>((per_head + 2047) / 2048, std::max<int64_t>(1, (int64_t)sms * 8 / BH + 1));
+        v_absmax_kernel<<<dim3(gx, (unsigned)BH), 256, 0, st>>>((const uint4*)v, amax, per_head);
+        ++*launches;
+        e4m3_convert_kernel<<<grid, 256, 0, st>>>((const uint4*)v, amax, 1.0f, (uint2*)v8, per_head, total);
+        ++*launches;
+    }
+    if (phik) {
+        e4m3_convert_kernel<<<grid, 256, 0, st>>>((const uint4*)phik, nullptr, 448.0f, (uint2*)phi8, per_head, total);
+        ++*launches;
+    }
     return cudaGetLastError();
 }
 
