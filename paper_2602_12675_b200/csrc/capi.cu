@@ -278,11 +278,7 @@ size_t carve(const Geo& g, void* base, Workspace* w) {
     t.htot = c.take<float>(g.BH * g.d * g.d);
     t.htot16 = c.take<uint16_t>(g.BH * g.d * g.d);
     t.phiq = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
-#ifdef SLA2_FA_SPARSE
-    t.ol = g.bf16 ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;
-#else
     t.ol = (g.bf16 && g.quant) ? c.take<uint16_t>(g.BH * g.N * g.d) : nullptr;  // QAT: linear-branch O_l
-#endif
     if (g.fp8) {
         t.v8 = c.take<uint8_t>(g.BH * g.N * g.d);
         t.phi8 = c.take<uint8_t>(g.BH * g.N * g.d);
@@ -686,18 +682,6 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
                 SLA2_CUDA_TRY(launch_attn_i8(ia, &mphi, &mv, st, &g_launches));
             else
                 SLA2_CUDA_TRY(launch_sparse_i8(ia, st, &g_launches));
-#ifdef SLA2_V3  // experiment build: make variant NAME=v3 DEFS=-DSLA2_V3
-        } else if (sparse_v3_eligible(sa)) {
-            SLA2_CUDA_TRY(launch_sparse_v3(sa, st, &g_launches));
-#endif
-#ifdef SLA2_FA_SPARSE  // experiment build: the split linear-branch + two-lane attention forward
-        } else if (sparse_fa_eligible(sa)) {
-            SLA2_CUDA_TRY(launch_sparse_fa(sa, st, &g_launches));
-#endif
-#ifdef SLA2_V4  // experiment build until measured: make variant NAME=v4 DEFS=-DSLA2_V4
-        } else if (sparse_v4_eligible(sa)) {
-            SLA2_CUDA_TRY(launch_sparse_v4(sa, st, &g_launches));
-#endif
         } else if (g.fp8) {
             // FP8 P/V (tolerance mode): the persistent kernel with E4M3 P, V and phi(K~)
             CUtensorMap mv8, mphi8;

@@ -143,12 +143,6 @@ cudaError_t launch_sparse_v2(const SparseLaunch& a, cudaStream_t st, int* launch
 // FP8 P/V operands: amax[bh] = max |V|, v8 = e4m3(V * 448 / amax), phi8 = e4m3(448 phi(K~)) (bf16 in)
 cudaError_t launch_fp8pv_prep(const void* v, const void* phik, uint8_t* v8, uint8_t* phi8, uint32_t* amax, int64_t BH,
                               int64_t N, cudaStream_t st, int* launches);
-// persistent variant with 8 softmax warps and double-buffered S (sparse_v3.cu)
-bool sparse_v3_eligible(const SparseLaunch& a);
-// persistent variant with 64-key steps, two S buffers and two O accumulators (sparse_v4.cu)
-bool sparse_v4_eligible(const SparseLaunch& a);
-cudaError_t launch_sparse_v4(const SparseLaunch& a, cudaStream_t st, int* launches);
-cudaError_t launch_sparse_v3(const SparseLaunch& a, cudaStream_t st, int* launches);
 // split forward (sparse_fa.cu): linear-branch kernel (O_l) + two-query-block attention kernel;
 // also the dense mode (full_attention)
 bool sparse_fa_eligible(const SparseLaunch& a);
