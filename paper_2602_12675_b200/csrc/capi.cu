@@ -490,6 +490,33 @@ struct LinPlan {
     std::function<sla2_status(cudaStream_t)> between;
 };
 
+// QuantLaunch of the forward's QAT operands (quant_prep_kernel; `which` picks Q / K~ / V).
+static QuantLaunch quant_launch(const sla2_fwd_params* p, const Geo& g, const Workspace& w, const void* q,
+                                const void* k, const void* v, int which) {
+    QuantLaunch qa{};
+    qa.B = g.B;
+    qa.H = g.H;
+    qa.N = (int)g.N;
+    qa.d = (int)g.d;
+    qa.bq = (int)g.bq;
+    qa.bk = (int)g.bk;
+    qa.tm = (int)g.tm;
+    qa.tn = (int)g.tn;
+    qa.q = q;
+    qa.k = k;
+    qa.v = v;
+    qa.mu = w.mu;
+    qa.smooth = p->smooth;
+    qa.qc = w.qc;
+    qa.qs = w.qs;
+    qa.kc = w.kc;
+    qa.ks = w.ks;
+    qa.vct = w.vct;
+    qa.vs = w.vs;
+    qa.which = which;
+    return qa;
+}
+
 // Linear-branch precompute then the sparse kernel.
 static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g, const Workspace& w, const void* q,
                                          const void* k, const void* v, const float* rho, const int32_t* idx,
@@ -537,6 +564,17 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         la.phik_ready = !(la.tm_k && la.mu);  // the fused kernel computes phi(K~) itself
         SLA2_CUDA_TRY(cudaEventRecord(ev_k, st));
         dep = ev_k;
+    }
+    cudaEvent_t kc_ready = nullptr;  // QAT: the K~ codes were made on the side stream
+    if (dep && g.quant && plan.qv_codes) {
+        // the K~ codes need only mu: on the QAT side stream (after its Q / V codes), beside the
+        // router's key side, instead of serially between the router and the attention kernels
+        cudaStream_t qs = aux_stream(3, -1);
+        kc_ready = aux_event(18);
+        SLA2_CUDA_TRY(cudaStreamWaitEvent(qs, dep, 0));
+        const QuantLaunch qk = quant_launch(p, g, w, q, k, v, 2);
+        SLA2_CUDA_TRY(launch_quant_prep(qk, qs, &g_launches));
+        SLA2_CUDA_TRY(cudaEventRecord(kc_ready, qs));
     }
     if (dep) {
         // lowest priority (the default level): the router's key side below runs above it
@@ -631,32 +669,13 @@ static sla2_status run_linear_and_sparse(const sla2_fwd_params* p, const Geo& g,
         sa.ol = w.ol;
         if (g.quant) {
             // INT8 QAT (QuantConfig, quant.hpp:15-19): per-tile codes + scales, then the kind::i8 kernel
-            QuantLaunch qa{};
-            qa.B = g.B;
-            qa.H = g.H;
-            qa.N = (int)g.N;
-            qa.d = (int)g.d;
-            qa.bq = (int)g.bq;
-            qa.bk = (int)g.bk;
-            qa.tm = (int)g.tm;
-            qa.tn = (int)g.tn;
-            qa.q = q;
-            qa.k = k;
-            qa.v = v;
-            qa.mu = w.mu;
-            qa.smooth = p->smooth;
-            qa.qc = w.qc;
-            qa.qs = w.qs;
-            qa.kc = w.kc;
-            qa.ks = w.ks;
-            qa.vct = w.vct;
-            qa.vs = w.vs;
-            if (plan.qv_codes) {  // Q / V codes are being made beside the router: K~ codes (need mu) only
-                qa.which = 2;
-                SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+            if (kc_ready) {  // every code was made on the side stream
+                SLA2_CUDA_TRY(cudaStreamWaitEvent(st, kc_ready, 0));
+            } else if (plan.qv_codes) {  // Q / V codes are being made beside the router: K~ codes (need mu) only
+                SLA2_CUDA_TRY(launch_quant_prep(quant_launch(p, g, w, q, k, v, 2), st, &g_launches));
                 SLA2_CUDA_TRY(cudaStreamWaitEvent(st, plan.qv_codes, 0));
             } else {
-                SLA2_CUDA_TRY(launch_quant_prep(qa, st, &g_launches));
+                SLA2_CUDA_TRY(launch_quant_prep(quant_launch(p, g, w, q, k, v, 1 | 2 | 4), st, &g_launches));
             }
             // the INT8 kernel addresses its bf16 tiles with 2-D [B*H*N][d] maps (N divisible)
             CUtensorMap mq2, mv2, mphi2;
