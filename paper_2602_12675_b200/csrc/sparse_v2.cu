@@ -299,22 +299,27 @@ __global__ void __launch_bounds__(384, 1)
             int64_t gv = 0;
             for (int t = blockIdx.x; t < nt; t += G) {
                 const V2Tile T = v2_tile(p, t);
-                for (int j = 0; j <= T.nb; ++j, ++gv) {
+                // FP8: one slot per key-block PAIR (V8 | phi8 of block 2n at 0 / 8 KB, of 2n+1 at
+                // 16 / 24 KB), so the ring holds twice the blocks in flight; bf16: one per block
+                const int nslot = F8 ? T.npair : T.nb;
+                for (int j = 0; j <= nslot; ++j, ++gv) {
                     const int s = (int)(gv % NSV);
+                    const int cnt = F8 ? min(2, T.nb - 2 * j) : 1;
                     if (lane == 0) {
                         if (gv >= NSV) V2_WAIT(&bar_v_empty[s], (uint32_t)(((gv / NSV) - 1) & 1));
-                        if (j == T.nb)  // the Hc slot: allocated, not loaded
+                        if (j == nslot)  // the Hc slot: allocated, not loaded
                             mbar_arrive(&bar_v_full[s]);
                         else if (F8)
-                            mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE8_BYTES : TILE8_BYTES);
+                            mbar_arrive_expect_tx(&bar_v_full[s], cnt * (T.linear ? 2 * TILE8_BYTES : TILE8_BYTES));
                         else
                             mbar_arrive_expect_tx(&bar_v_full[s], T.linear ? 2 * TILE_BYTES : TILE_BYTES);
                     }
                     __syncwarp();
-                    if (F8) {  // one 128-byte-wide box per tensor: V8 at the slot, phi8 TILE_BYTES in
-                        if (j < T.nb && lane < (T.linear ? 2 : 1))
-                            tma_load_3d_hint(sV(s) + lane * TILE_BYTES, lane == 0 ? &tmV : &tmPhi, 0, T.idx[j] * BK,
-                                             (int)T.bh, &bar_v_full[s], pol);
+                    if (F8) {  // one 128-byte-wide box per (block b, tensor t): lane = 2 b + t
+                        const int b = lane >> 1, tt = lane & 1;
+                        if (j < nslot && b < cnt && (tt == 0 || T.linear))
+                            tma_load_3d_hint(sV(s) + b * TILE_BYTES + tt * TILE8_BYTES, tt == 0 ? &tmV : &tmPhi, 0,
+                                             T.idx[2 * j + b] * BK, (int)T.bh, &bar_v_full[s], pol);
                     } else if (j < T.nb && lane < (T.linear ? 4 : 2)) {  // lane = (tensor V / phi, 64-column half)
                         const int krow = T.idx[j] * BK, hz = (int)T.bh, c = lane & 1;
                         tma_load_3d_hint(sV(s) + (lane >> 1) * TILE_BYTES + c * 8192, lane < 2 ? &tmV : &tmPhi, c * 64, krow,
@@ -368,12 +373,19 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     if (lane == 0 && n < 8) V2_TR(k, 25 + (n < 2 ? n : 2));
                     const int j0 = 2 * n, j1 = min(nbu, j0 + 2);
-                    for (int j = j0; j < j1; ++j) {
-                        const int v = gv + j;
-                        const int sv = v % NSV;
-                        V2_WAIT(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
+                    if (F8) {  // the pair's slot
+                        const int v = gv + n;
+                        V2_WAIT(&bar_v_full[v % NSV], (uint32_t)((v / NSV) & 1));
                         tc_fence_after();
-                        const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
+                    }
+                    for (int j = j0; j < j1; ++j) {
+                        const int v = F8 ? gv + n : gv + j;
+                        const int sv = v % NSV;
+                        if (!F8) {
+                            V2_WAIT(&bar_v_full[sv], (uint32_t)((v / NSV) & 1));
+                            tc_fence_after();
+                        }
+                        const uint64_t dV = dVm + ((sv * VS_BYTES + (F8 ? (j & 1) * TILE_BYTES : 0)) >> 4);
                         if (F8) {  // P: 4 e4m3 per TMEM column (16 per key block); V8 MN-major, 32 keys per MMA
                             const uint32_t aP = tm + TM_P + (uint32_t)((gg & 1) * 64 + (j & 1) * 16);
 #pragma unroll
@@ -388,10 +400,10 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     umma_commit_w(&bar_pv_done[gg & 1]);
                     for (int j = j0; j < j1; ++j) {
-                        const int sv = (int)((gv + j) % NSV);
+                        const int sv = (int)((F8 ? gv + n : gv + j) % NSV);
                         if (lin) {
-                            const uint64_t dV = dVm + ((sv * VS_BYTES) >> 4);
-                            const uint64_t dP = dV + (TILE_BYTES >> 4);
+                            const uint64_t dV = dVm + ((sv * VS_BYTES + (F8 ? (j & 1) * TILE_BYTES : 0)) >> 4);
+                            const uint64_t dP = dV + ((F8 ? TILE8_BYTES : TILE_BYTES) >> 4);
                             if (F8) {
 #pragma unroll
                                 for (int ks = 0; ks < 2; ++ks)
@@ -404,13 +416,13 @@ __global__ void __launch_bounds__(384, 1)
                                                    (j > 0 || ks > 0));
                             }
                         }
-                        umma_commit_w(&bar_v_empty[sv]);
+                        if (!F8 || j == j1 - 1) umma_commit_w(&bar_v_empty[sv]);  // FP8: once per pair slot
                     }
                 }
                 umma_commit_w(&bar_tile_done);
                 if (lane == 0) V2_TR(k, 28);
                 g += npu;
-                gv += nbu;
+                gv += F8 ? npu : nbu;
                 prev_hc = gv % NSV;  // the tile's Hc slot
                 gv += 1;
                 prev_linear = lin;
@@ -595,7 +607,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int t = blockIdx.x; t < nt; t += G, ++k) {
             const V2Tile T = v2_tile(p, t);
             const int pb = k & 1;
-            const int vhc = gv + T.nb;  // the tile's Hc slot
+            const int vhc = gv + (F8 ? T.npair : T.nb);  // the tile's Hc slot
             const int hcs = vhc % NSV;
             gv = vhc + 1;
             const int64_t grow = T.bh * (int64_t)p.N + (int64_t)T.i * BQ + r;
