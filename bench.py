@@ -57,6 +57,8 @@ CONFIGS = {
     # unquantized reference; the output bar is the FP8 one (1e-1 max normwise, tests/test_gpu_fp8.py)
     "cfg3fp8": dict(workload="wan2.1-1.3B-480p attention, FP8 P/V low-bit mode (BASELINE configs[2])", B=1, H=12,
                     N=32760, d=128, bq=128, bk=64, k_percent=3.0, bf16=True, quant="fp8"),
+    "cfg4fp8": dict(workload="wan2.1-14B-720p attention, FP8 P/V low-bit mode", B=1, H=40, N=75600, d=128,
+                    bq=128, bk=64, k_percent=3.0, bf16=True, quant="fp8"),
     "cfg4": dict(workload="wan2.1-14B-720p attention (BASELINE configs[3])", B=1, H=40, N=75600, d=128, bq=128,
                  bk=64, k_percent=3.0, bf16=True, quant=False),
     "cfg1": dict(workload="fp32 CPU-oracle case (BASELINE configs[0])", B=1, H=2, N=4096, d=64, bq=64, bk=64,
