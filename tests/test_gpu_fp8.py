@@ -46,7 +46,11 @@ def _run(cuda, q, k, v, pq, pk, rho, kp, quant):
 @pytest.mark.gpu
 @pytest.mark.parametrize("N,H,kp,seed,vscale", [(4096, 2, 3.0, 301, 1.0), (8192, 2, 10.0, 302, 1.0),
                                                 (2048, 1, 50.0, 303, 1.0), (8200, 2, 3.0, 304, 1.0),
-                                                (4096, 1, 3.0, 305, 37.0), (4096, 1, 3.0, 306, 1e-3)])
+                                                (4096, 1, 3.0, 305, 37.0), (4096, 1, 3.0, 306, 1e-3),
+                                                # odd kappa (a single-block last pair: 3 of 64 blocks,
+                                                # 9 of 128) and kappa = tn (no linear branch)
+                                                (4096, 1, 5.0, 307, 1.0), (8192, 1, 7.0, 308, 1.0),
+                                                (4096, 1, 100.0, 309, 1.0)])
 def test_fp8pv_vs_reference(cuda, N, H, kp, seed, vscale):
     """Masks bit-exact (same router as the bf16 path) and out within the FP8 bar of the
     reference's unquantized forward, including ragged N and V far from unit scale."""
