@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """SLA2 forward benchmark (BASELINE.json metric) on 1..8 B200s.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1|cfg2|cfg2pad|cfg3|cfg4|cfg5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1|cfg2|cfg2pad|cfg3|cfg3fp8|cfg4|cfg4fp8|cfg5|cfg5fp8]
                   [--impl b200|reference] [--scaling weak|strong]
 
 A step is one full SLA2 forward (router + linear precompute + sparse/linear/blend kernel) over
@@ -64,6 +64,8 @@ CONFIGS = {
     "cfg1": dict(workload="fp32 CPU-oracle case (BASELINE configs[0])", B=1, H=2, N=4096, d=64, bq=64, bk=64,
                  k_percent=10.0, bf16=False, quant=False),
     # configs[4]: the sweep (H = 12, the 1.3B model's heads); see sweep()
+    "cfg5fp8": dict(workload="the configs[4] sweep in the FP8 P/V low-bit mode", B=1, H=12, N=32768, d=128, bq=128,
+                    bk=64, k_percent=3.0, bf16=True, quant="fp8"),
     "cfg5": dict(workload="sparsity {80,85,90,95,97}% x N {8K..128K} vs dense (BASELINE configs[4])", B=1, H=12,
                  N=32768, d=128, bq=128, bk=64, k_percent=3.0, bf16=True, quant=False),
 }
@@ -257,14 +259,14 @@ def parity_block(c, masks_all, outs, dev, seed_base, dtype):
 
 
 # ------------------------------------------------------------------------------ cfg5 sweep
-def sweep(args, dev):
+def sweep(args, dev, name="cfg5"):
     """BASELINE configs[4]: SLA2 forward (graph replay) vs the dense tcgen05 kernel of the same
     build and cuDNN SDPA, over sparsity x N, H = 12, bf16."""
     import torch
     import torch.nn.functional as F
     import paper_2602_12675_b200 as sla2
     from paper_2602_12675_b200 import dist as sd
-    base = CONFIGS["cfg5"]
+    base = CONFIGS[name]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     points = []
     for N in SWEEP_N:
@@ -276,7 +278,7 @@ def sweep(args, dev):
         sdpa_ms = time_events(lambda: F.scaled_dot_product_attention(q, k, v), 3, flush)
         for sp in SWEEP_SPARSITY:
             kp = 100.0 - sp
-            kw = dict(k_percent=kp, bq=c["bq"], bk=c["bk"])
+            kw = dict(k_percent=kp, bq=c["bq"], bk=c["bk"], quant=c["quant"])
             g = sla2.CapturedForward(q, k, v, pq, pk, rho, **kw)
             for _ in range(max(args.warmup, 3)):
                 g()
@@ -356,9 +358,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    if cfg_name == "cfg5":
+    if cfg_name in ("cfg5", "cfg5fp8"):
         if rank == 0:
-            pts = sweep(args, dev)
+            pts = sweep(args, dev, cfg_name)
             at = next(p for p in pts if p["N"] == 32768 and p["sparsity_pct"] == 97)
             print(json.dumps({"metric": METRIC, "value": at["sla2_tflops"], "unit": "TFLOPS", "n_gpus": 1,
                               "steps": args.steps, "warmup": args.warmup, "ms_per_step": at["sla2_ms"],
