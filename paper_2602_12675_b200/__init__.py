@@ -272,7 +272,9 @@ def forward(q, k, v, proj_q, proj_k, rho, *, k_percent=3.0, bq=128, bk=64, quant
     """Router + blockwise forward (tape.hpp:263-272). Returns out or a tuple with
     (mask [B,H,tm,tn] u8, idx [B,H,tm,kappa] i32, saved dict) as requested; saved=True gives
     o_s, o_l, big_l, saved="full" all of SLA2ForwardSaved (+ the QAT S hook). `workspace` (a
-    uint8 CUDA tensor of at least workspace_bytes(...)) replaces the shared per-device cache."""
+    uint8 CUDA tensor of at least workspace_bytes(...)) replaces the shared per-device cache.
+    quant: False / "none"; True / "int8" (the reference's QuantConfig, exact codes); "fp8" (E4M3
+    P / V on kind::f8f6f4, out only, tolerance per DESIGN.md 4.2; not a reference mode)."""
     import torch
     _check_like(q, k, v)
     p = _params_from(q, bq, bk, k_percent, quant, smooth, exact_mu)
